@@ -1,0 +1,64 @@
+"""K-rank synchronous data parallelism and model averaging (ORACLE — test infrastructure only).
+
+WASSP-SGD phase 1: every rank computes the gradient of
+its own minibatch on the same snapshot (dropout streams include the rank), the K gradients
+are summed (the allreduce), and every rank applies Eq. 1 with grad_scale = 1/K and the
+learning rate of the "gradual warmup and linear scaling rule" (DESIGN
+reading 20).  Eq. 2 model averaging for identical supports is the plain
+mean of (w, b).  The paper's CPU parameter server itself is prior art (BASELINE.json
+north_star), so it is not modelled here.
+"""
+from __future__ import annotations
+
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+from .model import F32, F64, Grads, State, backward, forward, step
+
+
+def scaled_lr(base_lr: float, K: int, step_idx: int, warmup_steps: int) -> float:
+    """eta_t = eta * (1 + (K - 1) * min(1, t / warmup)): linear scaling with gradual warmup."""
+    if K <= 1:
+        return base_lr
+    frac = 1.0 if warmup_steps <= 0 else min(1.0, step_idx / float(warmup_steps))
+    return base_lr * (1.0 + (K - 1) * frac)
+
+
+def allreduce_sum(grads: Sequence[Grads]) -> Grads:
+    """SUM over ranks of every gradient value (float64 sum, one rounding to float32)."""
+    K = len(grads)
+    g = [np.sum([gr.g[i].astype(F64) for gr in grads], axis=0).astype(F32) for i in range(len(grads[0].g))]
+    gb = [np.sum([gr.gb[i].astype(F64) for gr in grads], axis=0).astype(F32) for i in range(len(grads[0].gb))]
+    return Grads(g, gb, float(np.mean([gr.loss for gr in grads])), [None] * len(grads[0].deltas))
+
+
+def dp_step(st: State, batches: Sequence[Tuple[np.ndarray, np.ndarray]], lr: float,
+            momentum: float, weight_decay: float, step_idx: int) -> float:
+    """One synchronous step of K = len(batches) replicas sharing ``st`` (identical topology).
+    Returns the mean loss over ranks."""
+    K = len(batches)
+    grads = []
+    for k, (x, y) in enumerate(batches):
+        tr = forward(st, x, True, step_idx, rank=k)
+        grads.append(backward(st, tr, y))
+    total = allreduce_sum(grads)
+    step(st, total, lr, momentum, weight_decay, grad_scale=1.0 / K)
+    return total.loss
+
+
+def average(states: List[State]) -> None:
+    """Eq. 2: theta_f = (1/K) sum_i theta_i over (w, b) of replicas with identical supports
+    (the union-and-re-sparsify form is SURVEY §8(f) item 1).  Momentum stays local.
+    Modifies every state in place."""
+    K = len(states)
+    for s in states[1:]:
+        for a, b in zip(states[0].layers, s.layers):
+            if not (np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col, b.col)):
+                raise ValueError("averaging requires identical supports")
+    for idx in range(len(states[0].layers)):
+        w = (np.sum([s.layers[idx].w.astype(F64) for s in states], axis=0) / K).astype(F32)
+        b = (np.sum([s.b[idx].astype(F64) for s in states], axis=0) / K).astype(F32)
+        for s in states:
+            s.layers[idx].w = w.copy()
+            s.b[idx] = b.copy()

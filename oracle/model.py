@@ -1,0 +1,385 @@
+"""Sparse MLP state, ER initialisation, forward, loss, backward and update (ORACLE — test
+infrastructure only; see oracle/__init__.py).
+
+Notation follows the paper: neuron layers l = 1..L with the input at l = 1;
+weight matrix W^(l) connects layer l-1 to layer l and has shape n_{l-1} x n_l, w_ij = 0
+meaning "no connection".  W^(l) is stored as CSR by input row i with sorted,
+unique columns (the paper orientation), aligned momentum v, dense biases b_l.
+
+Every stored tensor is float32 ("32-bit float precision") computed in float64
+and rounded once.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import philox
+
+F32 = np.float32
+F64 = np.float64
+
+
+# --------------------------------------------------------------------------------------
+# state
+# --------------------------------------------------------------------------------------
+@dataclass
+class Layer:
+    """Weight layer W^(l), CSR by input neuron i."""
+    l: int
+    n_in: int
+    n_out: int
+    row_ptr: np.ndarray      # int64 [n_in + 1]
+    col: np.ndarray          # int32 [nnz], sorted unique within each row
+    w: np.ndarray            # float32 [nnz]
+    v: np.ndarray            # float32 [nnz] momentum (Eq. 1 history)
+    dense_capped: bool = False
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col.shape[0])
+
+    def rows(self) -> np.ndarray:
+        return np.repeat(np.arange(self.n_in, dtype=np.int64), np.diff(self.row_ptr))
+
+    def keys(self) -> np.ndarray:
+        """Linear positions i * n_out + j (ascending in canonical order)."""
+        return self.rows() * self.n_out + self.col.astype(np.int64)
+
+    def dense(self, dtype=F64) -> np.ndarray:
+        D = np.zeros((self.n_in, self.n_out), dtype=dtype)
+        D[self.rows(), self.col] = self.w
+        return D
+
+    def copy(self) -> "Layer":
+        return Layer(self.l, self.n_in, self.n_out, self.row_ptr.copy(), self.col.copy(),
+                     self.w.copy(), self.v.copy(), self.dense_capped)
+
+
+@dataclass
+class State:
+    sizes: List[int]
+    epsilon: float
+    activation: str          # "all_relu" | "relu"
+    alpha: float
+    dropout: float
+    init: str                # "normal" | "xavier" | "he_uniform"
+    seed: int
+    rank: int
+    layers: List[Layer]      # layers[l-2] = W^(l), l = 2..L
+    b: List[np.ndarray]      # b[l-2] = bias of neuron layer l
+    vb: List[np.ndarray]     # bias momentum
+    alive: List[np.ndarray]  # alive[l-1] = uint8 liveness of neuron layer l (l = 1..L)
+    version: int = 0
+
+    @property
+    def L(self) -> int:
+        return len(self.sizes)
+
+    def layer(self, l: int) -> Layer:
+        return self.layers[l - 2]
+
+    def copy(self) -> "State":
+        return State(list(self.sizes), self.epsilon, self.activation, self.alpha, self.dropout,
+                     self.init, self.seed, self.rank, [x.copy() for x in self.layers],
+                     [x.copy() for x in self.b], [x.copy() for x in self.vb],
+                     [x.copy() for x in self.alive], self.version)
+
+
+# --------------------------------------------------------------------------------------
+# Erdos-Renyi initialisation (Alg. 2)
+# --------------------------------------------------------------------------------------
+def er_count(n_in: int, n_out: int, epsilon: float) -> int:
+    """M = min(n_in * n_out, floor(eps * (n_in + n_out))): the ER density
+    eps(n_in+n_out)/(n_in n_out) of BASELINE.json north_star, capped at 1 (DESIGN reading 1)."""
+    return int(min(n_in * n_out, math.floor(epsilon * (n_in + n_out))))
+
+
+def candidate_ij(x0: np.ndarray, x1: np.ndarray, n_in: int, n_out: int):
+    """Map two uniform 32-bit words to a position: i = floor(x0 * n_in / 2^32), j likewise."""
+    i = (x0.astype(np.uint64) * np.uint64(n_in)) >> np.uint64(32)
+    j = (x1.astype(np.uint64) * np.uint64(n_out)) >> np.uint64(32)
+    return i.astype(np.int64), j.astype(np.int64)
+
+
+def init_values(init: str, n_in: int, n_out: int, x2: np.ndarray, x3: np.ndarray) -> np.ndarray:
+    """Initial / regrown weight values (Table 5 scheme names; DESIGN reading 3).
+
+    he_uniform: U(-lim, lim), lim = sqrt(6 / n_in); xavier: lim = sqrt(6 / (n_in + n_out)).
+      u = (x2 >> 8) * 2^-24 in [0, 1); value = fp32((2u - 1) * lim)  (all steps exact but the last).
+    normal: N(0, 2 / n_in) by Box-Muller on (x2, x3), in float64, rounded to fp32."""
+    if init in ("he_uniform", "xavier"):
+        lim64 = math.sqrt(6.0 / n_in) if init == "he_uniform" else math.sqrt(6.0 / (n_in + n_out))
+        lim = F32(lim64)
+        u = (x2 >> np.uint32(8)).astype(F32) * F32(2.0 ** -24)
+        t = u * F32(2.0) - F32(1.0)
+        return (t * lim).astype(F32)
+    if init == "normal":
+        u1 = ((x2 >> np.uint32(8)).astype(F64) + 1.0) * (2.0 ** -24)
+        u2 = (x3 >> np.uint32(8)).astype(F64) * (2.0 ** -24)
+        r = np.sqrt(-2.0 * np.log(u1))
+        c = np.cos((2.0 * math.pi) * u2)
+        std = math.sqrt(2.0 / n_in)
+        return ((r * c) * std).astype(F32)
+    raise ValueError(f"unknown init scheme {init!r}")
+
+
+def er_layer(n_in: int, n_out: int, epsilon: float, init: str, seed: int, l: int) -> Layer:
+    """G(n, M) Erdos-Renyi layer: the first M distinct positions of the INIT candidate
+    stream (DESIGN reading 2), values from the accepting candidate's words (x2, x3).
+    A dense-capped layer (M = n_in n_out) takes every position; its values come from
+    the INIT_DENSE stream at index = linear position."""
+    total = n_in * n_out
+    M = er_count(n_in, n_out, epsilon)
+    if M == total:
+        pos = np.arange(total, dtype=np.int64)
+        x0, x1, x2, x3 = philox.stream(seed, philox.PURPOSE_INIT_DENSE, 0, l, 0, pos.astype(np.uint64))
+        w = init_values(init, n_in, n_out, x2, x3)
+        row_ptr = np.arange(n_in + 1, dtype=np.int64) * n_out
+        col = np.tile(np.arange(n_out, dtype=np.int32), n_in)
+        return Layer(l, n_in, n_out, row_ptr, col, w, np.zeros(total, F32), True)
+    C = M + M // 8 + 1024
+    while True:
+        m = np.arange(C, dtype=np.uint64)
+        x0, x1, x2, x3 = philox.stream(seed, philox.PURPOSE_INIT, 0, l, 0, m)
+        i, j = candidate_ij(x0, x1, n_in, n_out)
+        pos = i * n_out + j
+        _, first = np.unique(pos, return_index=True)      # first occurrence of every distinct pos
+        if len(first) >= M:
+            break
+        C *= 2
+    acc = np.sort(first)[:M]                                # the first M distinct, in stream order
+    w_acc = init_values(init, n_in, n_out, x2[acc], x3[acc])
+    p_acc = pos[acc]
+    order = np.argsort(p_acc, kind="stable")
+    p_sorted = p_acc[order]
+    rows = p_sorted // n_out
+    col = (p_sorted % n_out).astype(np.int32)
+    row_ptr = np.zeros(n_in + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n_in), out=row_ptr[1:])
+    return Layer(l, n_in, n_out, row_ptr, col, w_acc[order], np.zeros(M, F32), False)
+
+
+def create(sizes, epsilon, activation="all_relu", alpha=0.5, dropout=0.0, init="he_uniform",
+           seed=0, rank=0) -> State:
+    """sparse_mlp_create: ER init of every weight layer, zero momentum and biases, version 0."""
+    sizes = [int(s) for s in sizes]
+    if len(sizes) < 3 or min(sizes) < 1 or not epsilon > 0 or alpha < 0 or not (0 <= dropout < 1):
+        raise ValueError("invalid configuration")
+    layers, b, vb = [], [], []
+    for l in range(2, len(sizes) + 1):
+        layers.append(er_layer(sizes[l - 2], sizes[l - 1], epsilon, init, seed, l))
+        b.append(np.zeros(sizes[l - 1], F32))
+        vb.append(np.zeros(sizes[l - 1], F32))
+    alive = [np.ones(n, np.uint8) for n in sizes]
+    return State(sizes, float(epsilon), activation, float(alpha), float(dropout), init,
+                 int(seed), int(rank), layers, b, vb, alive, 0)
+
+
+# --------------------------------------------------------------------------------------
+# sparse products (fp64 accumulation, chunked so large layers fit in memory)
+# --------------------------------------------------------------------------------------
+_CHUNK_ELEMS = 1 << 24
+
+
+def _csr64(Ly: Layer, wabs: bool = False):
+    """W^(l) as a SciPy float64 CSR matrix [n_in x n_out] (library sparse container)."""
+    w = np.abs(Ly.w) if wabs else Ly.w
+    return sp.csr_matrix((w.astype(F64), Ly.col.astype(np.int64), Ly.row_ptr.astype(np.int64)),
+                         shape=(Ly.n_in, Ly.n_out))
+
+
+def spmm_fwd(a: np.ndarray, Ly: Layer, wabs: bool = False) -> np.ndarray:
+    """z = a . W^(l)  ([B x n_in] x [n_in x n_out]) in float64, summing over the support only
+    (W zero-filled off the support: PAPER.md:51).  Library sparse matmul as the step."""
+    src = np.abs(a) if wabs else a
+    W = _csr64(Ly, wabs)
+    return np.asarray((W.T @ src.astype(F64).T).T)
+
+
+def spmm_bwd(delta: np.ndarray, Ly: Layer) -> np.ndarray:
+    """delta . W^(l)^T  ([B x n_out] x [n_out x n_in]) in float64 over the support only."""
+    W = _csr64(Ly)
+    return np.asarray((W @ delta.astype(F64).T).T)
+
+
+def sddmm(a: np.ndarray, delta: np.ndarray, Ly: Layer) -> np.ndarray:
+    """g_ij = sum_b a[b, i] delta[b, j] for (i, j) in the support only (fp64)."""
+    rows = Ly.rows()
+    col = Ly.col.astype(np.int64)
+    g = np.zeros(Ly.nnz, dtype=F64)
+    B = a.shape[0]
+    step = max(1, _CHUNK_ELEMS // max(B, 1))
+    for s0 in range(0, Ly.nnz, step):
+        s1 = min(Ly.nnz, s0 + step)
+        g[s0:s1] = (a[:, rows[s0:s1]].astype(F64) * delta[:, col[s0:s1]].astype(F64)).sum(axis=0)
+    return g
+
+
+# --------------------------------------------------------------------------------------
+# activations (Eq. 3 All-ReLU PAPER.md:106-112; Eq. 5 ReLU PAPER.md:533-539)
+# --------------------------------------------------------------------------------------
+def neg_slope(st_or_act, alpha: float, l: int) -> float:
+    """Slope of f_l for x <= 0: -alpha for even l, +alpha for odd l (All-ReLU); 0 for ReLU."""
+    act = st_or_act.activation if hasattr(st_or_act, "activation") else st_or_act
+    if act == "relu":
+        return 0.0
+    return -alpha if l % 2 == 0 else alpha
+
+
+def activation(x, l: int, alpha: float, act: str = "all_relu"):
+    s = neg_slope(act, alpha, l)
+    x = np.asarray(x, dtype=F64)
+    return np.where(x > 0, x, s * x)
+
+
+def activation_grad(x, l: int, alpha: float, act: str = "all_relu"):
+    """f_l'(x): 1 for x > 0, the negative-side slope for x <= 0 (x = 0 takes the x <= 0
+    branch of Eq. 3 literally)."""
+    s = neg_slope(act, alpha, l)
+    x = np.asarray(x, dtype=F64)
+    return np.where(x > 0, 1.0, s)
+
+
+def dropout_keep(seed: int, rank: int, l: int, step: int, B: int, n: int, rate: float) -> np.ndarray:
+    """Inverted-dropout keep mask [B x n] of hidden layer l (PAPER.md:957 rate; DESIGN reading 13):
+    element (b, j) -> e = b * n + j, word (e & 3) of Philox(DROPOUT, idx = e >> 2, c3 = step);
+    kept iff word >= floor(rate * 2^32)."""
+    if rate <= 0.0:
+        return np.ones((B, n), dtype=bool)
+    e = np.arange(B * n, dtype=np.uint64)
+    words = philox.stream(seed, philox.PURPOSE_DROPOUT, rank, l, step & 0xFFFFFFFF, e >> np.uint64(2))
+    W = np.stack(words, axis=0)                          # [4, B*n]
+    word = W[(e & np.uint64(3)).astype(np.int64), np.arange(B * n)]
+    thr = np.uint64(math.floor(rate * 4294967296.0))
+    return (word.astype(np.uint64) >= thr).reshape(B, n)
+
+
+# --------------------------------------------------------------------------------------
+# forward / loss / backward / update
+# --------------------------------------------------------------------------------------
+@dataclass
+class Trace:
+    B: int
+    train: bool
+    step: int
+    version: int
+    a: List[np.ndarray]                # a[l-1] = float32 activations of layer l (a[0] = x)
+    z: List[Optional[np.ndarray]]      # z[l-1] = float64 pre-activations (None for l = 1)
+    keep: List[Optional[np.ndarray]]   # dropout keep masks of hidden layers
+    p: np.ndarray                      # float32 softmax probabilities [B x n_L]
+    p64: np.ndarray
+    ambiguous: List[int]               # per layer: #elements with |z| within fp32 rounding of 0
+
+
+def forward(st: State, x: np.ndarray, train: bool = True, step: int = 0, rank: Optional[int] = None) -> Trace:
+    """sparse_mlp_forward: z_l = a_{l-1} W^(l) + b_l, a_l = f_l(z_l) (Eq. 3) then inverted dropout
+    in train mode (hidden layers only); p = softmax(z_L) computed stably."""
+    rank = st.rank if rank is None else rank
+    x = np.asarray(x, dtype=F32)
+    B = x.shape[0]
+    a = [x]
+    zs: List[Optional[np.ndarray]] = [None]
+    keeps: List[Optional[np.ndarray]] = [None]
+    amb = [0]
+    L = st.L
+    scale = 1.0 / (1.0 - st.dropout) if st.dropout > 0 else 1.0
+    for l in range(2, L + 1):
+        Ly = st.layer(l)
+        z = spmm_fwd(a[-1], Ly) + st.b[l - 2].astype(F64)
+        mag = spmm_fwd(a[-1], Ly, wabs=True) + np.abs(st.b[l - 2].astype(F64))
+        # pre-activations within fp32 summation error of the All-ReLU kink (hidden layers):
+        # there the branch taken by an fp32 kernel may legitimately differ (DESIGN: kink guard)
+        amb.append(int(np.count_nonzero(np.abs(z) <= mag * (2.0 ** -20))) if l < L else 0)
+        zs.append(z)
+        if l < L:
+            h = activation(z, l, st.alpha, st.activation)
+            keep = None
+            if train and st.dropout > 0:
+                keep = dropout_keep(st.seed, rank, l, step, B, Ly.n_out, st.dropout)
+                h = h * keep * scale
+            keeps.append(keep)
+            a.append(h.astype(F32))
+        else:
+            keeps.append(None)
+    zL = zs[-1]
+    zmax = zL.max(axis=1, keepdims=True)
+    ez = np.exp(zL - zmax)
+    p64 = ez / ez.sum(axis=1, keepdims=True)
+    return Trace(B, bool(train), int(step), st.version, a, zs, keeps, p64.astype(F32), p64, amb)
+
+
+def loss_grad(p64: np.ndarray, y: np.ndarray):
+    """Softmax cross-entropy (DESIGN reading 12): L = (1/B) sum_b -ln p[b, y_b];
+    dL/dz_L = (p - onehot) / B, the 1/B applied exactly once."""
+    y = np.asarray(y, dtype=np.int64)
+    B, C = p64.shape
+    if np.any(y < 0) or np.any(y >= C):
+        raise ValueError("label out of range")
+    loss = float(-np.log(p64[np.arange(B), y]).mean())
+    d = p64.copy()
+    d[np.arange(B), y] -= 1.0
+    return loss, d / B
+
+
+@dataclass
+class Grads:
+    g: List[np.ndarray]      # g[l-2]: float32 [nnz of W^(l)] aligned to canonical CSR order
+    gb: List[np.ndarray]     # gb[l-2]: float32 [n_l]
+    loss: float
+    deltas: List[Optional[np.ndarray]]   # deltas[l-1]: float32 [B x n_l] (None for l = 1)
+
+
+def backward(st: State, tr: Trace, y: np.ndarray) -> Grads:
+    """sparse_mlp_backward: for l = L..2, g_ij = sum_b a_{l-1}[b,i] delta_l[b,j] on the support
+    only (SDDMM), gb_l = sum_b delta_l, delta_{l-1} = (delta_l W^(l)T) * f'_{l-1}(z_{l-1}) * keep/(1-r)
+    for l >= 3.  delta_L = (p - onehot)/B."""
+    if tr.version != st.version or not tr.train:
+        raise RuntimeError("stale trace")
+    L = st.L
+    loss, dz = loss_grad(tr.p64, y)
+    delta = dz.astype(F32)
+    scale = 1.0 / (1.0 - st.dropout) if st.dropout > 0 else 1.0
+    g: List[Optional[np.ndarray]] = [None] * (L - 1)
+    gb: List[Optional[np.ndarray]] = [None] * (L - 1)
+    deltas: List[Optional[np.ndarray]] = [None] * L
+    deltas[L - 1] = delta
+    for l in range(L, 1, -1):
+        Ly = st.layer(l)
+        g[l - 2] = sddmm(tr.a[l - 2], delta, Ly).astype(F32)
+        gb[l - 2] = delta.astype(F64).sum(axis=0).astype(F32)
+        if l >= 3:
+            d = spmm_bwd(delta, Ly) * activation_grad(tr.z[l - 2], l - 1, st.alpha, st.activation)
+            if tr.keep[l - 2] is not None:
+                d = d * tr.keep[l - 2] * scale
+            delta = d.astype(F32)
+            deltas[l - 2] = delta
+    return Grads(g, gb, loss, deltas)
+
+
+def step(st: State, grads: Grads, lr: float, momentum: float, weight_decay: float,
+         grad_scale: float = 1.0) -> None:
+    """sparse_mlp_step: Eq. 1 in velocity form, weight decay folded into the
+    gradient (DESIGN reading 14):  v <- mu v - eta (s g + lambda w);  w <- w + v.
+    Biases: vb <- mu vb - eta s gb; b <- b + vb (no decay)."""
+    for idx, Ly in enumerate(st.layers):
+        g = grads.g[idx].astype(F64) * grad_scale
+        v = momentum * Ly.v.astype(F64) - lr * (g + weight_decay * Ly.w.astype(F64))
+        Ly.v = v.astype(F32)
+        Ly.w = (Ly.w.astype(F64) + Ly.v.astype(F64)).astype(F32)
+        gbv = grads.gb[idx].astype(F64) * grad_scale
+        vb = momentum * st.vb[idx].astype(F64) - lr * gbv
+        st.vb[idx] = vb.astype(F32)
+        st.b[idx] = (st.b[idx].astype(F64) + st.vb[idx].astype(F64)).astype(F32)
+
+
+def train_step(st: State, x, y, lr, momentum, weight_decay, step_idx: int = 0):
+    """One minibatch: forward (train) -> backward -> update.  Returns (loss, trace, grads)."""
+    tr = forward(st, x, True, step_idx)
+    gr = backward(st, tr, y)
+    step(st, gr, lr, momentum, weight_decay)
+    return gr.loss, tr, gr

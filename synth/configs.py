@@ -1,0 +1,92 @@
+"""The five workload configurations C1..C5 (SURVEY.md §8 table, §8(d) recipes).
+
+Values come from BASELINE.json ``configs`` first and from the paper's
+Supp. Table 5 / P:957 where BASELINE.json is silent.
+Non-paper choices are marked and listed in DESIGN.md ("readings").
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field, asdict
+from typing import Tuple
+
+
+@dataclass(frozen=True)
+class WorkloadConfig:
+    name: str
+    stand_in_for: str
+    sizes: Tuple[int, ...]          # n_1 .. n_L (paper notation, input first)
+    epsilon: float                  # ER density parameter
+    alpha: float                    # All-ReLU slope (Eq. 3)
+    activation: str = "all_relu"    # "all_relu" | "relu"
+    dropout: float = 0.0            # inverted dropout rate on hidden activations
+    init: str = "he_uniform"        # "normal" | "xavier" | "he_uniform" (Table 5)
+    batch: int = 128                # per-rank minibatch B
+    lr: float = 0.01                # eta
+    momentum: float = 0.9           # mu
+    weight_decay: float = 2e-4      # lambda: value not given by the paper (non-paper default)
+    zeta: float = 0.3               # SET prune fraction
+    n_samples: int = 2000
+    epochs: int = 3
+    prune: bool = False             # Importance Pruning (Alg. 2)
+    prune_percentile: float = 5.0   # rho (Supp. C)
+    prune_every: int = 1            # p
+    prune_start: int = 0            # tau (paper: 200; C3 uses 0 so it fires in short runs)
+    data_seed: int = 0
+    model_seed: int = 0
+
+    @property
+    def n_layers(self) -> int:
+        return len(self.sizes)
+
+    @property
+    def n_classes(self) -> int:
+        return self.sizes[-1]
+
+    def to_json(self) -> dict:
+        d = asdict(self)
+        d["sizes"] = list(self.sizes)
+        return d
+
+
+def _cfg(idx: int, **kw) -> WorkloadConfig:
+    return WorkloadConfig(data_seed=1000 + idx, model_seed=2000 + idx, **kw)
+
+
+CONFIGS = {
+    # BASELINE.json configs[0]; Madelon stand-in
+    "C1": _cfg(1, name="C1", stand_in_for="Madelon (PAPER.md:147)",
+               sizes=(500, 400, 100, 400, 2), epsilon=10.0, alpha=0.6,
+               dropout=0.0, init="he_uniform", batch=128, lr=0.01,
+               n_samples=2000, epochs=3),
+    # configs[1]; FashionMNIST stand-in
+    "C2": _cfg(2, name="C2", stand_in_for="FashionMNIST (PAPER.md:148)",
+               sizes=(784, 1000, 1000, 1000, 10), epsilon=20.0, alpha=0.75,
+               dropout=0.3, init="he_uniform", batch=128, lr=0.01,
+               n_samples=60000, epochs=1),
+    # configs[2]; Leukemia stand-in, importance pruning each epoch
+    "C3": _cfg(3, name="C3", stand_in_for="Leukemia GSE13159 (PAPER.md:145)",
+               sizes=(54675, 27500, 27500, 18), epsilon=10.0, alpha=0.75,
+               dropout=0.3, init="normal", batch=5, lr=0.005,
+               n_samples=2096, epochs=1, prune=True, prune_percentile=5.0,
+               prune_every=1, prune_start=0),
+    # configs[3]; HIGGS x100 stand-in
+    "C4": _cfg(4, name="C4", stand_in_for="HIGGS x100 (PAPER.md:146)",
+               sizes=(28, 1000, 1000, 1000, 2), epsilon=10.0, alpha=0.05,
+               dropout=0.3, init="xavier", batch=128, lr=0.01,
+               n_samples=10_500_000, epochs=1),
+    # configs[4]; Table 4 row 1 scaled up
+    "C5": _cfg(5, name="C5", stand_in_for="make_classification 65536-feature set (PAPER.md:409)",
+               sizes=(65536, 500000, 500000, 500000, 2), epsilon=20.0, alpha=0.5,
+               dropout=0.0, init="he_uniform", batch=128, lr=0.01,
+               n_samples=100_000, epochs=1),
+}
+
+
+def get_config(name: str, **overrides) -> WorkloadConfig:
+    base = CONFIGS[name]
+    if not overrides:
+        return base
+    d = base.to_json()
+    d.update(overrides)
+    d["sizes"] = tuple(d["sizes"])
+    return WorkloadConfig(**d)
