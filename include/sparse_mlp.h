@@ -1,0 +1,243 @@
+/*
+ * sparse_mlp.h — C ABI of libsparse_mlp.so, the B200 (sm_100a) hot path of truly sparse
+ * MLP training with SET, All-ReLU and Importance Pruning (arXiv 2102.01732).
+ *
+ * Citations: "PAPER.md:n" = line n of the paper text; readings R1..R26 = DESIGN.md
+ * "Readings of the paper".  The problem statement the calls follow:
+ *   - train f_s(x; theta_s) with sparse W^(l), n_{l-1} x n_l, w_ij = 0 meaning "no
+ *     connection", to minimise sum L(f(x; theta), y)
+ *   - Alg. 2 init / train / update / prune / evolve loop
+ *   - Alg. 1 gradient exchange and model averaging
+ *
+ * Conventions (every call):
+ *   - Return 0 (SMLP_OK) on success, a negative SMLP_E_* code on failure; the text of the
+ *     last failure is sparse_mlp_last_error(h).  No call ever falls back to the CPU.
+ *   - Asynchrony: calls enqueue work on the handle's stream (create's cfg.stream, or the
+ *     one set by sparse_mlp_set_stream) and return immediately unless marked SYNC.
+ *   - Ownership: the caller owns every pointer it passes (x, labels, probs, loss, host
+ *     arrays) and keeps it valid until the stream's work completes.  The library owns all
+ *     model state and workspace, allocated through cfg.allocator (or cudaMallocAsync).
+ *   - Graph capture: forward / backward / step / train_step_device do no host sync and no
+ *     allocation once the handle exists, and keep every device pointer stable across
+ *     evolve_topology / prune_neurons (device-side counts), so a CUDA graph captured once
+ *     stays valid for the life of the handle (per batch size B).
+ *   - Threading: not thread-safe per handle; callers serialise.
+ *   - Layer indices follow the paper: neuron layers l = 1..L (input l = 1),
+ *     weight layer l = 2..L is W^(l) between neuron layers l-1 and l.
+ */
+#ifndef SPARSE_MLP_H
+#define SPARSE_MLP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMLP_MAX_LAYERS 16
+
+/* status codes */
+#define SMLP_OK        0
+#define SMLP_E_ARG    -1   /* invalid argument / configuration (S:119 preconditions)        */
+#define SMLP_E_NOMEM  -2   /* allocator returned NULL                                        */
+#define SMLP_E_CUDA   -3   /* a CUDA runtime call or kernel launch failed                    */
+#define SMLP_E_SHAPE  -4   /* B > max_batch, layer index out of range, buffer too small      */
+#define SMLP_E_STALE  -5   /* backward without a train-mode forward on the current topology  */
+#define SMLP_E_DATA   -6   /* a label outside [0, n_L) was seen by a previous backward       */
+#define SMLP_E_STATE  -7   /* step without pending gradients                                 */
+#define SMLP_E_STRUCT -8   /* imported CSR violates the invariants (sorted unique, bounds)  */
+
+/* activation (Eq. 3 All-ReLU PAPER.md:106-112; Eq. 5 ReLU PAPER.md:533-539) */
+#define SMLP_ACT_RELU      0
+#define SMLP_ACT_ALL_RELU  1
+
+/* weight initialisation (Table 5 names; reading R3) */
+#define SMLP_INIT_NORMAL     0   /* N(0, 2/n_{l-1}), Box-Muller                          */
+#define SMLP_INIT_XAVIER_U   1   /* U(-sqrt(6/(n_{l-1}+n_l)), +sqrt(6/(n_{l-1}+n_l)))    */
+#define SMLP_INIT_HE_U       2   /* U(-sqrt(6/n_{l-1}), +sqrt(6/n_{l-1}))                */
+
+/* prune flags */
+#define SMLP_PRUNE_OUTGOING  1   /* also remove the outgoing row of a pruned neuron (R17)   */
+
+typedef struct smlp_handle smlp_handle;
+
+/* Device allocator.  alloc(bytes, stream, ctx) returns device memory or NULL; free(ptr,
+ * bytes, stream, ctx) releases it.  Used for every model / workspace allocation.  The
+ * Python binding passes torch's caching allocator.  NULL => cudaMallocAsync/cudaFreeAsync. */
+typedef struct {
+    void* (*alloc)(size_t bytes, void* stream, void* ctx);
+    void  (*free)(void* ptr, size_t bytes, void* stream, void* ctx);
+    void* ctx;
+} smlp_allocator;
+
+typedef struct {
+    int32_t        n_layers;     /* L >= 3 (input, >= 1 hidden, output)                       */
+    const int64_t* sizes;        /* [L] neuron counts n_1..n_L, each >= 1 (host pointer)      */
+    double         epsilon;      /* ER density parameter eps > 0             */
+    int32_t        activation;   /* SMLP_ACT_*                                                */
+    float          alpha;        /* All-ReLU slope alpha >= 0                                 */
+    float          dropout;      /* inverted dropout rate in [0, 1) on hidden activations     */
+    int32_t        init;         /* SMLP_INIT_*                                               */
+    uint64_t       seed;         /* Philox key: topology and values are a function of it      */
+    int32_t        rank;         /* data-parallel rank: enters the dropout stream only        */
+    int32_t        max_batch;    /* largest B passed to forward, >= 1                         */
+    int32_t        chunk_batch;  /* batch columns per activation chunk (4..128, power of 2);
+                                    0 = auto (min(128, next_pow2(max(4, max_batch))))        */
+    int32_t        device;       /* CUDA device ordinal                                       */
+    void*          stream;       /* cudaStream_t the handle enqueues on (NULL = legacy)       */
+    const smlp_allocator* allocator; /* NULL = cudaMallocAsync on `stream`                   */
+} smlp_config;
+
+/* Momentum SGD with weight decay, Eq. 1 in velocity form (reading R14):
+ *   v <- mu v - lr (grad_scale g + weight_decay w);  w <- w + v;   biases: no decay.      */
+typedef struct {
+    float lr;
+    float momentum;
+    float weight_decay;
+    float grad_scale;   /* 1/K after a K-rank SUM allreduce; 1 for one rank */
+} smlp_sgd;
+
+typedef struct {
+    int32_t  n_layers;
+    int32_t  chunk_batch;
+    uint64_t version;                        /* topology version, +1 per structural edit  */
+    int64_t  sizes[SMLP_MAX_LAYERS];         /* n_l at index l-1                          */
+    int64_t  alive[SMLP_MAX_LAYERS];         /* alive neurons of layer l at index l-1     */
+    int64_t  nnz[SMLP_MAX_LAYERS];           /* nnz of W^(l) at index l-1 (0 for l = 1)   */
+    int64_t  cap[SMLP_MAX_LAYERS];           /* capacity of W^(l) (initial nnz)           */
+    int32_t  dense_capped[SMLP_MAX_LAYERS];  /* W^(l) dense-capped, never evolved (R9)    */
+    int64_t  val_offset[SMLP_MAX_LAYERS];    /* offset of W^(l) values in the param view  */
+    int64_t  bias_offset[SMLP_MAX_LAYERS];   /* offset of b_l in the param view           */
+    int64_t  param_count;                    /* floats in the param / grad views          */
+    int64_t  launches;                       /* kernels launched by this handle so far    */
+} smlp_info;
+
+/* sparse_mlp_create — PAPER.md:51-52 ("Initially each W^(l) is a Erdos-Renyi random graph"),
+ * Alg. 2 PAPER.md:643-646.  Per weight layer M = min(n_in n_out, floor(eps (n_in + n_out)))
+ * connections (R1): the first M distinct positions of the INIT Philox stream (R2), values
+ * from the scheme `init`; dense-capped layers take every position.  Momentum and biases are
+ * zero, version = 0.  SYNC (returns after the initial topology is built).
+ * Errors: SMLP_E_ARG (L < 3 or > SMLP_MAX_LAYERS, n_l < 1, eps <= 0, alpha < 0, dropout
+ * outside [0,1), max_batch < 1, bad enum, nnz >= 2^31 in a layer), SMLP_E_NOMEM, SMLP_E_CUDA.
+ * On failure *out is NULL. */
+int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out);
+
+/* Frees everything through the allocator on the handle's stream.  NULL is a no-op. */
+int sparse_mlp_destroy(smlp_handle* h);
+
+/* Replace the stream subsequent calls enqueue on (e.g. torch's current stream). */
+int sparse_mlp_set_stream(smlp_handle* h, void* stream);
+
+/* sparse_mlp_forward — a_1 = x; for l = 2..L: z_l = a_{l-1} W^(l) + b_l; for hidden l,
+ * a_l = f_l(z_l) (Eq. 3) then, if train, inverted dropout with rate
+ * cfg.dropout drawn from Philox(DROPOUT, rank, l, step) (R13); p = softmax(z_L).
+ *   x:      device fp32, row-major [rows x n_1]; sample b is row (x_idx ? x_idx[b] : b).
+ *   x_idx:  device int32 [B] or NULL.
+ *   B:      1..max_batch.   train: 0/1.   step: global step (dropout stream counter).
+ *   probs:  device fp32 [B x n_L] row-major, or NULL.
+ * Records a trace (version, B, train) for backward.
+ * Errors: SMLP_E_SHAPE (B < 1 or B > max_batch), SMLP_E_CUDA. */
+int sparse_mlp_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int32_t B,
+                       int32_t train, uint64_t step, float* probs);
+
+/* sparse_mlp_backward — softmax cross-entropy (R12): loss = (1/B) sum_b -ln p[b, y_b],
+ * delta_L = (p - onehot)/B; for l = L..2: g_ij = sum_b a_{l-1}[b,i] delta_l[b,j] on the
+ * support only (SDDMM), gb_l = sum_b delta_l[b,:], and for l >= 3
+ * delta_{l-1} = (delta_l W^(l)T) * f'_{l-1}(z_{l-1}) * keep/(1-r).
+ *   labels: device int32 [rows]; sample b uses labels[y_idx ? y_idx[b] : b].
+ *   y_idx:  device int32 [B] or NULL (normally the x_idx of the forward).
+ *   loss:   device fp32 scalar or NULL.
+ *   fused:  NULL -> gradients are written to the grad view for a later sparse_mlp_step
+ *           (the multi-GPU path, after the caller's allreduce); non-NULL -> the Eq. 1
+ *           update (fused->grad_scale ignored, = 1) is applied in the same pass.
+ * Errors: SMLP_E_STALE (no train-mode forward since the last topology change),
+ * SMLP_E_DATA (an out-of-range label was flagged by an earlier backward; the flag is
+ * checked without synchronising, so it is reported one call late), SMLP_E_CUDA. */
+int sparse_mlp_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx,
+                        float* loss, const smlp_sgd* fused);
+
+/* sparse_mlp_step — Eq. 1 update on the grad view (after the caller's SUM allreduce and
+ * with sgd->grad_scale = 1/K).  Errors: SMLP_E_STATE if no unfused backward is pending. */
+int sparse_mlp_step(smlp_handle* h, const smlp_sgd* sgd);
+
+/* One fused training step with HOST buffers (pinned for async copies): H2D of
+ * x_host [B x n_1] and y_host [B], forward(train) + fused backward, D2H of the loss.
+ * The copies are enqueued on the handle's stream; SYNC at the end (loss is ready). */
+int sparse_mlp_train_step_host(smlp_handle* h, const float* x_host, const int32_t* y_host,
+                               int32_t B, uint64_t step, const smlp_sgd* sgd, float* loss_host);
+
+/* Contiguous device views [values of W^(2..L) at their capacity offsets || biases b_2..b_L],
+ * identical layout on every replica, stable for the life of the handle (holes left by
+ * pruning are zero).  grad view: filled by an unfused backward (X1 allreduce, SUM).
+ * param view: the parameters theta = (w, b) (X2 averaging, Eq. 2). */
+int sparse_mlp_grad_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version);
+int sparse_mlp_param_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version);
+
+/* sparse_mlp_evolve_topology — Alg. 2 PAPER.md:659-664 on every weight layer that is not
+ * dense-capped: per sign class k = floor(zeta n_+/-), remove the k positives and the k
+ * negatives closest to zero (key: |w| bits, canonical index; R5-R7), regrow R = k_+ + k_-
+ * connections at the first R distinct positions of the REGROW Philox stream (counter
+ * evolve_idx) that are outside the pre-call support and join two alive neurons (R8); new
+ * w from the init scheme, new v = 0; survivors keep (w, v) bit-exactly.  A layer with
+ * fewer free positions than R is left unchanged (R9).  Deterministic in (seed, evolve_idx,
+ * weights), so replicas agree without communication.  version += 1.
+ *   removed_per_layer: host int64 [L] or NULL; index l-1 = removed count of W^(l), -1 =
+ *   skipped (dense-capped or saturated).
+ * SYNC (small count read-backs).  Errors: SMLP_E_ARG if zeta not in (0, 1). */
+int sparse_mlp_evolve_topology(smlp_handle* h, double zeta, uint64_t evolve_idx,
+                               int64_t* removed_per_layer);
+
+/* sparse_mlp_prune_neurons — Importance Pruning, Alg. 2 PAPER.md:652-658 with Eq. 4
+ * I_j = sum_i |w_ij| (sequential fp64 sum, ascending i) over the hidden
+ * layers h = 2..L-1, all importances taken before any removal (R19); threshold
+ * t = percentile(alive I, `percentile`) by linear interpolation (R15); alive neurons with
+ * I_j < t lose their incoming column of W^(h) and, with SMLP_PRUNE_OUTGOING, their outgoing
+ * row of W^(h+1) (R17); a layer that would lose every alive neuron is skipped.  version += 1.
+ *   pruned_per_layer: host int64 [L] or NULL (index l-1; -1 = skipped).
+ *   removed_conn:     host int64 [L] or NULL (index l-1 = connections removed from W^(l)).
+ * SYNC.  Errors: SMLP_E_ARG if percentile not in [0, 100). */
+int sparse_mlp_prune_neurons(smlp_handle* h, double percentile, int32_t flags,
+                             int64_t* pruned_per_layer, int64_t* removed_conn);
+
+/* Eq. 4 importances of neuron layer l (2..L-1) into out [n_l] (device or host fp64). SYNC. */
+int sparse_mlp_importance(smlp_handle* h, int32_t l, double* out, int32_t to_host);
+
+/* Model information (host struct).  SYNC-free (host-side bookkeeping). */
+int sparse_mlp_info(smlp_handle* h, smlp_info* info);
+
+/* Export W^(l) (l = 2..L) in the paper orientation: CSR by input row i (row_ptr [n_{l-1}+1],
+ * col_idx / val / mom [nnz]) with sorted unique columns.  to_host: 1 = host buffers, 0 =
+ * device buffers.  Any pointer may be NULL to skip that array.  SYNC. */
+int sparse_mlp_export_layer(smlp_handle* h, int32_t l, int32_t* row_ptr, int32_t* col_idx,
+                            float* val, float* mom, int32_t to_host);
+
+/* Import W^(l) from HOST arrays (parity tests / checkpoints).  nnz must not exceed the
+ * layer's capacity.  The invariants of SPEC S:26-29 are checked (row_ptr monotone from 0 to
+ * nnz, columns sorted unique within rows and in [0, n_l)); on violation SMLP_E_STRUCT names
+ * the offending (row, col).  Rebuilds the output-major mirror; version += 1.  SYNC. */
+int sparse_mlp_import_layer(smlp_handle* h, int32_t l, int64_t nnz, const int32_t* row_ptr,
+                            const int32_t* col_idx, const float* val, const float* mom);
+
+/* Biases b_l / momentum of b_l (l = 2..L) and liveness of neuron layer l (1..L), host. SYNC. */
+int sparse_mlp_export_bias(smlp_handle* h, int32_t l, float* bias, float* bias_mom);
+int sparse_mlp_import_bias(smlp_handle* h, int32_t l, const float* bias, const float* bias_mom);
+int sparse_mlp_export_alive(smlp_handle* h, int32_t l, uint8_t* alive);
+int sparse_mlp_import_alive(smlp_handle* h, int32_t l, const uint8_t* alive);
+
+/* Trace export for parity tests: kind 0 = activations a_l (l = 1..L-1; l = L gives the
+ * logits z_L), kind 1 = deltas delta_l (l = 2..L) of the last forward / backward, as host
+ * fp32 row-major [B x n_l].  kind 2 = gradient of W^(l) values from the grad view (host
+ * fp32 [nnz]) and kind 3 = bias gradient of layer l (host fp32 [n_l]).  SYNC. */
+int sparse_mlp_export_trace(smlp_handle* h, int32_t kind, int32_t l, float* out);
+
+/* Last error text of this handle (or of the last failed create when h is NULL). */
+const char* sparse_mlp_last_error(const smlp_handle* h);
+
+/* Library version string. */
+const char* sparse_mlp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSE_MLP_H */

@@ -1,0 +1,258 @@
+// smlp_internal.cuh — internal state and device helpers of libsparse_mlp.so (sm_100a).
+//
+// Layout in HBM:
+//   param / mom / grad : one contiguous fp32 buffer each, [W^(2) cap | ... | W^(L) cap | b_2 | ... | b_L]
+//                        (offsets rounded to 32 floats) — the grad view is what a multi-GPU
+//                        step allreduces (X1), the param view what averaging allreduces (X2).
+//   W^(l) canonical    : input-major CSR (the paper orientation): row_ptr int32
+//                        [n_{l-1}+1], col int32 [cap], val/mom/grad fp32 slices [cap], rowid int32
+//                        [cap] (row of each entry, for nnz-parallel kernels).
+//   W^(l) mirror       : output-major CSR: mrow_ptr [n_l+1], msrc [cap] (input neuron i),
+//                        mperm [cap] (canonical index of the entry).
+//   activations        : "chunked transposed": act[l] = [n_chunks][n_l][CB] fp32, CB = chunk_batch
+//                        batch columns per chunk, so one neuron's CB values are one contiguous
+//                        row (CB = 128 -> 512 B, one float4 per lane of a warp).
+//   masks              : per hidden neuron row and chunk, uint4 = 4 x 32 bits; word c, bit q
+//                        is batch column 4q + c of the chunk (one ballot per float4 lane).
+//   work lists         : per layer, forward segments over mirror rows and backward segments
+//                        over canonical rows, each <= SEG_NNZ entries, counts in device memory.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sparse_mlp.h"
+
+namespace smlp {
+
+constexpr int SEG_NNZ = 512;              // max nnz per work segment (long-row split)
+constexpr int WARPS_PER_BLOCK = 8;        // 256-thread blocks for the warp-per-row kernels
+
+struct LayerMeta {                         // device-resident counts (graph-stable)
+    int32_t nnz;
+    int32_t n_fseg;
+    int32_t n_bseg;
+    int32_t n_fmulti;
+    int32_t n_bmulti;
+    int32_t pad[3];
+};
+
+struct Layer {
+    int l = 0;
+    int64_t n_in = 0, n_out = 0;
+    bool dense = false;
+    int64_t cap = 0, nnz = 0;
+    int64_t val_off = 0, bias_off = 0;
+    // canonical CSR
+    int32_t* row_ptr = nullptr;
+    int32_t* col = nullptr;
+    int32_t* rowid = nullptr;
+    float* val = nullptr;
+    float* mom = nullptr;
+    float* grad = nullptr;
+    // output-major mirror
+    int32_t* mrow_ptr = nullptr;
+    int32_t* msrc = nullptr;
+    int32_t* mperm = nullptr;
+    // segment work lists: int4 (row, beg, end, slot) ; multi: int4 (row, first_slot, n_slots, 0)
+    int64_t fseg_cap = 0, bseg_cap = 0, fslot_cap = 0, bslot_cap = 0;
+    int4* fseg = nullptr;
+    int4* bseg = nullptr;
+    int4* fmulti = nullptr;
+    int4* bmulti = nullptr;
+    float* fws = nullptr;   // [fslot_cap][CB] partial sums of multi-segment forward rows
+    float* bws = nullptr;   // [bslot_cap][CB] partial delta sums of multi-segment backward rows
+    float* bgs = nullptr;   // [n_in] bias-grad accumulator across chunks (for layer l-1)
+    LayerMeta* meta = nullptr;
+    LayerMeta meta_h{};
+    // biases of neuron layer l live in param/mom/grad at bias_off
+    float* bias = nullptr;
+    float* bias_mom = nullptr;
+    float* bias_grad = nullptr;
+};
+
+struct Alloc {
+    size_t bytes;
+    void* ptr;
+};
+
+}  // namespace smlp
+
+struct smlp_handle {
+    int L = 0;
+    int64_t sizes[SMLP_MAX_LAYERS] = {0};
+    double eps = 0;
+    int activation = SMLP_ACT_ALL_RELU;
+    float alpha = 0.f, dropout = 0.f;
+    int init = SMLP_INIT_HE_U;
+    uint64_t seed = 0;
+    int rank = 0;
+    int max_batch = 0;
+    int CB = 128;
+    int max_chunks = 1;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    smlp_allocator allocator{};
+    bool has_allocator = false;
+    std::vector<smlp::Alloc> allocs;   // every live allocation (freed at destroy)
+
+    std::vector<smlp::Layer> layers;   // layers[l-2] = W^(l)
+    float* param = nullptr;
+    float* mom = nullptr;
+    float* grad = nullptr;
+    int64_t param_count = 0;
+    int64_t bias_base = 0;
+
+    float* act[SMLP_MAX_LAYERS + 1] = {nullptr};     // index l (1..L)
+    float* delta[SMLP_MAX_LAYERS + 1] = {nullptr};   // index l (2..L)
+    uint4* zmask[SMLP_MAX_LAYERS + 1] = {nullptr};   // hidden l: bit = (z > 0)
+    uint4* kmask[SMLP_MAX_LAYERS + 1] = {nullptr};   // hidden l: bit = dropout keep
+    uint8_t* alive[SMLP_MAX_LAYERS + 1] = {nullptr}; // index l (1..L)
+    int64_t alive_h[SMLP_MAX_LAYERS + 1] = {0};
+
+    int32_t* d_err = nullptr;       // label-range flag
+    float* d_loss = nullptr;        // scratch loss for train_step_host
+    float* x_stage = nullptr;       // [max_batch x n_1] for train_step_host
+    int32_t* y_stage = nullptr;
+
+    // trace of the last forward
+    bool trace_valid = false;
+    bool trace_train = false;
+    int trace_B = 0;
+    uint64_t trace_version = 0;
+    uint64_t trace_step = 0;
+    bool grads_pending = false;
+
+    uint64_t version = 0;
+    int num_sms = 148;
+    int64_t launches = 0;
+    std::string err;
+};
+
+namespace smlp {
+
+// ------------------------------------------------------------------------------------------
+// error helpers
+// ------------------------------------------------------------------------------------------
+int set_err(smlp_handle* h, int code, const std::string& msg);
+int check_cuda(smlp_handle* h, cudaError_t e, const char* what);
+#define SMLP_CK(h, call)                                                   \
+    do {                                                                   \
+        cudaError_t _e = (call);                                           \
+        if (_e != cudaSuccess) return ::smlp::check_cuda((h), _e, #call);  \
+    } while (0)
+#define SMLP_CK_LAUNCH(h, what)                                            \
+    do {                                                                   \
+        (h)->launches++;                                                   \
+        cudaError_t _e = cudaGetLastError();                               \
+        if (_e != cudaSuccess) return ::smlp::check_cuda((h), _e, what);   \
+    } while (0)
+#define SMLP_TRY(call)             \
+    do {                           \
+        int _rc = (call);          \
+        if (_rc != SMLP_OK) return _rc; \
+    } while (0)
+
+// allocation through the caller's allocator (or cudaMallocAsync); tracked for destroy
+void* dev_alloc(smlp_handle* h, size_t bytes);
+void dev_free(smlp_handle* h, void* p);
+// temporary allocation freed by the caller with tmp_free (not tracked)
+void* tmp_alloc(smlp_handle* h, size_t bytes);
+void tmp_free(smlp_handle* h, void* p, size_t bytes);
+
+// ------------------------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11) and the stream layout of DESIGN.md (R2, R8, R13)
+// ------------------------------------------------------------------------------------------
+enum Purpose : uint32_t { P_INIT = 1, P_INIT_DENSE = 2, P_REGROW = 3, P_DROPOUT = 4 };
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        if (r < 9) {
+            k.x += 0x9E3779B9u;
+            k.y += 0xBB67AE85u;
+        }
+    }
+    return c;
+}
+
+__device__ __forceinline__ uint4 rng_stream(uint64_t seed, uint32_t purpose, uint32_t rank,
+                                            uint32_t layer, uint32_t c3, uint64_t idx) {
+    const uint4 c = make_uint4((uint32_t)idx, (uint32_t)(idx >> 32),
+                               ((purpose & 0xffu) << 24) | ((rank & 0xffu) << 16) | (layer & 0xffffu), c3);
+    return philox4x32_10(c, make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+}
+
+// candidate position from two uniform words: i = floor(x0 n_in / 2^32), j likewise
+__device__ __forceinline__ uint32_t scale_u32(uint32_t x, uint64_t n) {
+    return (uint32_t)(((uint64_t)x * n) >> 32);
+}
+
+// Initial / regrown value (R3, R4): uniform schemes are exact but for the final fp32 multiply;
+// "normal" is Box-Muller in fp64 rounded once to fp32.
+struct InitParams {
+    int scheme;
+    float lim;      // fp32(sqrt(6/n_in)) or fp32(sqrt(6/(n_in+n_out)))
+    double std;     // sqrt(2/n_in)
+};
+
+__device__ __forceinline__ float init_value(const InitParams& p, uint32_t x2, uint32_t x3) {
+    if (p.scheme != SMLP_INIT_NORMAL) {
+        const float u = __fmul_rn((float)(x2 >> 8), 5.9604644775390625e-08f);
+        const float t = __fadd_rn(__fmul_rn(u, 2.0f), -1.0f);
+        return __fmul_rn(t, p.lim);
+    }
+    const double u1 = __dmul_rn((double)(x2 >> 8) + 1.0, 5.9604644775390625e-08);
+    const double u2 = __dmul_rn((double)(x3 >> 8), 5.9604644775390625e-08);
+    const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+    const double c = cos(__dmul_rn(6.283185307179586, u2));
+    return (float)__dmul_rn(__dmul_rn(r, c), p.std);
+}
+
+InitParams init_params(const smlp_handle* h, const Layer& L);
+
+// ------------------------------------------------------------------------------------------
+// topology build helpers (topology.cu)
+// ------------------------------------------------------------------------------------------
+// From a canonical CSR (row_ptr, col filled for nnz entries) rebuild rowid, the output-major
+// mirror and both segment work lists; refreshes meta (device + host).
+int rebuild_derived(smlp_handle* h, Layer& L);
+// Sorted unique positions (u64 pos = i * n_out + j) with values -> canonical CSR arrays of L
+// (row_ptr, col, val; mom zeroed) for n entries.  pos/val are device arrays.
+int csr_from_sorted_positions(smlp_handle* h, Layer& L, const uint64_t* pos, const float* val,
+                              int64_t n);
+// "First R distinct valid candidates in stream order" (R2, R8): candidates m = 0.. of stream
+// (purpose, layer, c3); valid = not in the current support of L (if exclude_support) and both
+// neurons alive (if alive_in/alive_out non-NULL).  Output: R positions sorted ascending and
+// their values (init scheme).  out_pos/out_val are device arrays of >= R elements.
+int first_distinct_candidates(smlp_handle* h, const Layer& L, uint32_t purpose, uint32_t c3,
+                              int64_t R, bool exclude_support, const uint8_t* alive_in,
+                              const uint8_t* alive_out, int64_t n_free, uint64_t* out_pos,
+                              float* out_val);
+int fill_dense_layer(smlp_handle* h, Layer& L);
+int launch_grid(const smlp_handle* h, int64_t items, int threads);
+
+// step.cu
+int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, bool train,
+                uint64_t step, float* probs);
+int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss,
+                 const smlp_sgd* fused);
+int run_step(smlp_handle* h, const smlp_sgd* sgd);
+
+// evolve.cu / prune.cu
+int run_evolve(smlp_handle* h, double zeta, uint64_t e, int64_t* removed);
+int run_importance(smlp_handle* h, int l, double* out_dev);
+int run_prune(smlp_handle* h, double rho, int flags, int64_t* pruned, int64_t* removed);
+// compact W^(l) to the entries whose flag is 0 (no additions), rebuild derived state
+int compact_layer(smlp_handle* h, Layer& L, const uint8_t* remove_flags);
+// merge: survivors (flag 0) of L plus R sorted additions (pos, val) -> new canonical CSR
+int merge_layer(smlp_handle* h, Layer& L, const uint8_t* remove_flags, const uint64_t* add_pos,
+                const float* add_val, int64_t R);
+
+}  // namespace smlp
