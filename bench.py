@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark: training samples/s of the truly sparse MLP step on B200 (BASELINE.json "metric").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1: synchronous DP over NCCL)
+
+A step is one pass of the whole hot path over one minibatch B per rank: input
+staging (a1), forward SpMM + All-ReLU (a2, a3), softmax-CE, backward delta SpMM + SDDMM (a4, a5),
+the Eq. 1 momentum / weight-decay update (a6; fused into the backward on one GPU), and for N > 1
+the NCCL SUM allreduce of the grad view (a7) + the update kernel.  Inputs are resident in HBM
+(C5: 100k x 65536 fp32 = 26.2 GB per rank, far larger than the 126 MB L2, so no L2 flush is
+needed between steps).  Per-epoch SET evolution / pruning is measured separately ("epoch" key).
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training samples/sec per sparse-MLP step"
+UNIT = "samples/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            P = json.load(f)
+        return float(P["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def f1_bytes(sizes, nnz, B):
+    """Formula F1: algorithmic HBM bytes of one fused 1-GPU step."""
+    tot = 0.0
+    for l in range(2, len(sizes) + 1):
+        tot += 32.0 * nnz[l - 1] + 4.0 * B * (3 * sizes[l - 2] + 2 * sizes[l - 1])
+    return tot - 4.0 * B * sizes[0]
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------ data
+def load_data(cfg, rank, world, device):
+    """Resident per-rank shard (X [n x n_1] fp32, Y [n] int32) on the device."""
+    import numpy as np
+    import torch
+
+    from paper_2102_01732_b200.dp import shard_bounds
+    from synth.data import c5_device_dataset, make_dataset
+    lo, hi = shard_bounds(cfg.n_samples, rank, world)
+    if cfg.name == "C5":
+        return c5_device_dataset(cfg, hi - lo, device, seed_offset=rank)
+    X, Y = make_dataset(cfg, n=hi)
+    return (torch.from_numpy(np.ascontiguousarray(X[lo:hi])).to(device),
+            torch.from_numpy(np.ascontiguousarray(Y[lo:hi])).to(device))
+
+
+def cpu_baseline_job(cfg_name: str, batch: int, steps: int) -> dict:
+    """The oracle as it stands, on the host cores, over a bounded sample of the same workload."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("MKL_NUM_THREADS", "1")
+    import numpy as np
+
+    from oracle import model as M
+    from synth import get_config
+    from synth.data import c5_host_rows, make_dataset
+    cfg = get_config(cfg_name)
+    t0 = time.perf_counter()
+    st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed)
+    t_init = time.perf_counter() - t0
+    n = batch * steps
+    X, Y = (c5_host_rows(cfg, np.arange(n)) if cfg.name == "C5" else make_dataset(cfg, n=n))
+    t0 = time.perf_counter()
+    for s in range(steps):
+        sl = slice(s * batch, (s + 1) * batch)
+        M.train_step(st, X[sl], Y[sl], cfg.lr, cfg.momentum, cfg.weight_decay, s)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{steps} oracle training steps (fwd+bwd+Eq.1 update) of {cfg_name} at batch {batch} "
+                      f"(of {cfg.batch}); {dt:.1f} s timed, {t_init:.1f} s untimed ER init; NumPy/SciPy, "
+                      f"1 thread, os.cpu_count()={os.cpu_count()}"}
+
+
+# ------------------------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from synth import get_config
+    cfg = get_config(args.config)
+    sample_B = min(cfg.batch, 8) if cfg.name in ("C5", "C3") else cfg.batch
+    warm = max(0, min(args.warmup, 1))
+    res = cpu_baseline_job(cfg.name, sample_B, args.steps + warm)
+    line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "global_batch": sample_B, "layer_sizes": list(cfg.sizes),
+                       "epsilon": cfg.epsilon},
+            "cpu_baseline": res,
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--chunk-batch", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-epoch", action="store_true")
+    ap.add_argument("--profile-json", default="")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    args.warmup = max(3, args.warmup)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2102_01732_b200 import SGD, SparseMLP
+    from paper_2102_01732_b200.dp import allreduce_sum_, init_process_group, replicas_identical, scaled_lr
+    from synth import get_config
+
+    rank, world, local = init_process_group()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    cfg = get_config(args.config)
+    B = cfg.batch
+
+    # cpu_baseline (oracle, host cores) in a side process on rank 0, N = 1 only
+    cpu_fut = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import concurrent.futures as cf
+        import multiprocessing as mp
+        ex = cf.ProcessPoolExecutor(1, mp_context=mp.get_context("spawn"))
+        cpu_B = min(B, 8) if cfg.name in ("C5", "C3") else B
+        cpu_fut = ex.submit(cpu_baseline_job, cfg.name, cpu_B, 2 if cfg.name == "C5" else 20)
+
+    t0 = time.perf_counter()
+    model = SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed,
+                      rank, B, args.chunk_batch, local)
+    t_create = time.perf_counter() - t0
+    X, Y = load_data(cfg, rank, world, device)
+    n_local = X.shape[0]
+    rng = np.random.default_rng([cfg.data_seed, 77, rank])
+    total_steps = args.warmup + args.steps
+    idx_all = torch.from_numpy(np.concatenate([rng.permutation(n_local)[: B] for _ in range(total_steps)])
+                               .astype(np.int32)).to(device)
+    loss = torch.zeros(1, device=device)
+    info0 = model.info()
+    nnz = info0["nnz"]
+    warm_steps = max(1, (cfg.n_samples // (B * world)))    # one epoch of linear-scaling warmup
+
+    def one_step(s):
+        idx = idx_all[s * B:(s + 1) * B]
+        lr = scaled_lr(cfg.lr, world, s, warm_steps)
+        model.forward(X, x_idx=idx, train=True, step=s)
+        if world == 1:
+            model.backward(Y, y_idx=idx, loss=loss, fused=SGD(lr, cfg.momentum, cfg.weight_decay))
+        else:
+            model.backward(Y, y_idx=idx, loss=loss, fused=None)
+            g, _ = model.grad_view()
+            allreduce_sum_(g)
+            model.step(SGD(lr, cfg.momentum, cfg.weight_decay, 1.0 / world))
+
+    for s in range(args.warmup):
+        one_step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = model.info()["launches"]
+    model.sparse_mlp_profile(True)
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0.record(stream)
+    for s in range(args.warmup, total_steps):
+        one_step(s)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = model.sparse_mlp_profile_read()
+    model.sparse_mlp_profile(False)
+    launches = model.info()["launches"] - launches0
+    clk = clocks.stop()
+    t_ms = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms = float(t_ms.item())
+    ms_per_step = ms / args.steps
+    value = B * world * args.steps / (ms / 1e3)
+
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    peak, peak_src = _peaks()
+    dom = max(prof, key=lambda r: r["total_ms"]) if prof else None
+    roof = None
+    if dom:
+        avg_ms = dom["total_ms"] / dom["launches"]
+        achieved = dom["bytes_per_launch"] / (avg_ms * 1e-3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            try:
+                T = json.load(open(tpath))
+                traffic = T.get(cfg.name, {}).get(f"{dom['kernel']}:{dom['layer']}")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": f"{dom['kernel']} W^({dom['layer']})", "avg_launch_ms": round(avg_ms, 4),
+                "algorithmic_bytes_per_launch": dom["bytes_per_launch"], "peak_source": peak_src}
+    step_bytes = f1_bytes(cfg.sizes, nnz, B)
+    step_roof = {"bytes_per_step_F1": step_bytes, "achieved_GBps": round(step_bytes / (ms_per_step * 1e-3) / 1e9, 1),
+                 "frac": round(step_bytes / (ms_per_step * 1e-3) / 1e9 / peak, 4)}
+
+    # ---------------------------------------------------------------- end to end through the host-buffer API
+    e2e = None
+    if not args.no_e2e:
+        nb = 4
+        if cfg.name == "C5":
+            from synth.data import c5_host_rows
+            Xh, Yh = c5_host_rows(cfg, np.arange(rank * nb * B, (rank + 1) * nb * B))
+        else:
+            Xh = X[: nb * B].cpu().numpy()
+            Yh = Y[: nb * B].cpu().numpy()
+        xp = torch.from_numpy(Xh).pin_memory()
+        yp = torch.from_numpy(Yh.astype(np.int32)).pin_memory()
+        sgd = SGD(cfg.lr, cfg.momentum, cfg.weight_decay)
+        for s in range(2):
+            model.train_step_host(xp[s * B:(s + 1) * B], yp[s * B:(s + 1) * B], B, 10_000 + s, sgd)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        k2 = max(3, min(args.steps, 10))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(k2):
+            j = s % nb
+            model.train_step_host(xp[j * B:(j + 1) * B], yp[j * B:(j + 1) * B], B, 20_000 + s, sgd)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": B * world * k2 / (float(et.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": B * cfg.sizes[0] * 4 + B * 4, "d2h_bytes_per_step": 4,
+               "api": "sparse_mlp_train_step_host (pinned host x, y -> device, fwd, fused bwd, loss -> host)"}
+
+    # ---------------------------------------------------------------- epoch-boundary ops (evolve / prune)
+    epoch = None
+    if not args.no_epoch:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if cfg.prune:
+            model.prune_neurons(cfg.prune_percentile)
+        model.evolve_topology(cfg.zeta, 0)
+        torch.cuda.synchronize()
+        t_ev = time.perf_counter() - t0
+        steps_per_epoch = math.ceil(cfg.n_samples / (B * world))
+        epoch = {"evolve_s": round(t_ev, 4), "steps_per_epoch": steps_per_epoch,
+                 "epoch_samples_per_s_incl_evolve": cfg.n_samples / (steps_per_epoch * ms_per_step / 1e3 + t_ev),
+                 "replicas_identical": bool(replicas_identical(model.param_view()[0])) if world > 1 else True}
+
+    cpu = None
+    if cpu_fut is not None:
+        try:
+            cpu = cpu_fut.result(timeout=900)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": cfg.name, "stand_in_for": cfg.stand_in_for, "global_batch": B * world,
+                           "batch_per_rank": B, "layer_sizes": list(cfg.sizes), "epsilon": cfg.epsilon,
+                           "nnz": sum(nnz), "chunk_batch": info0["chunk_batch"],
+                           "parallelism": f"dp{world}", "l2_flush": "inputs larger than L2 (resident shard "
+                           f"{X.numel() * 4 / 1e9:.1f} GB; per-step traffic {step_bytes / 1e9:.2f} GB)",
+                           "create_s": round(t_create, 2)},
+                "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clk, "epoch": epoch,
+                "kernels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in prof]}
+        print(json.dumps(line), flush=True)
+        if args.profile_json:
+            with open(args.profile_json, "w") as f:
+                json.dump(line, f, indent=1)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

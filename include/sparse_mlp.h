@@ -231,6 +231,31 @@ int sparse_mlp_import_alive(smlp_handle* h, int32_t l, const uint8_t* alive);
  * fp32 [nnz]) and kind 3 = bias gradient of layer l (host fp32 [n_l]).  SYNC. */
 int sparse_mlp_export_trace(smlp_handle* h, int32_t kind, int32_t l, float* out);
 
+/* Per-kernel timing with CUDA events on the handle's stream (bench.py's roofline evidence).
+ * sparse_mlp_profile(h, 1) clears the records and starts recording an event pair around every
+ * hot-path kernel launch; (h, 0) stops.  Not usable while a CUDA graph is being captured.
+ * sparse_mlp_profile_read (SYNC) aggregates the recorded launches by (kind, layer): kind
+ * 0 stage_input, 1 fwd, 2 fwd_finish, 3 softmax_ce, 4 bwd, 5 bwd_finish, 6 sgd_update.
+ * bytes_per_launch / flops_per_launch are the ALGORITHMIC figures of DESIGN.md (formula F1 split
+ * per launch: index/value terms 12 B/nnz forward, 20 B/nnz fused backward (12 unfused), 20 B per
+ * value for sgd_update, activation terms 4 B per batch column per neuron read or written). */
+typedef struct {
+    int32_t kind;
+    int32_t layer;
+    int64_t launches;
+    double  total_ms;
+    double  bytes_per_launch;
+    double  flops_per_launch;
+} smlp_kernel_stat;
+int sparse_mlp_profile(smlp_handle* h, int32_t enable);
+int sparse_mlp_profile_read(smlp_handle* h, smlp_kernel_stat* out, int32_t cap, int32_t* n);
+
+/* Dropout step source for CUDA-graph replay: when dev_counter is non-NULL, train-mode forward
+ * reads the dropout stream counter (R13) from *dev_counter (device uint64) at kernel time
+ * instead of its `step` argument, so one captured graph draws fresh masks on every replay
+ * (the caller advances the counter, e.g. inside the same graph).  NULL restores `step`. */
+int sparse_mlp_set_step_counter(smlp_handle* h, const uint64_t* dev_counter);
+
 /* Last error text of this handle (or of the last failed create when h is NULL). */
 const char* sparse_mlp_last_error(const smlp_handle* h);
 

@@ -62,6 +62,26 @@ void dev_free(smlp_handle* h, void* p) {
     }
 }
 
+void prof_start(smlp_handle* h, int kind, int layer, double bytes, double flops) {
+    if (!h->prof) return;
+    ProfRec r{kind, layer, nullptr, nullptr, bytes, flops};
+    for (cudaEvent_t* e : {&r.a, &r.b}) {
+        if (!h->ev_pool.empty()) {
+            *e = h->ev_pool.back();
+            h->ev_pool.pop_back();
+        } else {
+            cudaEventCreate(e);
+        }
+    }
+    cudaEventRecord(r.a, h->stream);
+    h->prof_recs.push_back(r);
+}
+
+void prof_stop(smlp_handle* h) {
+    if (!h->prof || h->prof_recs.empty()) return;
+    cudaEventRecord(h->prof_recs.back().b, h->stream);
+}
+
 }  // namespace smlp
 
 using namespace smlp;
@@ -266,11 +286,60 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
 int sparse_mlp_destroy(smlp_handle* h) {
     if (!h) return SMLP_OK;
     cudaStreamSynchronize(h->stream);
+    for (auto& r : h->prof_recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : h->ev_pool) cudaEventDestroy(e);
     for (auto& a : h->allocs) tmp_free(h, a.ptr, a.bytes);
     h->allocs.clear();
     if (h->x_stage || h->y_stage) { /* tracked above */ }
     cudaStreamSynchronize(h->stream);
     delete h;
+    return SMLP_OK;
+}
+
+int sparse_mlp_profile(smlp_handle* h, int32_t enable) {
+    if (!h) return SMLP_E_ARG;
+    if (enable) {
+        for (auto& r : h->prof_recs) {
+            h->ev_pool.push_back(r.a);
+            h->ev_pool.push_back(r.b);
+        }
+        h->prof_recs.clear();
+    }
+    h->prof = enable != 0;
+    return SMLP_OK;
+}
+
+int sparse_mlp_profile_read(smlp_handle* h, smlp_kernel_stat* out, int32_t cap, int32_t* n) {
+    if (!h || !n) return SMLP_E_ARG;
+    SMLP_CK(h, cudaStreamSynchronize(h->stream));
+    std::vector<smlp_kernel_stat> agg;
+    for (auto& r : h->prof_recs) {
+        float ms = 0.f;
+        SMLP_CK(h, cudaEventElapsedTime(&ms, r.a, r.b));
+        smlp_kernel_stat* s = nullptr;
+        for (auto& a : agg)
+            if (a.kind == r.kind && a.layer == r.layer) s = &a;
+        if (!s) {
+            agg.push_back(smlp_kernel_stat{r.kind, r.layer, 0, 0.0, 0.0, 0.0});
+            s = &agg.back();
+        }
+        // running mean of the per-launch algorithmic figures (chunks may differ in width)
+        s->bytes_per_launch = (s->bytes_per_launch * (double)s->launches + r.bytes) / (double)(s->launches + 1);
+        s->flops_per_launch = (s->flops_per_launch * (double)s->launches + r.flops) / (double)(s->launches + 1);
+        s->launches += 1;
+        s->total_ms += ms;
+    }
+    *n = (int32_t)agg.size();
+    for (int32_t k = 0; k < std::min<int32_t>(cap, *n); ++k) out[k] = agg[(size_t)k];
+    return SMLP_OK;
+}
+
+int sparse_mlp_set_step_counter(smlp_handle* h, const uint64_t* dev_counter) {
+    if (!h) return SMLP_E_ARG;
+    h->step_counter = dev_counter;
     return SMLP_OK;
 }
 

@@ -79,6 +79,14 @@ struct Alloc {
     void* ptr;
 };
 
+enum KernelKind { K_STAGE = 0, K_FWD = 1, K_FWD_FINISH = 2, K_SOFTMAX = 3, K_BWD = 4, K_BWD_FINISH = 5, K_SGD = 6 };
+
+struct ProfRec {
+    int kind, layer;
+    cudaEvent_t a, b;
+    double bytes, flops;
+};
+
 }  // namespace smlp
 
 struct smlp_handle {
@@ -127,6 +135,10 @@ struct smlp_handle {
     bool grads_pending = false;
 
     uint64_t version = 0;
+    const uint64_t* step_counter = nullptr;   // device dropout-step source (graph replay)
+    bool prof = false;
+    std::vector<smlp::ProfRec> prof_recs;
+    std::vector<cudaEvent_t> ev_pool;
     int num_sms = 148;
     int64_t launches = 0;
     std::string err;
@@ -155,6 +167,10 @@ int check_cuda(smlp_handle* h, cudaError_t e, const char* what);
         int _rc = (call);          \
         if (_rc != SMLP_OK) return _rc; \
     } while (0)
+
+// per-kernel CUDA-event timing (no-ops unless h->prof)
+void prof_start(smlp_handle* h, int kind, int layer, double bytes, double flops);
+void prof_stop(smlp_handle* h);
 
 // allocation through the caller's allocator (or cudaMallocAsync); tracked for destroy
 void* dev_alloc(smlp_handle* h, size_t bytes);

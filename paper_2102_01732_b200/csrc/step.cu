@@ -106,13 +106,14 @@ struct FwdArgs {
     int rank;
     int layer;
     uint32_t step_lo;
+    const uint64_t* step_ptr; // device dropout-step source (graph replay) or null
     int b0;                   // global batch index of column 0 of this chunk
 };
 
 // Epilogue of one output neuron row j: all 32 lanes call it (ballots); lanes of group 0
 // (lane < G) own batch columns 4q..4q+3 of the chunk.
 template <int CB>
-__device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4 acc, int lane) {
+__device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4 acc, int lane, uint32_t step_lo) {
     constexpr int G = CB / 4;
     const bool own = lane < G;
     const int q = lane % G;
@@ -134,7 +135,7 @@ __device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4
         if (A.dropout_on) {
             const uint64_t b = (uint64_t)(A.b0 + q * 4 + c);
             const uint64_t e = b * (uint64_t)A.n_out + (uint64_t)j;
-            const uint4 r = rng_stream(A.seed, P_DROPOUT, A.rank, A.layer, A.step_lo, e >> 2);
+            const uint4 r = rng_stream(A.seed, P_DROPOUT, A.rank, A.layer, step_lo, e >> 2);
             keep = word(r, (int)(e & 3)) >= A.drop_thr;
             a = keep ? a * A.keep_scale : 0.f;
         }
@@ -192,11 +193,12 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs A) {
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int nseg = A.meta->n_fseg;
     constexpr int G = CB / 4;
+    const uint32_t step_lo = A.step_ptr ? (uint32_t)(*A.step_ptr) : A.step_lo;
     for (int s = warp; s < nseg; s += nwarps) {
         const int4 sg = A.seg[s];
         const float4 acc = fwd_segment<CB>(A, sg.y, sg.z, lane);
         if (sg.w < 0) {
-            fwd_epilogue<CB>(A, sg.x, acc, lane);
+            fwd_epilogue<CB>(A, sg.x, acc, lane, step_lo);
         } else if (lane < G) {
             st4(A.ws + (int64_t)sg.w * CB + lane * 4, acc);
         }
@@ -211,6 +213,7 @@ __global__ void __launch_bounds__(256) fwd_finish_kernel(FwdArgs A) {
     const int nm = A.meta->n_fmulti;
     constexpr int G = CB / 4;
     const int q = lane % G;
+    const uint32_t step_lo = A.step_ptr ? (uint32_t)(*A.step_ptr) : A.step_lo;
     for (int r = warp; r < nm; r += nwarps) {
         const int4 m = A.multi[r];
         float4 acc = f4zero();
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(256) fwd_finish_kernel(FwdArgs A) {
             const float4 p = ldg4(A.ws + (int64_t)(m.y + t) * CB + q * 4);
             acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
         }
-        fwd_epilogue<CB>(A, m.x, acc, lane);
+        fwd_epilogue<CB>(A, m.x, acc, lane, step_lo);
     }
 }
 
@@ -575,8 +578,10 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
     const int nchunks = (B + CB - 1) / CB;
     {
         dim3 grid((unsigned)((h->sizes[0] + 31) / 32), (unsigned)((nchunks * CB + 31) / 32));
+        prof_start(h, K_STAGE, 1, 8.0 * (double)B * (double)h->sizes[0], 0.0);
         stage_input_kernel<<<grid, dim3(32, 32), 0, h->stream>>>(x, x_idx, B, nchunks, CB, h->sizes[0], h->act[1]);
         SMLP_CK_LAUNCH(h, "stage_input_kernel");
+        prof_stop(h);
     }
     const bool drop = train && h->dropout > 0.f;
     for (int c = 0; c < nchunks; ++c) {
@@ -607,8 +612,13 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             A.rank = h->rank;
             A.layer = l;
             A.step_lo = (uint32_t)step;
+            A.step_ptr = h->step_counter;
             A.b0 = c * CB;
+            const int Bc = std::min(CB, B - c * CB);
+            const double nnz = (double)Ly.nnz;
+            prof_start(h, K_FWD, l, 12.0 * nnz / nchunks + 4.0 * Bc * (double)(nin + nout), 2.0 * nnz * Bc);
             SMLP_TRY(dispatch_fwd(h, A, Ly));
+            prof_stop(h);
         }
     }
     if (probs) SMLP_TRY(run_probs(h, B, probs));
@@ -648,8 +658,10 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
         S.fused = is_fused ? 1 : 0;
         S.lr = lr;
         S.mu = mu;
+        prof_start(h, K_SOFTMAX, L, 8.0 * (double)B * (double)S.nL, 0.0);
         softmax_ce_kernel<<<1, 512, 0, h->stream>>>(S);
         SMLP_CK_LAUNCH(h, "softmax_ce_kernel");
+        prof_stop(h);
     }
     for (int l = L; l >= 2; --l) {
         Layer& Ly = h->layers[l - 2];
@@ -684,7 +696,13 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.lr = lr;
             A.mu = mu;
             A.wd = wd;
+            const int Bc = std::min(CB, B - c * CB);
+            const double nnz = (double)Ly.nnz;
+            const double act_bytes = 4.0 * Bc * (double)(nin + nout + (has_dprev ? nin : 0));
+            prof_start(h, K_BWD, l, (is_fused ? 20.0 : 12.0) * nnz / nchunks + act_bytes,
+                       (has_dprev ? 4.0 : 2.0) * nnz * Bc);
             SMLP_TRY(dispatch_bwd(h, A, Ly, has_dprev));
+            prof_stop(h);
         }
     }
     return SMLP_OK;
@@ -694,9 +712,11 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
     const int threads = 256;
     const int64_t n = h->param_count;
     const int grid = (int)std::min<int64_t>((n + threads - 1) / threads, (int64_t)h->num_sms * 16);
+    prof_start(h, K_SGD, 0, 20.0 * (double)n, 0.0);
     sgd_update_kernel<<<grid, threads, 0, h->stream>>>(h->param, h->mom, h->grad, n, h->bias_base, sgd->lr,
                                                        sgd->momentum, sgd->weight_decay, sgd->grad_scale);
     SMLP_CK_LAUNCH(h, "sgd_update_kernel");
+    prof_stop(h);
     return SMLP_OK;
 }
 

@@ -1,0 +1,105 @@
+"""Synchronous data parallelism for the sparse MLP (WASSP-SGD phase 1).
+
+One process per GPU; every rank holds the full, identical replica (same seed -> same ER topology,
+same values).  Per step every rank runs forward + unfused backward on its own minibatch, the
+contiguous grad view is SUM-allreduced over the process group (NCCL over NVLink / NVSwitch on
+B200 boxes; gloo in the CPU tests), and every rank applies the same Eq. 1 update with
+grad_scale = 1/K, so replicas stay bit-identical.  SET evolution and importance pruning are
+deterministic functions of (seed, evolve index, weights) and run replicated with no collective.
+Averaging points (Eq. 2) allreduce the param view and divide by K.
+
+The learning rate follows the "gradual warmup and linear scaling rule" of PAPER.md:323
+(DESIGN reading R20): eta_t = eta (1 + (K - 1) min(1, t / warmup_steps)).
+"""
+from __future__ import annotations
+
+import os
+from typing import Optional, Tuple
+
+import numpy as np
+
+
+def init_process_group(backend: Optional[str] = None) -> Tuple[int, int, int]:
+    """(rank, world, local_rank) from the torchrun environment; world 1 without one."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend is None:
+            import torch
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend, rank=rank, world_size=world)
+    return rank, world, local
+
+
+def scaled_lr(base_lr: float, world: int, step: int, warmup_steps: int) -> float:
+    if world <= 1:
+        return base_lr
+    frac = 1.0 if warmup_steps <= 0 else min(1.0, step / float(warmup_steps))
+    return base_lr * (1.0 + (world - 1) * frac)
+
+
+def shard_bounds(n: int, rank: int, world: int) -> Tuple[int, int]:
+    """Rank k owns samples [k n / K, (k+1) n / K) of the (globally permuted) training set."""
+    return (rank * n) // world, ((rank + 1) * n) // world
+
+
+def allreduce_sum_(t, group=None):
+    """In-place SUM allreduce of a flat tensor (the grad view, X1)."""
+    import torch.distributed as dist
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def average_(t, group=None):
+    """Eq. 2 on a flat parameter tensor: SUM allreduce then / K (X2)."""
+    import torch.distributed as dist
+    if dist.is_initialized():
+        K = dist.get_world_size(group)
+        if K > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            t.div_(K)
+    return t
+
+
+def tensor_hash(t) -> int:
+    """64-bit hash of a float32 tensor's bit pattern (X3 replica-identity check)."""
+    import torch
+    bits = t.detach().contiguous().view(torch.int32).to(torch.int64).cpu().numpy().astype(np.uint64)
+    idx = np.arange(1, len(bits) + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        h = np.bitwise_xor.reduce(bits * np.uint64(0x9E3779B97F4A7C15) + idx * np.uint64(0xC2B2AE3D27D4EB4F))
+        h = int(h) ^ int(np.sum(bits * idx, dtype=np.uint64))
+    return h & ((1 << 63) - 1)
+
+
+def replicas_identical(t, group=None) -> bool:
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return True
+    h = torch.tensor([tensor_hash(t)], dtype=torch.int64, device=t.device)
+    hs = [torch.zeros_like(h) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(hs, h, group=group)
+    return all(int(x.item()) == int(h.item()) for x in hs)
+
+
+def dp_train_step(model, X, Y, idx, step: int, lr: float, momentum: float, weight_decay: float,
+                  world: int, loss=None, group=None):
+    """One synchronous step on this rank: forward / unfused backward on the local batch, X1
+    allreduce of the grad view, Eq. 1 update with grad_scale = 1/K (identical on every rank)."""
+    from .sparse_mlp import SGD
+    if world == 1:
+        model.forward(X, x_idx=idx, train=True, step=step)
+        model.backward(Y, y_idx=idx, loss=loss, fused=SGD(lr, momentum, weight_decay))
+        return
+    model.forward(X, x_idx=idx, train=True, step=step)
+    model.backward(Y, y_idx=idx, loss=loss, fused=None)
+    g, _ = model.grad_view()
+    allreduce_sum_(g, group)
+    model.step(SGD(lr, momentum, weight_decay, 1.0 / world))

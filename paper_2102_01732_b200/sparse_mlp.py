@@ -34,7 +34,10 @@ EXPORTED = [
     "sparse_mlp_importance", "sparse_mlp_info", "sparse_mlp_export_layer", "sparse_mlp_import_layer",
     "sparse_mlp_export_bias", "sparse_mlp_import_bias", "sparse_mlp_export_alive",
     "sparse_mlp_import_alive", "sparse_mlp_export_trace", "sparse_mlp_last_error", "sparse_mlp_version",
+    "sparse_mlp_profile", "sparse_mlp_profile_read", "sparse_mlp_set_step_counter",
 ]
+KERNEL_KINDS = {0: "stage_input", 1: "fwd", 2: "fwd_finish", 3: "softmax_ce", 4: "bwd", 5: "bwd_finish",
+                6: "sgd_update"}
 
 
 class SparseMLPError(RuntimeError):
@@ -62,6 +65,11 @@ class smlp_config(C.Structure):
 class smlp_sgd(C.Structure):
     _fields_ = [("lr", C.c_float), ("momentum", C.c_float), ("weight_decay", C.c_float),
                 ("grad_scale", C.c_float)]
+
+
+class smlp_kernel_stat(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("layer", C.c_int32), ("launches", C.c_int64), ("total_ms", C.c_double),
+                ("bytes_per_launch", C.c_double), ("flops_per_launch", C.c_double)]
 
 
 class smlp_info(C.Structure):
@@ -107,6 +115,9 @@ def load_library(path: str = LIB_PATH):
         "sparse_mlp_export_alive": (I32, [VP, I32, VP]),
         "sparse_mlp_import_alive": (I32, [VP, I32, VP]),
         "sparse_mlp_export_trace": (I32, [VP, I32, I32, VP]),
+        "sparse_mlp_profile": (I32, [VP, I32]),
+        "sparse_mlp_profile_read": (I32, [VP, P(smlp_kernel_stat), I32, P(I32)]),
+        "sparse_mlp_set_step_counter": (I32, [VP, VP]),
         "sparse_mlp_last_error": (C.c_char_p, [VP]),
         "sparse_mlp_version": (C.c_char_p, []),
     }
@@ -327,6 +338,23 @@ class SparseMLP:
         if kind == 2:
             out = out[: self.sparse_mlp_info()["nnz"][l - 1]]
         return out
+
+    # -------------------------------------------------------------------------------- timing / graphs
+    def sparse_mlp_profile(self, enable: bool):
+        self._check(self.lib.sparse_mlp_profile(self.h, int(bool(enable))))
+
+    def sparse_mlp_profile_read(self) -> list:
+        cap = 64
+        arr = (smlp_kernel_stat * cap)()
+        n = C.c_int32(0)
+        self._check(self.lib.sparse_mlp_profile_read(self.h, arr, cap, C.byref(n)))
+        return [{"kernel": KERNEL_KINDS.get(a.kind, str(a.kind)), "layer": a.layer, "launches": a.launches,
+                 "total_ms": a.total_ms, "bytes_per_launch": a.bytes_per_launch,
+                 "flops_per_launch": a.flops_per_launch} for a in arr[: min(cap, n.value)]]
+
+    def sparse_mlp_set_step_counter(self, counter=None):
+        """counter: a CUDA uint64/int64 tensor holding the dropout step (graph replay), or None."""
+        self._check(self.lib.sparse_mlp_set_step_counter(self.h, _ptr(counter)))
 
     # short aliases
     forward = sparse_mlp_forward
