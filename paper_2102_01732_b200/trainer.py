@@ -1,0 +1,160 @@
+"""Epoch driver for the sparse MLP (Alg. 2; SURVEY.md §3 call stacks 3-4).
+
+Per epoch: the rank's shard is reshuffled (Alg. 1), every full minibatch runs the hot path
+(forward, backward, Eq. 1 update; for K > 1 the grad-view allreduce and the update kernel), the
+last partial batch is kept and normalised by its own size; at the epoch end, when
+scheduled, Importance Pruning runs first and SET evolution second (Alg. 2 order, reading R18),
+replicated on every rank with no communication.  Evolution is skipped after the final epoch
+(reading R10).
+
+Full batches replay one CUDA graph of ``graph_steps`` captured steps (forward + backward + the
+dropout-counter increment), reading their sample indices from a static device window that is
+refilled before each replay; the graph stays valid across evolve / prune because the library
+keeps every device pointer stable and reads its work-list sizes from device memory.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from .dp import allreduce_sum_, average_, scaled_lr, shard_bounds
+from .sparse_mlp import SGD, SparseMLP
+
+
+@dataclass
+class EpochRecord:
+    epoch: int
+    loss: float
+    samples: int
+    train_s: float
+    evolve_s: float
+    prune_s: float
+    nnz: List[int]
+    alive: List[int]
+    removed: List[int] = field(default_factory=list)
+    pruned: List[int] = field(default_factory=list)
+
+
+class Trainer:
+    def __init__(self, model: SparseMLP, cfg, X, Y, rank: int = 0, world: int = 1, use_graph: bool = True,
+                 graph_steps: int = 8, group=None, average_every_epoch: bool = False):
+        import torch
+        self.torch = torch
+        self.m = model
+        self.cfg = cfg
+        self.X, self.Y = X, Y                 # resident device tensors of this rank's shard
+        self.rank, self.world, self.group = rank, world, group
+        self.B = cfg.batch
+        self.use_graph = use_graph and world == 1
+        self.graph_steps = graph_steps
+        self.average_every_epoch = average_every_epoch
+        self.n = X.shape[0]
+        self.global_step = 0
+        self.dev = X.device
+        self.counter = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.loss_buf = torch.zeros(max(1, graph_steps), dtype=torch.float32, device=self.dev)
+        self.idx_win = torch.zeros(self.B * max(1, graph_steps), dtype=torch.int32, device=self.dev)
+        self.graph = None
+        self._graph_lr = None
+        self.warmup_steps = max(1, cfg.n_samples // (self.B * max(1, world)))
+
+    # ---------------------------------------------------------------------------------- batches
+    def epoch_order(self, epoch: int) -> np.ndarray:
+        return np.random.default_rng([self.cfg.data_seed, epoch, self.rank]).permutation(self.n).astype(np.int32)
+
+    def _sgd(self, step: int, grad_scale: float = 1.0) -> SGD:
+        lr = scaled_lr(self.cfg.lr, self.world, step, self.warmup_steps)
+        return SGD(lr, self.cfg.momentum, self.cfg.weight_decay, grad_scale)
+
+    def _eager_step(self, idx, loss_slot, step: int):
+        B = int(idx.shape[0])
+        self.m.forward(self.X, x_idx=idx, train=True, step=step)
+        if self.world == 1:
+            self.m.backward(self.Y, y_idx=idx, loss=loss_slot, fused=self._sgd(step))
+        else:
+            self.m.backward(self.Y, y_idx=idx, loss=loss_slot, fused=None)
+            g, _ = self.m.grad_view()
+            allreduce_sum_(g, self.group)
+            self.m.step(self._sgd(step, 1.0 / self.world))
+        return B
+
+    def _capture(self, lr: SGD):
+        torch = self.torch
+        self.m.sparse_mlp_set_step_counter(self.counter)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for k in range(self.graph_steps):
+                    idx = self.idx_win[k * self.B:(k + 1) * self.B]
+                    self.m.forward(self.X, x_idx=idx, train=True, step=0)
+                    self.m.backward(self.Y, y_idx=idx, loss=self.loss_buf[k:k + 1], fused=lr)
+                    self.counter.add_(1)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+        self._graph_lr = lr
+
+    # ---------------------------------------------------------------------------------- epoch
+    def train_epoch(self, epoch: int, last: bool = False) -> EpochRecord:
+        torch = self.torch
+        cfg = self.cfg
+        order = torch.from_numpy(self.epoch_order(epoch)).to(self.dev)
+        nfull = self.n // self.B
+        loss_sum = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        one = torch.zeros(1, dtype=torch.float32, device=self.dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s = 0
+        if self.use_graph and self.world == 1:
+            lr = self._sgd(self.global_step)
+            while s + self.graph_steps <= nfull:
+                if self.graph is None or self._graph_lr != lr:
+                    self.counter.fill_(self.global_step)
+                    self._capture(lr)
+                    # the capture does not execute: the counter is restored for the replay
+                self.counter.fill_(self.global_step)
+                self.idx_win.copy_(order[s * self.B:(s + self.graph_steps) * self.B])
+                self.graph.replay()
+                loss_sum += self.loss_buf.double().sum() * self.B
+                s += self.graph_steps
+                self.global_step += self.graph_steps
+            self.m.sparse_mlp_set_step_counter(None)
+        while s < nfull:
+            self._eager_step(order[s * self.B:(s + 1) * self.B], one, self.global_step)
+            loss_sum += one.double() * self.B
+            s += 1
+            self.global_step += 1
+        tail = self.n - nfull * self.B
+        if tail > 0:
+            self._eager_step(order[nfull * self.B:], one, self.global_step)
+            loss_sum += one.double() * tail
+            self.global_step += 1
+        torch.cuda.synchronize()
+        train_s = time.perf_counter() - t0
+        loss = float(loss_sum.item()) / self.n
+        # ---- epoch boundary: Eq. 2 averaging (periodic, optional), pruning, evolution
+        if self.average_every_epoch and self.world > 1:
+            p, _ = self.m.param_view()
+            average_(p, self.group)
+        prune_s = evolve_s = 0.0
+        pruned, removed = [], []
+        if cfg.prune and epoch % cfg.prune_every == 0 and epoch >= cfg.prune_start:
+            t1 = time.perf_counter()
+            pruned, _ = self.m.prune_neurons(cfg.prune_percentile)
+            torch.cuda.synchronize()
+            prune_s = time.perf_counter() - t1
+        if not last:
+            t1 = time.perf_counter()
+            removed = self.m.evolve_topology(cfg.zeta, epoch)
+            torch.cuda.synchronize()
+            evolve_s = time.perf_counter() - t1
+        inf = self.m.info()
+        return EpochRecord(epoch, loss, self.n, train_s, evolve_s, prune_s, inf["nnz"], inf["alive"], removed,
+                           pruned)
+
+    def fit(self, epochs: int) -> List[EpochRecord]:
+        return [self.train_epoch(e, last=(e == epochs - 1)) for e in range(epochs)]
