@@ -174,6 +174,10 @@ int sparse_mlp_train_step_host(smlp_handle* h, const float* x_host, const int32_
 int sparse_mlp_grad_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version);
 int sparse_mlp_param_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version);
 
+/* Call after writing the param view directly (e.g. the Eq. 2 averaging allreduce): refreshes
+ * the forward's mirror-ordered copy of the weights.  Asynchronous, graph-capturable. */
+int sparse_mlp_params_updated(smlp_handle* h);
+
 /* sparse_mlp_evolve_topology — Alg. 2 PAPER.md:659-664 on every weight layer that is not
  * dense-capped: per sign class k = floor(zeta n_+/-), remove the k positives and the k
  * negatives closest to zero (key: |w| bits, canonical index; R5-R7), regrow R = k_+ + k_-

@@ -170,6 +170,8 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
         Ly.mrow_ptr = zalloc<int32_t>(h, (size_t)Ly.n_out + 1, &rc);
         Ly.msrc = zalloc<int32_t>(h, cap, &rc);
         Ly.mperm = zalloc<int32_t>(h, cap, &rc);
+        Ly.minv = zalloc<int32_t>(h, cap, &rc);
+        Ly.mval = zalloc<float>(h, cap, &rc);
         Ly.fseg_cap = Ly.n_out + Ly.cap / SEG_NNZ + 1;
         Ly.bseg_cap = Ly.n_in + Ly.cap / SEG_NNZ + 1;
         Ly.fslot_cap = Ly.n_in > SEG_NNZ ? 2 * (Ly.cap / SEG_NNZ) + 2 : 0;   // mirror rows <= n_in long
@@ -248,10 +250,20 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
         return set_err(nullptr, SMLP_E_ARG, "unknown activation");
     if (cfg->init < SMLP_INIT_NORMAL || cfg->init > SMLP_INIT_HE_U) return set_err(nullptr, SMLP_E_ARG, "unknown init");
     int CB = cfg->chunk_batch;
-    if (CB == 0) CB = std::min(128, next_pow2(std::max(4, cfg->max_batch)));
-    if (CB < 4 || CB > 128 || (CB & (CB - 1)))
+    if (CB != 0 && (CB < 4 || CB > 128 || (CB & (CB - 1))))
         return set_err(nullptr, SMLP_E_ARG, "chunk_batch must be a power of two in [4, 128]");
     if (cudaSetDevice(cfg->device) != cudaSuccess) return set_err(nullptr, SMLP_E_CUDA, "cudaSetDevice failed");
+    if (CB == 0) {
+        // auto: the widest chunk (<= 128 columns) whose largest activation slab n_l x CB x 4 B
+        // fits in half the L2, so the row gathers of a chunk pass hit in L2
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, cfg->device);
+        if (l2 <= 0) l2 = 126 << 20;
+        int64_t nmax = 0;
+        for (int l = 0; l < cfg->n_layers; ++l) nmax = std::max<int64_t>(nmax, cfg->sizes[l]);
+        CB = std::min(128, next_pow2(std::max(4, cfg->max_batch)));
+        while (CB > 4 && (double)nmax * CB * 4.0 > 0.5 * (double)l2) CB >>= 1;
+    }
 
     smlp_handle* h = new smlp_handle();
     h->L = cfg->n_layers;
@@ -334,6 +346,12 @@ int sparse_mlp_profile_read(smlp_handle* h, smlp_kernel_stat* out, int32_t cap, 
     }
     *n = (int32_t)agg.size();
     for (int32_t k = 0; k < std::min<int32_t>(cap, *n); ++k) out[k] = agg[(size_t)k];
+    return SMLP_OK;
+}
+
+int sparse_mlp_params_updated(smlp_handle* h) {
+    if (!h) return SMLP_E_ARG;
+    for (auto& Ly : h->layers) SMLP_TRY(refresh_mirror_values(h, Ly));
     return SMLP_OK;
 }
 

@@ -57,6 +57,8 @@ struct Layer {
     int32_t* mrow_ptr = nullptr;
     int32_t* msrc = nullptr;
     int32_t* mperm = nullptr;
+    int32_t* minv = nullptr;    // canonical index -> mirror position (inverse of mperm)
+    float* mval = nullptr;      // mirror-ordered copy of val (the forward reads it sequentially)
     // segment work lists: int4 (row, beg, end, slot) ; multi: int4 (row, first_slot, n_slots, 0)
     int64_t fseg_cap = 0, bseg_cap = 0, fslot_cap = 0, bslot_cap = 0;
     int4* fseg = nullptr;
@@ -260,6 +262,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
 int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss,
                  const smlp_sgd* fused);
 int run_step(smlp_handle* h, const smlp_sgd* sgd);
+int refresh_mirror_values(smlp_handle* h, Layer& Ly);
 
 // evolve.cu / prune.cu
 int run_evolve(smlp_handle* h, double zeta, uint64_t e, int64_t* removed);

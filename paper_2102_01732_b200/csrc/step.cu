@@ -1,19 +1,26 @@
 // step.cu — the per-minibatch hot path on sm_100a CUDA cores.
 //
 //   stage_input    a1  x[B x n_1] (optionally row-gathered by x_idx) -> act[1] chunked transposed
-//   fwd_kernel     a2/a3  z_l = a_{l-1} W^(l) + b_l over the output-major mirror, one warp per
-//                  <=SEG_NNZ-entry segment of an output row, G = CB/4 lanes per gathered row;
-//                  epilogue: All-ReLU (Eq. 3), inverted dropout, sign/keep bits
-//   fwd_finish     long rows split in several segments: fixed-order sum of the partials + epilogue
+//   fwd_kernel     a2/a3  z_l = a_{l-1} W^(l) + b_l over the output-major mirror.  A "group" of
+//                  G = CB/4 lanes owns one <= SEG_NNZ-entry segment of an output row (P = 32/G groups
+//                  per warp run in lock-step, predicated to the longest segment); each lane holds one
+//                  float4 of the CB batch columns; per block of G entries the group loads (src, w)
+//                  coalesced, broadcasts them by shuffle, and keeps G row gathers in flight (the next
+//                  block's indices are prefetched).  Epilogue: bias, All-ReLU (Eq. 3),
+//                  inverted dropout (Philox), sign / keep bit masks.
+//   fwd_finish     rows split into several segments: fixed-order sum of the partials + epilogue
 //   softmax_ce     a3  p = softmax(z_L), loss, delta_L = (p - onehot)/B, output-bias gradient
-//   bwd_kernel     a4/a5/a6  one warp per segment of an input row i of the canonical CSR:
-//                  gathers delta_l[j] once per entry, accumulates delta_{l-1}[i] += w_ij delta_l[j]
-//                  (SpMM against W^T), g_ij = <a_{l-1}[i], delta_l[j]> over the batch (SDDMM, a
-//                  transpose-reduction of G partial dots per lane), then the Eq. 1 update of
-//                  (w, v) in place (1-GPU fused path) or the gradient into the grad view
+//   bwd_kernel     a4/a5/a6  a group owns a segment of an input row i of the canonical CSR: per
+//                  entry it gathers delta_l[j] once, accumulates delta_{l-1}[i] += w_ij delta_l[j]
+//                  (SpMM against W^T) and the partial dot <a_{l-1}[i], delta_l[j]> (SDDMM); a
+//                  transpose reduction over the G lanes leaves lane q with the batch sum of entry q,
+//                  which it applies as the Eq. 1 update of (w, v) in place (1-GPU fused path, also
+//                  refreshing the forward's mirror-ordered copy of w) or writes to the grad view
 //   bwd_finish     multi-segment rows: fixed-order sum of the delta partials + epilogue
-//   sgd_update     a6 on the grad view after the caller's allreduce (K > 1)
+//   sgd_update     a6 on the grad view after the caller's allreduce (K > 1), then mirror refresh
 //
+// Batch chunks: with CB < B the batch is processed in ceil(B/CB) chunk launches so the gathered
+// activation slab (n x CB fp32) stays L2-resident; gradients accumulate over chunks in order.
 // No float atomics anywhere: every reduction has a fixed order, so results are deterministic.
 #include <cuda_runtime.h>
 
@@ -36,25 +43,23 @@ __device__ __forceinline__ void fma4(float4& acc, float w, const float4& x) {
     acc.z = fmaf(w, x.z, acc.z);
     acc.w = fmaf(w, x.w, acc.w);
 }
-__device__ __forceinline__ float4 shfl_xor4(float4 v, int m) {
-    v.x += __shfl_xor_sync(FULL, v.x, m);
-    v.y += __shfl_xor_sync(FULL, v.y, m);
-    v.z += __shfl_xor_sync(FULL, v.z, m);
-    v.w += __shfl_xor_sync(FULL, v.w, m);
-    return v;
-}
 __device__ __forceinline__ float comp(const float4& v, int c) {
     return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 __device__ __forceinline__ uint32_t word(const uint4& v, int c) {
     return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
+template <int G>
+__device__ __forceinline__ uint32_t group_bits(uint32_t ballot, int g) {
+    return G == 32 ? ballot : ((ballot >> (g * G)) & ((1u << G) - 1u));
+}
 
 // ------------------------------------------------------------------------------------------
 // a1: input staging (transpose + optional row gather), zero padding of columns b >= B
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) stage_input_kernel(const float* __restrict__ x, const int32_t* __restrict__ x_idx,
-                                   int B, int nchunks, int CB, int64_t n1, float* __restrict__ act1) {
+                                                           int B, int nchunks, int CB, int64_t n1,
+                                                           float* __restrict__ act1) {
     __shared__ float tile[32][33];
     const int64_t f0 = (int64_t)blockIdx.x * 32;
     const int b0 = blockIdx.y * 32;
@@ -91,9 +96,8 @@ struct FwdArgs {
     const int4* seg;
     const int4* multi;
     const LayerMeta* meta;
-    const int32_t* msrc;
-    const int32_t* mperm;
-    const float* val;
+    const int32_t* msrc;      // mirror: input neuron of each entry
+    const float* mval;        // mirror-ordered copy of the weights
     const float* bias;
     float* ws;
     int64_t n_out;
@@ -110,15 +114,15 @@ struct FwdArgs {
     int b0;                   // global batch index of column 0 of this chunk
 };
 
-// Epilogue of one output neuron row j: all 32 lanes call it (ballots); lanes of group 0
-// (lane < G) own batch columns 4q..4q+3 of the chunk.
+// Epilogue of one output row j per group: all 32 lanes call it (ballots); `own` marks the
+// groups whose row is complete here.  Lane q of a group owns batch columns 4q..4q+3 of the chunk.
 template <int CB>
-__device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4 acc, int lane, uint32_t step_lo) {
+__device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4 acc, bool own, int lane,
+                                             uint32_t step_lo) {
     constexpr int G = CB / 4;
-    const bool own = lane < G;
-    const int q = lane % G;
-    const float bj = __ldg(A.bias + j);
-    float4 z = make_float4(acc.x + bj, acc.y + bj, acc.z + bj, acc.w + bj);
+    const int g = lane / G, q = lane % G;
+    const float bj = own ? __ldg(A.bias + j) : 0.f;
+    const float4 z = make_float4(acc.x + bj, acc.y + bj, acc.z + bj, acc.w + bj);
     if (!A.hidden) {
         if (own) st4(A.a_out + j * CB + q * 4, z);
         return;
@@ -129,7 +133,7 @@ __device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4
     for (int c = 0; c < 4; ++c) {
         const float zc = comp(z, c);
         const bool pos = zc > 0.f;
-        zb[c] = __ballot_sync(FULL, own && pos);
+        zb[c] = group_bits<G>(__ballot_sync(FULL, own && pos), g);
         float a = pos ? zc : A.neg_slope * zc;
         bool keep = true;
         if (A.dropout_on) {
@@ -139,89 +143,99 @@ __device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4
             keep = word(r, (int)(e & 3)) >= A.drop_thr;
             a = keep ? a * A.keep_scale : 0.f;
         }
-        kb[c] = __ballot_sync(FULL, own && keep);
+        kb[c] = group_bits<G>(__ballot_sync(FULL, own && keep), g);
         out[c] = a;
     }
-    if (own) st4(A.a_out + j * CB + q * 4, make_float4(out[0], out[1], out[2], out[3]));
-    if (lane == 0) {
-        A.zmask[j] = make_uint4(zb[0], zb[1], zb[2], zb[3]);
-        if (A.dropout_on) A.kmask[j] = make_uint4(kb[0], kb[1], kb[2], kb[3]);
+    if (own) {
+        st4(A.a_out + j * CB + q * 4, make_float4(out[0], out[1], out[2], out[3]));
+        if (q == 0) {
+            A.zmask[j] = make_uint4(zb[0], zb[1], zb[2], zb[3]);
+            if (A.dropout_on) A.kmask[j] = make_uint4(kb[0], kb[1], kb[2], kb[3]);
+        }
     }
 }
 
+// Gather-accumulate of one segment [beg, end) per group (groups in lock-step up to maxblk).
 template <int CB>
-__device__ __forceinline__ float4 fwd_segment(const FwdArgs& A, int beg, int end, int lane) {
-    constexpr int G = CB / 4, P = 32 / G;
-    constexpr int U = (32 / P) < 8 ? (32 / P) : 8;
-    const int g = lane / G, q = lane % G;
+__device__ __forceinline__ float4 fwd_segment(const FwdArgs& A, int beg, int end, int maxblk, int lane) {
+    constexpr int G = CB / 4;
+    constexpr int U = G < 8 ? G : 8;
+    const int g = lane / G, q = lane % G, gbase = g * G;
     float4 acc = f4zero();
-    for (int k0 = beg; k0 < end; k0 += 32) {
-        const int n = min(32, end - k0);
-        int src = 0;
-        float w = 0.f;
-        if (lane < n) {
-            src = __ldg(A.msrc + k0 + lane);
-            w = __ldg(A.val + __ldg(A.mperm + k0 + lane));
+    int k = beg + q;
+    int src = 0;
+    float w = 0.f;
+    if (k < end) {
+        src = __ldg(A.msrc + k);
+        w = __ldg(A.mval + k);
+    }
+    for (int b = 0; b < maxblk; ++b) {
+        const int kn = k + G;                          // prefetch the next block's entries
+        int src_n = 0;
+        float w_n = 0.f;
+        if (kn < end) {
+            src_n = __ldg(A.msrc + kn);
+            w_n = __ldg(A.mval + kn);
         }
+        const int base = beg + b * G;
 #pragma unroll
-        for (int t0 = 0; t0 < 32; t0 += P * U) {
-            if (t0 >= n) break;
+        for (int u0 = 0; u0 < G; u0 += U) {
             float4 x[U];
             float wv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int t = t0 + u * P + g;
-                const int s = __shfl_sync(FULL, src, t & 31);
-                const float ww = __shfl_sync(FULL, w, t & 31);
-                const bool ok = t < n;
-                wv[u] = ok ? ww : 0.f;
-                x[u] = ok ? ldg4(A.a_prev + (int64_t)s * CB + q * 4) : f4zero();
+                const int s = __shfl_sync(FULL, src, gbase + u0 + u);
+                wv[u] = __shfl_sync(FULL, w, gbase + u0 + u);
+                x[u] = (base + u0 + u < end) ? ldg4(A.a_prev + (int64_t)s * CB + q * 4) : f4zero();
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) fma4(acc, wv[u], x[u]);
         }
+        k = kn;
+        src = src_n;
+        w = w_n;
     }
-#pragma unroll
-    for (int m = G; m < 32; m <<= 1) acc = shfl_xor4(acc, m);
     return acc;
 }
 
 template <int CB>
 __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs A) {
-    const int lane = threadIdx.x & 31;
+    constexpr int G = CB / 4, P = 32 / G;
+    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int nseg = A.meta->n_fseg;
-    constexpr int G = CB / 4;
     const uint32_t step_lo = A.step_ptr ? (uint32_t)(*A.step_ptr) : A.step_lo;
-    for (int s = warp; s < nseg; s += nwarps) {
-        const int4 sg = A.seg[s];
-        const float4 acc = fwd_segment<CB>(A, sg.y, sg.z, lane);
-        if (sg.w < 0) {
-            fwd_epilogue<CB>(A, sg.x, acc, lane, step_lo);
-        } else if (lane < G) {
-            st4(A.ws + (int64_t)sg.w * CB + lane * 4, acc);
-        }
+    for (int s0 = warp * P; s0 < nseg; s0 += nwarps * P) {
+        const int s = s0 + g;
+        const bool active = s < nseg;
+        const int4 sg = active ? A.seg[s] : make_int4(0, 0, 0, -2);
+        const int nblk = (sg.z - sg.y + G - 1) / G;
+        const int maxblk = __reduce_max_sync(FULL, nblk);
+        const float4 acc = fwd_segment<CB>(A, sg.y, sg.z, maxblk, lane);
+        fwd_epilogue<CB>(A, sg.x, acc, active && sg.w < 0, lane, step_lo);
+        if (active && sg.w >= 0) st4(A.ws + (int64_t)sg.w * CB + q * 4, acc);
     }
 }
 
 template <int CB>
 __global__ void __launch_bounds__(256) fwd_finish_kernel(FwdArgs A) {
-    const int lane = threadIdx.x & 31;
+    constexpr int G = CB / 4, P = 32 / G;
+    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int nm = A.meta->n_fmulti;
-    constexpr int G = CB / 4;
-    const int q = lane % G;
     const uint32_t step_lo = A.step_ptr ? (uint32_t)(*A.step_ptr) : A.step_lo;
-    for (int r = warp; r < nm; r += nwarps) {
-        const int4 m = A.multi[r];
+    for (int r0 = warp * P; r0 < nm; r0 += nwarps * P) {
+        const int r = r0 + g;
+        const bool active = r < nm;
+        const int4 m = active ? A.multi[r] : make_int4(0, 0, 0, 0);
         float4 acc = f4zero();
         for (int t = 0; t < m.z; ++t) {          // fixed order: slot first .. first + n - 1
             const float4 p = ldg4(A.ws + (int64_t)(m.y + t) * CB + q * 4);
             acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
         }
-        fwd_epilogue<CB>(A, m.x, acc, lane, step_lo);
+        fwd_epilogue<CB>(A, m.x, acc, active, lane, step_lo);
     }
 }
 
@@ -233,7 +247,6 @@ struct SoftmaxArgs {
     float* delta;             // delta[L] same layout
     const int32_t* labels;
     const int32_t* y_idx;
-    float* probs;             // [B x n_L] or null
     float* loss;              // scalar or null
     int32_t* err;
     float* bias;              // b_L
@@ -274,7 +287,6 @@ __global__ void __launch_bounds__(512) softmax_ce_kernel(SoftmaxArgs A) {
         for (int64_t j = 0; j < A.nL; ++j) {
             const float p = expf(zc[j * A.CB] - mx) * inv;
             dc[j * A.CB] = (p - (j == y ? 1.f : 0.f)) * invB;
-            if (A.probs) A.probs[(int64_t)b * A.nL + j] = p;
         }
     }
     red[tid] = lsum;
@@ -301,6 +313,20 @@ __global__ void __launch_bounds__(512) softmax_ce_kernel(SoftmaxArgs A) {
     }
 }
 
+__global__ void softmax_probs_kernel(const float* __restrict__ logits, float* __restrict__ probs, int64_t nL, int B,
+                                     int CB) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const int c = b / CB, lb = b % CB;
+    const float* zc = logits + (int64_t)c * nL * CB + lb;
+    float mx = -INFINITY;
+    for (int64_t j = 0; j < nL; ++j) mx = fmaxf(mx, zc[j * CB]);
+    float s = 0.f;
+    for (int64_t j = 0; j < nL; ++j) s += expf(zc[j * CB] - mx);
+    const float inv = 1.0f / s;
+    for (int64_t j = 0; j < nL; ++j) probs[(int64_t)b * nL + j] = expf(zc[j * CB] - mx) * inv;
+}
+
 // ------------------------------------------------------------------------------------------
 // backward (delta SpMM against W^T + SDDMM + fused update)
 // ------------------------------------------------------------------------------------------
@@ -317,6 +343,8 @@ struct BwdArgs {
     float* val;
     float* mom;
     float* grad;
+    float* mval;              // mirror-ordered copy of w (refreshed by the fused update)
+    const int32_t* minv;      // canonical index -> mirror position
     float* ws;
     float* bgs;               // [n_in] bias-grad accumulator over chunks
     float* bias_prev;
@@ -330,30 +358,31 @@ struct BwdArgs {
     float lr, mu, wd;
 };
 
-// Epilogue for delta_{l-1} of input row i: apply f'(z) (sign bits) and the dropout keep
-// bits, store, and the bias gradient of layer l-1 (accumulated across chunks in order).
+// delta_{l-1} of input row i per group: f'(z) from the sign bits, dropout keep bits, store, and
+// the bias gradient of layer l-1 (accumulated across chunks in order).
 template <int CB>
-__device__ __forceinline__ void bwd_epilogue(const BwdArgs& A, int64_t i, float4 d, int lane) {
+__device__ __forceinline__ void bwd_epilogue(const BwdArgs& A, int64_t i, float4 d, bool own, int lane) {
     constexpr int G = CB / 4;
-    const bool own = lane < G;
     const int q = lane % G;
-    const uint4 zb = A.zmask_prev[i];
-    uint4 kb = make_uint4(FULL, FULL, FULL, FULL);
-    if (A.dropout_prev) kb = A.kmask_prev[i];
-    float o[4];
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    if (own) {
+        const uint4 zb = A.zmask_prev[i];
+        uint4 kb = make_uint4(FULL, FULL, FULL, FULL);
+        if (A.dropout_prev) kb = A.kmask_prev[i];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const bool pos = (word(zb, c) >> q) & 1u;
-        const bool keep = (word(kb, c) >> q) & 1u;
-        const float fp = pos ? 1.f : A.neg_slope_prev;
-        const float v = comp(d, c) * fp;
-        o[c] = A.dropout_prev ? (keep ? v * A.keep_scale_prev : 0.f) : v;
+        for (int c = 0; c < 4; ++c) {
+            const bool pos = (word(zb, c) >> q) & 1u;
+            const bool keep = (word(kb, c) >> q) & 1u;
+            const float fp = pos ? 1.f : A.neg_slope_prev;
+            const float v = comp(d, c) * fp;
+            o[c] = A.dropout_prev ? (keep ? v * A.keep_scale_prev : 0.f) : v;
+        }
+        st4(A.d_prev + i * CB + q * 4, make_float4(o[0], o[1], o[2], o[3]));
     }
-    if (own) st4(A.d_prev + i * CB + q * 4, make_float4(o[0], o[1], o[2], o[3]));
-    float s = own ? (o[0] + o[1]) + (o[2] + o[3]) : 0.f;
+    float s = (o[0] + o[1]) + (o[2] + o[3]);
 #pragma unroll
     for (int m = 1; m < G; m <<= 1) s += __shfl_xor_sync(FULL, s, m);
-    if (lane == 0) {
+    if (own && q == 0) {
         float tot = s;
         if (A.chunk > 0) tot += A.bgs[i];
         if (A.chunk + 1 < A.nchunks) {
@@ -373,46 +402,55 @@ __global__ void __launch_bounds__(256) bwd_kernel(BwdArgs A) {
     constexpr int G = CB / 4, P = 32 / G;
     constexpr int U = G < 8 ? G : 8;
     const int lane = threadIdx.x & 31;
-    const int g = lane / G, q = lane % G;
+    const int g = lane / G, q = lane % G, gbase = g * G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int nseg = A.meta->n_bseg;
     const bool first_chunk = A.chunk == 0, last_chunk = A.chunk + 1 == A.nchunks;
-    for (int s = warp; s < nseg; s += nwarps) {
-        const int4 sg = A.seg[s];
+    for (int s0 = warp * P; s0 < nseg; s0 += nwarps * P) {
+        const int s = s0 + g;
+        const bool active = s < nseg;
+        const int4 sg = active ? A.seg[s] : make_int4(0, 0, 0, -2);
         const int64_t i = sg.x;
-        const float4 ai = ldg4(A.a_prev + i * CB + q * 4);
+        const int beg = sg.y, end = sg.z;
+        const int maxblk = __reduce_max_sync(FULL, (end - beg + G - 1) / G);
+        const float4 ai = active ? ldg4(A.a_prev + i * CB + q * 4) : f4zero();
         float4 dacc = f4zero();
-        for (int k0 = sg.y; k0 < sg.z; k0 += 32) {
-            const int n = min(32, sg.z - k0);
-            int jcol = 0;
-            float w = 0.f;
-            if (lane < n) {
-                jcol = __ldg(A.col + k0 + lane);
-                w = A.val[k0 + lane];
+        int k = beg + q;
+        int jcol = 0;
+        float w = 0.f;
+        if (k < end) {
+            jcol = __ldg(A.col + k);
+            w = A.val[k];
+        }
+        for (int b = 0; b < maxblk; ++b) {
+            const int kn = k + G;                      // prefetch the next block's entries
+            int jcol_n = 0;
+            float w_n = 0.f;
+            if (kn < end) {
+                jcol_n = __ldg(A.col + kn);
+                w_n = A.val[kn];
             }
+            const int base = beg + b * G;
             float p[G];
 #pragma unroll
-            for (int it0 = 0; it0 < G; it0 += U) {
+            for (int u0 = 0; u0 < G; u0 += U) {
                 float4 dx[U];
                 float wv[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int t = (it0 + u) * P + g;
-                    const int jj = __shfl_sync(FULL, jcol, t & 31);
-                    const float ww = __shfl_sync(FULL, w, t & 31);
-                    const bool ok = t < n;
-                    wv[u] = ok ? ww : 0.f;
-                    dx[u] = ok ? ldg4(A.d_out + (int64_t)jj * CB + q * 4) : f4zero();
+                    const int jj = __shfl_sync(FULL, jcol, gbase + u0 + u);
+                    wv[u] = __shfl_sync(FULL, w, gbase + u0 + u);
+                    dx[u] = (base + u0 + u < end) ? ldg4(A.d_out + (int64_t)jj * CB + q * 4) : f4zero();
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     if (HAS_DPREV) fma4(dacc, wv[u], dx[u]);
-                    p[it0 + u] = fmaf(ai.x, dx[u].x, fmaf(ai.y, dx[u].y, fmaf(ai.z, dx[u].z, ai.w * dx[u].w)));
+                    p[u0 + u] = fmaf(ai.x, dx[u].x, fmaf(ai.y, dx[u].y, fmaf(ai.z, dx[u].z, ai.w * dx[u].w)));
                 }
             }
-            // transpose reduction over the G lanes of the group: lane q ends with the full
-            // batch sum of slot it = q, i.e. entry t = q * P + g of this 32-entry block
+            // transpose reduction over the G lanes of the group: lane q ends with the batch sum
+            // of entry q of this block (= its own entry k)
 #pragma unroll
             for (int h = G / 2; h >= 1; h >>= 1) {
                 const bool upper = (q & h) != 0;
@@ -423,59 +461,52 @@ __global__ void __launch_bounds__(256) bwd_kernel(BwdArgs A) {
                     p[u] = keep + __shfl_xor_sync(FULL, send, h);
                 }
             }
-            const int t = q * P + g;
-            const float w_t = __shfl_sync(FULL, w, t & 31);
-            if (t < n) {
-                const int64_t k = k0 + t;
+            if (k < end) {
                 float gk = p[0];
                 if (!first_chunk) gk += A.grad[k];
-                if (!last_chunk) {
+                if (!last_chunk || !A.fused) {
                     A.grad[k] = gk;
-                } else if (A.fused) {
-                    const float v = A.mu * A.mom[k] - A.lr * (gk + A.wd * w_t);
-                    A.mom[k] = v;
-                    A.val[k] = w_t + v;
                 } else {
-                    A.grad[k] = gk;
+                    const float v = A.mu * A.mom[k] - A.lr * (gk + A.wd * w);
+                    const float wn = w + v;
+                    A.mom[k] = v;
+                    A.val[k] = wn;
+                    A.mval[__ldg(A.minv + k)] = wn;
                 }
             }
+            k = kn;
+            jcol = jcol_n;
+            w = w_n;
         }
         if (HAS_DPREV) {
-#pragma unroll
-            for (int m = G; m < 32; m <<= 1) dacc = shfl_xor4(dacc, m);
-            if (sg.w < 0) {
-                bwd_epilogue<CB>(A, i, dacc, lane);
-            } else if (lane < G) {
-                st4(A.ws + (int64_t)sg.w * CB + lane * 4, dacc);
-            }
+            bwd_epilogue<CB>(A, i, dacc, active && sg.w < 0, lane);
+            if (active && sg.w >= 0) st4(A.ws + (int64_t)sg.w * CB + q * 4, dacc);
         }
     }
 }
 
 template <int CB>
 __global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
-    const int lane = threadIdx.x & 31;
+    constexpr int G = CB / 4, P = 32 / G;
+    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int nm = A.meta->n_bmulti;
-    constexpr int G = CB / 4;
-    const int q = lane % G;
-    for (int r = warp; r < nm; r += nwarps) {
-        const int4 m = A.multi[r];
+    for (int r0 = warp * P; r0 < nm; r0 += nwarps * P) {
+        const int r = r0 + g;
+        const bool active = r < nm;
+        const int4 m = active ? A.multi[r] : make_int4(0, 0, 0, 0);
         float4 acc = f4zero();
         for (int t = 0; t < m.z; ++t) {
             const float4 p = ldg4(A.ws + (int64_t)(m.y + t) * CB + q * 4);
             acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
         }
-        bwd_epilogue<CB>(A, m.x, acc, lane);
+        bwd_epilogue<CB>(A, m.x, acc, active, lane);
     }
 }
 
-// rows of layer 1 (= input) need no delta; but a layer l = 2 hidden bias never exists on
-// the input side, so HAS_DPREV = false skips the epilogue entirely.
-
 // ------------------------------------------------------------------------------------------
-// a6 standalone: Eq. 1 over the whole grad view (K > 1 path)
+// a6 standalone: Eq. 1 over the whole grad view (K > 1 path), then the mirror refresh
 // ------------------------------------------------------------------------------------------
 __global__ void sgd_update_kernel(float* __restrict__ w, float* __restrict__ v, const float* __restrict__ g,
                                   int64_t n, int64_t bias_base, float lr, float mu, float wd, float gs) {
@@ -488,19 +519,28 @@ __global__ void sgd_update_kernel(float* __restrict__ w, float* __restrict__ v, 
     }
 }
 
-int persistent_grid(const smlp_handle* h, int64_t items) {
-    const int64_t need = (items + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK;
+__global__ void mirror_values_kernel(const float* __restrict__ val, const int32_t* __restrict__ mperm,
+                                     const LayerMeta* __restrict__ meta, float* __restrict__ mval) {
+    const int64_t n = meta->nnz;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        mval[t] = __ldg(val + __ldg(mperm + t));
+}
+
+int persistent_grid(const smlp_handle* h, int64_t groups, int groups_per_warp) {
+    const int64_t warps = (groups + groups_per_warp - 1) / groups_per_warp;
+    const int64_t need = (warps + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK;
     const int64_t cap = (int64_t)h->num_sms * 8;
     return (int)std::max<int64_t>(1, std::min(need, cap));
 }
 
 template <int CB>
 int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
-    const int grid = persistent_grid(h, L.fseg_cap);
+    constexpr int P = 32 / (CB / 4);
+    const int grid = persistent_grid(h, L.fseg_cap, P);
     fwd_kernel<CB><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
     SMLP_CK_LAUNCH(h, "fwd_kernel");
     if (L.fslot_cap > 0) {
-        const int g2 = persistent_grid(h, std::max<int64_t>(1, L.fslot_cap / 2));
+        const int g2 = persistent_grid(h, std::max<int64_t>(1, L.fslot_cap / 2), P);
         fwd_finish_kernel<CB><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
         SMLP_CK_LAUNCH(h, "fwd_finish_kernel");
     }
@@ -509,7 +549,8 @@ int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
 
 template <int CB>
 int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev) {
-    const int grid = persistent_grid(h, L.bseg_cap);
+    constexpr int P = 32 / (CB / 4);
+    const int grid = persistent_grid(h, L.bseg_cap, P);
     if (has_dprev) {
         bwd_kernel<CB, true><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
     } else {
@@ -517,7 +558,7 @@ int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev)
     }
     SMLP_CK_LAUNCH(h, "bwd_kernel");
     if (has_dprev && L.bslot_cap > 0) {
-        const int g2 = persistent_grid(h, std::max<int64_t>(1, L.bslot_cap / 2));
+        const int g2 = persistent_grid(h, std::max<int64_t>(1, L.bslot_cap / 2), P);
         bwd_finish_kernel<CB><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
         SMLP_CK_LAUNCH(h, "bwd_finish_kernel");
     }
@@ -550,21 +591,12 @@ uint32_t drop_threshold(float rate) {
 
 }  // namespace
 
-namespace {
-__global__ void softmax_probs_kernel(const float* __restrict__ logits, float* __restrict__ probs, int64_t nL, int B,
-                                     int CB) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= B) return;
-    const int c = b / CB, lb = b % CB;
-    const float* zc = logits + (int64_t)c * nL * CB + lb;
-    float mx = -INFINITY;
-    for (int64_t j = 0; j < nL; ++j) mx = fmaxf(mx, zc[j * CB]);
-    float s = 0.f;
-    for (int64_t j = 0; j < nL; ++j) s += expf(zc[j * CB] - mx);
-    const float inv = 1.0f / s;
-    for (int64_t j = 0; j < nL; ++j) probs[(int64_t)b * nL + j] = expf(zc[j * CB] - mx) * inv;
+int refresh_mirror_values(smlp_handle* h, Layer& Ly) {
+    if (Ly.cap == 0) return SMLP_OK;
+    mirror_values_kernel<<<launch_grid(h, Ly.cap, 256), 256, 0, h->stream>>>(Ly.val, Ly.mperm, Ly.meta, Ly.mval);
+    SMLP_CK_LAUNCH(h, "mirror_values_kernel");
+    return SMLP_OK;
 }
-}  // namespace
 
 int run_probs(smlp_handle* h, int B, float* probs) {
     softmax_probs_kernel<<<(B + 127) / 128, 128, 0, h->stream>>>(h->act[h->L], probs, h->sizes[h->L - 1], B, h->CB);
@@ -598,8 +630,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             A.multi = Ly.fmulti;
             A.meta = Ly.meta;
             A.msrc = Ly.msrc;
-            A.mperm = Ly.mperm;
-            A.val = Ly.val;
+            A.mval = Ly.mval;
             A.bias = Ly.bias;
             A.ws = Ly.fws;
             A.n_out = nout;
@@ -645,7 +676,6 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
         S.delta = h->delta[L];
         S.labels = labels;
         S.y_idx = y_idx;
-        S.probs = nullptr;
         S.loss = loss;
         S.err = h->d_err;
         S.bias = Lo.bias;
@@ -682,6 +712,8 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.val = Ly.val;
             A.mom = Ly.mom;
             A.grad = Ly.grad;
+            A.mval = Ly.mval;
+            A.minv = Ly.minv;
             A.ws = Ly.bws;
             A.bgs = Ly.bgs;
             A.bias_prev = Lp ? Lp->bias : nullptr;
@@ -717,6 +749,7 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
                                                        sgd->momentum, sgd->weight_decay, sgd->grad_scale);
     SMLP_CK_LAUNCH(h, "sgd_update_kernel");
     prof_stop(h);
+    for (auto& Ly : h->layers) SMLP_TRY(refresh_mirror_values(h, Ly));
     return SMLP_OK;
 }
 

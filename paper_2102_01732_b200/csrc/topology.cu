@@ -144,10 +144,15 @@ __global__ void iota_kernel(int32_t* __restrict__ a, int64_t n) {
         a[k] = (int32_t)k;
 }
 
-__global__ void mirror_fill_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ rowid, int64_t nnz,
-                                   int32_t* __restrict__ msrc) {
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nnz; t += (int64_t)gridDim.x * blockDim.x)
-        msrc[t] = rowid[perm[t]];
+__global__ void mirror_fill_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ rowid,
+                                   const float* __restrict__ val, int64_t nnz, int32_t* __restrict__ msrc,
+                                   int32_t* __restrict__ minv, float* __restrict__ mval) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nnz; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t k = perm[t];
+        msrc[t] = rowid[k];
+        minv[k] = (int32_t)t;
+        mval[t] = val[k];
+    }
 }
 
 __global__ void mrow_ptr_kernel(const int32_t* __restrict__ sorted_col, int64_t nnz, int64_t n_out,
@@ -330,7 +335,8 @@ int rebuild_derived(smlp_handle* h, Layer& L) {
         if (!tmp) return set_err(h, SMLP_E_NOMEM, "radix temp");
         SMLP_CK(h, cub::DeviceRadixSort::SortPairs(tmp, tb, ukeys, ukeys_out, idx_in, L.mperm, (int64_t)nnz, 0,
                                                    endbit, h->stream));
-        mirror_fill_kernel<<<launch_grid(h, nnz, TPB), TPB, 0, h->stream>>>(L.mperm, L.rowid, nnz, L.msrc);
+        mirror_fill_kernel<<<launch_grid(h, nnz, TPB), TPB, 0, h->stream>>>(L.mperm, L.rowid, L.val, nnz, L.msrc,
+                                                                             L.minv, L.mval);
         SMLP_CK_LAUNCH(h, "mirror_fill_kernel");
         mrow_ptr_kernel<<<launch_grid(h, L.n_out + 1, TPB), TPB, 0, h->stream>>>(keys_out, nnz, L.n_out, L.mrow_ptr);
         SMLP_CK_LAUNCH(h, "mrow_ptr_kernel");

@@ -35,6 +35,7 @@ EXPORTED = [
     "sparse_mlp_export_bias", "sparse_mlp_import_bias", "sparse_mlp_export_alive",
     "sparse_mlp_import_alive", "sparse_mlp_export_trace", "sparse_mlp_last_error", "sparse_mlp_version",
     "sparse_mlp_profile", "sparse_mlp_profile_read", "sparse_mlp_set_step_counter",
+    "sparse_mlp_params_updated",
 ]
 KERNEL_KINDS = {0: "stage_input", 1: "fwd", 2: "fwd_finish", 3: "softmax_ce", 4: "bwd", 5: "bwd_finish",
                 6: "sgd_update"}
@@ -118,6 +119,7 @@ def load_library(path: str = LIB_PATH):
         "sparse_mlp_profile": (I32, [VP, I32]),
         "sparse_mlp_profile_read": (I32, [VP, P(smlp_kernel_stat), I32, P(I32)]),
         "sparse_mlp_set_step_counter": (I32, [VP, VP]),
+        "sparse_mlp_params_updated": (I32, [VP]),
         "sparse_mlp_last_error": (C.c_char_p, [VP]),
         "sparse_mlp_version": (C.c_char_p, []),
     }
@@ -255,6 +257,11 @@ class SparseMLP:
         p, n, v = C.c_void_p(), C.c_int64(), C.c_uint64()
         self._check(self.lib.sparse_mlp_param_view(self.h, C.byref(p), C.byref(n), C.byref(v)))
         return self._torch.as_tensor(_CudaArray(p.value, n.value), device=f"cuda:{self.device}"), v.value
+
+    def sparse_mlp_params_updated(self):
+        """Call after writing the param view in place (averaging): refreshes the mirror copy."""
+        self._sync_stream()
+        self._check(self.lib.sparse_mlp_params_updated(self.h))
 
     # -------------------------------------------------------------------------------- topology
     def sparse_mlp_evolve_topology(self, zeta: float, evolve_idx: int):
