@@ -232,7 +232,10 @@ int sparse_mlp_import_alive(smlp_handle* h, int32_t l, const uint8_t* alive);
 /* Trace export for parity tests: kind 0 = activations a_l (l = 1..L-1; l = L gives the
  * logits z_L), kind 1 = deltas delta_l (l = 2..L) of the last forward / backward, as host
  * fp32 row-major [B x n_l].  kind 2 = gradient of W^(l) values from the grad view (host
- * fp32 [nnz]) and kind 3 = bias gradient of layer l (host fp32 [n_l]).  SYNC. */
+ * fp32 [nnz]) and kind 3 = bias gradient of layer l (host fp32 [n_l]).  kind 4 (l ignored):
+ * out[0] = 1 if the last forward took the exact binary-input path of W^(2) (every input value
+ * 0 or 1), 0 if it took the fp32 gather path, -1 if the path is disabled
+ * (padded batch > 128).  SYNC. */
 int sparse_mlp_export_trace(smlp_handle* h, int32_t kind, int32_t l, float* out);
 
 /* Per-kernel timing with CUDA events on the handle's stream (bench.py's roofline evidence).

@@ -293,8 +293,10 @@ def forward(st: State, x: np.ndarray, train: bool = True, step: int = 0, rank: O
         z = spmm_fwd(a[-1], Ly) + st.b[l - 2].astype(F64)
         mag = spmm_fwd(a[-1], Ly, wabs=True) + np.abs(st.b[l - 2].astype(F64))
         # pre-activations within fp32 summation error of the All-ReLU kink (hidden layers):
-        # there the branch taken by an fp32 kernel may legitimately differ (DESIGN: kink guard)
-        amb.append(int(np.count_nonzero(np.abs(z) <= mag * (2.0 ** -20))) if l < L else 0)
+        # there the branch taken by an fp32 kernel may legitimately differ (R30, kink
+        # guard).  mag == 0 means every term is an exact zero (e.g. no active binary input and a
+        # zero bias): z is exactly 0 on every path, so that element is not ambiguous.
+        amb.append(int(np.count_nonzero((np.abs(z) <= mag * (2.0 ** -20)) & (mag > 0))) if l < L else 0)
         zs.append(z)
         if l < L:
             h = activation(z, l, st.alpha, st.activation)

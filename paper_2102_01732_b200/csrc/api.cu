@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -184,6 +185,13 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
         Ly.bws = zalloc<float>(h, (size_t)std::max<int64_t>(Ly.bslot_cap, 1) * CB, &rc);
         Ly.bgs = zalloc<float>(h, (size_t)Ly.n_in, &rc);
         Ly.meta = zalloc<LayerMeta>(h, 1, &rc);
+        // narrow output layer: stream the canonical rows instead of gathering
+        Ly.nout_pad = std::max(2, next_pow2((int)std::min<int64_t>(Ly.n_out, 1 << 20)));
+        Ly.narrow = Ly.l == L && Ly.n_out <= NARROW_MAX && (int64_t)Ly.nout_pad * CB <= NARROW_MAX_ELEMS;
+        if (Ly.narrow) {
+            Ly.ngrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->num_sms * 4, (Ly.n_in + 63) / 64));
+            Ly.nws = zalloc<float>(h, (size_t)Ly.ngrid * Ly.nout_pad * CB, &rc);
+        }
     }
     if (rc) return rc;
     // --- neuron-layer buffers
@@ -201,6 +209,12 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
         h->alive_h[l] = (int64_t)n;
     }
     h->d_err = zalloc<int32_t>(h, 1, &rc);
+    // binary-input path of W^(2): bit-packed input, usable when the padded batch fits 128 columns
+    if ((int64_t)h->max_chunks * CB <= 32 * XBITS_WORDS) {
+        h->xbits = zalloc<uint32_t>(h, (size_t)h->sizes[0] * XBITS_WORDS, &rc);
+        h->d_nonbinary = zalloc<int32_t>(h, 1, &rc);
+        h->gmirror2 = zalloc<float>(h, (size_t)std::max<int64_t>(h->layers[0].cap, 1), &rc);
+    }
     h->d_loss = zalloc<float>(h, 1, &rc);
     if (rc) return rc;
     // --- Erdos-Renyi initialisation (R1, R2)
@@ -285,6 +299,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
         h->has_allocator = true;
     }
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+    if (const char* e = std::getenv("SMLP_GATHER_EVICT_LAST")) h->gather_evict_last = std::atoi(e) != 0;
     const int rc = build_handle(h, cfg);
     if (rc != SMLP_OK) {
         g_create_error = h->err;
@@ -616,6 +631,17 @@ int sparse_mlp_export_trace(smlp_handle* h, int32_t kind, int32_t l, float* out)
         const size_t n = kind == 2 ? (size_t)Ly.nnz : (size_t)Ly.n_out;
         if (n) SMLP_CK(h, cudaMemcpyAsync(out, src, n * 4, cudaMemcpyDeviceToHost, h->stream));
         SMLP_CK(h, cudaStreamSynchronize(h->stream));
+        return SMLP_OK;
+    }
+    if (kind == 4) {   // path flag of the last forward: binary-input W^(2) path taken (1), not (0), off (-1)
+        if (!h->xbits) {
+            out[0] = -1.f;
+            return SMLP_OK;
+        }
+        int32_t nb = 0;
+        SMLP_CK(h, cudaMemcpyAsync(&nb, h->d_nonbinary, 4, cudaMemcpyDeviceToHost, h->stream));
+        SMLP_CK(h, cudaStreamSynchronize(h->stream));
+        out[0] = nb ? 0.f : 1.f;
         return SMLP_OK;
     }
     return set_err(h, SMLP_E_ARG, "export_trace: unknown kind");

@@ -30,6 +30,10 @@ namespace smlp {
 
 constexpr int SEG_NNZ = 512;              // max nnz per work segment (long-row split)
 constexpr int WARPS_PER_BLOCK = 8;        // 256-thread blocks for the warp-per-row kernels
+constexpr int NARROW_MAX = 32;            // output layers with n_L <= 32 take the narrow path
+constexpr int NARROW_MAX_ELEMS = 2048;    // ... if next_pow2(n_L) x chunk_batch <= this
+constexpr int NARROW_WARPS = 8;
+constexpr int XBITS_WORDS = 4;          // bit-packed input: 128 batch columns per input neuron
 
 struct LayerMeta {                         // device-resident counts (graph-stable)
     int32_t nnz;
@@ -70,6 +74,11 @@ struct Layer {
     float* bgs = nullptr;   // [n_in] bias-grad accumulator across chunks (for layer l-1)
     LayerMeta* meta = nullptr;
     LayerMeta meta_h{};
+    // narrow output layer path (l = L, n_L <= NARROW_MAX): canonical-row streaming fwd / bwd
+    bool narrow = false;
+    int nout_pad = 0;       // next power of two >= n_out (>= 2)
+    int ngrid = 0;          // CTAs of the narrow forward
+    float* nws = nullptr;   // [ngrid][nout_pad][CB] CTA partial logits
     // biases of neuron layer l live in param/mom/grad at bias_off
     float* bias = nullptr;
     float* bias_mom = nullptr;
@@ -81,7 +90,8 @@ struct Alloc {
     void* ptr;
 };
 
-enum KernelKind { K_STAGE = 0, K_FWD = 1, K_FWD_FINISH = 2, K_SOFTMAX = 3, K_BWD = 4, K_BWD_FINISH = 5, K_SGD = 6 };
+enum KernelKind { K_STAGE = 0, K_FWD = 1, K_FWD_FINISH = 2, K_SOFTMAX = 3, K_BWD = 4, K_BWD_FINISH = 5, K_SGD = 6,
+                  K_FWD_BITS = 7, K_BWD_BITS = 8, K_LAYER_UPDATE = 9, K_MIRROR = 10 };
 
 struct ProfRec {
     int kind, layer;
@@ -124,6 +134,9 @@ struct smlp_handle {
     int64_t alive_h[SMLP_MAX_LAYERS + 1] = {0};
 
     int32_t* d_err = nullptr;       // label-range flag
+    uint32_t* xbits = nullptr;      // [n_1][XBITS_WORDS] bit-packed input (binary-input path) or null
+    int32_t* d_nonbinary = nullptr; // set by stage_input when an input value is not 0 or 1
+    float* gmirror2 = nullptr;      // [cap of W^(2)] gradient in mirror order (binary-input path)
     float* d_loss = nullptr;        // scratch loss for train_step_host
     float* x_stage = nullptr;       // [max_batch x n_1] for train_step_host
     int32_t* y_stage = nullptr;
@@ -142,6 +155,7 @@ struct smlp_handle {
     std::vector<smlp::ProfRec> prof_recs;
     std::vector<cudaEvent_t> ev_pool;
     int num_sms = 148;
+    int gather_evict_last = 0;      // tuning knob (env SMLP_GATHER_EVICT_LAST): L2 policy of row gathers
     int64_t launches = 0;
     std::string err;
 };

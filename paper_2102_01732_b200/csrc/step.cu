@@ -14,8 +14,9 @@
 //                  entry it gathers delta_l[j] once, accumulates delta_{l-1}[i] += w_ij delta_l[j]
 //                  (SpMM against W^T) and the partial dot <a_{l-1}[i], delta_l[j]> (SDDMM); a
 //                  transpose reduction over the G lanes leaves lane q with the batch sum of entry q,
-//                  which it applies as the Eq. 1 update of (w, v) in place (1-GPU fused path, also
-//                  refreshing the forward's mirror-ordered copy of w) or writes to the grad view
+//                  which it applies as the Eq. 1 update of (w, v) in place (1-GPU fused path) or
+//                  writes to the grad view; mirror_values then refreshes the forward's
+//                  mirror-ordered copy of w by a gather (a scatter would cost a sector read-fill)
 //   bwd_finish     multi-segment rows: fixed-order sum of the delta partials + epilogue
 //   sgd_update     a6 on the grad view after the caller's allreduce (K > 1), then mirror refresh
 //
@@ -54,12 +55,60 @@ __device__ __forceinline__ uint32_t group_bits(uint32_t ballot, int g) {
     return G == 32 ? ballot : ((ballot >> (g * G)) & ((1u << G) - 1u));
 }
 
+// L2 eviction policies (sm_80+ createpolicy / .L2::cache_hint): data streamed once per pass
+// (indices, values, momenta, gradients) is marked evict_first so it does not push the gathered
+// activation / delta slab of the chunk out of the L2; the gathers keep the normal policy.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// read-only for the whole kernel
+__device__ __forceinline__ int32_t ldro_i32(const int32_t* p, uint64_t pol) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ldro_f32(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float4 ldro_f4(const float* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+// gathered rows: read-only, L1 not allocated (no reuse within the SM), policy chosen by the caller
+__device__ __forceinline__ float4 ldg_row4(const float* p, uint64_t pol) { return ldro_f4(p, pol); }
+// read-write by the same thread within the kernel (coherent path)
+__device__ __forceinline__ float ldrw_f32(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_f32(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(p), "f"(v), "l"(pol) : "memory");
+}
+
 // ------------------------------------------------------------------------------------------
 // a1: input staging (transpose + optional row gather), zero padding of columns b >= B
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) stage_input_kernel(const float* __restrict__ x, const int32_t* __restrict__ x_idx,
                                                            int B, int nchunks, int CB, int64_t n1,
-                                                           float* __restrict__ act1) {
+                                                           float* __restrict__ act1, uint32_t* __restrict__ xbits,
+                                                           int32_t* __restrict__ nonbinary) {
     __shared__ float tile[32][33];
     const int64_t f0 = (int64_t)blockIdx.x * 32;
     const int b0 = blockIdx.y * 32;
@@ -78,9 +127,20 @@ __global__ void __launch_bounds__(1024) stage_input_kernel(const float* __restri
     {
         const int b = b0 + tx;
         const int64_t f = f0 + ty;
+        const float v = tile[tx][ty];
         if (f < n1 && b < nchunks * CB) {
             const int c = b / CB, lb = b % CB;
-            act1[((int64_t)c * n1 + f) * CB + lb] = tile[tx][ty];
+            act1[((int64_t)c * n1 + f) * CB + lb] = v;
+        }
+        if (xbits) {
+            // warp ty holds feature f over batch b0..b0+31: one 32-bit word of the bit-packed
+            // input (bit b%32 = x[b][f] != 0) for the exact binary-input path of layer 2
+            const unsigned word = __ballot_sync(FULL, v != 0.f);
+            const bool nb = __any_sync(FULL, v != 0.f && v != 1.f);
+            if (tx == 0 && f < n1) {
+                xbits[f * XBITS_WORDS + blockIdx.y] = word;
+                if (nb) atomicOr(nonbinary, 1);
+            }
         }
     }
 }
@@ -112,6 +172,8 @@ struct FwdArgs {
     uint32_t step_lo;
     const uint64_t* step_ptr; // device dropout-step source (graph replay) or null
     int b0;                   // global batch index of column 0 of this chunk
+    const int32_t* skip_if_binary;   // layer 2 with the binary-input path: return if *flag == 0
+    int gather_evict_last;           // L2 policy of the gathered rows: evict_last (1) or normal (0)
 };
 
 // Epilogue of one output row j per group: all 32 lanes call it (ballots); `own` marks the
@@ -157,7 +219,8 @@ __device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4
 
 // Gather-accumulate of one segment [beg, end) per group (groups in lock-step up to maxblk).
 template <int CB>
-__device__ __forceinline__ float4 fwd_segment(const FwdArgs& A, int beg, int end, int maxblk, int lane) {
+__device__ __forceinline__ float4 fwd_segment(const FwdArgs& A, int beg, int end, int maxblk, int lane,
+                                              uint64_t pol_s, uint64_t pol_g) {
     constexpr int G = CB / 4;
     constexpr int U = G < 8 ? G : 8;
     const int g = lane / G, q = lane % G, gbase = g * G;
@@ -166,16 +229,16 @@ __device__ __forceinline__ float4 fwd_segment(const FwdArgs& A, int beg, int end
     int src = 0;
     float w = 0.f;
     if (k < end) {
-        src = __ldg(A.msrc + k);
-        w = __ldg(A.mval + k);
+        src = ldro_i32(A.msrc + k, pol_s);
+        w = ldro_f32(A.mval + k, pol_s);
     }
     for (int b = 0; b < maxblk; ++b) {
         const int kn = k + G;                          // prefetch the next block's entries
         int src_n = 0;
         float w_n = 0.f;
         if (kn < end) {
-            src_n = __ldg(A.msrc + kn);
-            w_n = __ldg(A.mval + kn);
+            src_n = ldro_i32(A.msrc + kn, pol_s);
+            w_n = ldro_f32(A.mval + kn, pol_s);
         }
         const int base = beg + b * G;
 #pragma unroll
@@ -186,7 +249,7 @@ __device__ __forceinline__ float4 fwd_segment(const FwdArgs& A, int beg, int end
             for (int u = 0; u < U; ++u) {
                 const int s = __shfl_sync(FULL, src, gbase + u0 + u);
                 wv[u] = __shfl_sync(FULL, w, gbase + u0 + u);
-                x[u] = (base + u0 + u < end) ? ldg4(A.a_prev + (int64_t)s * CB + q * 4) : f4zero();
+                x[u] = (base + u0 + u < end) ? ldg_row4(A.a_prev + (int64_t)s * CB + q * 4, pol_g) : f4zero();
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) fma4(acc, wv[u], x[u]);
@@ -201,18 +264,21 @@ __device__ __forceinline__ float4 fwd_segment(const FwdArgs& A, int beg, int end
 template <int CB>
 __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs A) {
     constexpr int G = CB / 4, P = 32 / G;
+    if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int nseg = A.meta->n_fseg;
     const uint32_t step_lo = A.step_ptr ? (uint32_t)(*A.step_ptr) : A.step_lo;
+    const uint64_t pol_s = policy_evict_first();
+    const uint64_t pol_g = A.gather_evict_last ? policy_evict_last() : policy_evict_normal();
     for (int s0 = warp * P; s0 < nseg; s0 += nwarps * P) {
         const int s = s0 + g;
         const bool active = s < nseg;
         const int4 sg = active ? A.seg[s] : make_int4(0, 0, 0, -2);
         const int nblk = (sg.z - sg.y + G - 1) / G;
         const int maxblk = __reduce_max_sync(FULL, nblk);
-        const float4 acc = fwd_segment<CB>(A, sg.y, sg.z, maxblk, lane);
+        const float4 acc = fwd_segment<CB>(A, sg.y, sg.z, maxblk, lane, pol_s, pol_g);
         fwd_epilogue<CB>(A, sg.x, acc, active && sg.w < 0, lane, step_lo);
         if (active && sg.w >= 0) st4(A.ws + (int64_t)sg.w * CB + q * 4, acc);
     }
@@ -221,6 +287,7 @@ __global__ void __launch_bounds__(256) fwd_kernel(FwdArgs A) {
 template <int CB>
 __global__ void __launch_bounds__(256) fwd_finish_kernel(FwdArgs A) {
     constexpr int G = CB / 4, P = 32 / G;
+    if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -353,9 +420,11 @@ struct BwdArgs {
     float neg_slope_prev;
     float keep_scale_prev;
     int dropout_prev;
-    int chunk, nchunks;
+    int first, last;          // first / last chunk processed for this layer (grad accumulation)
     int fused;
     float lr, mu, wd;
+    const int32_t* skip_if_binary;   // layer 2 with the binary-input path: return if *flag == 0
+    int gather_evict_last;           // L2 policy of the gathered rows: evict_last (1) or normal (0)
 };
 
 // delta_{l-1} of input row i per group: f'(z) from the sign bits, dropout keep bits, store, and
@@ -384,8 +453,8 @@ __device__ __forceinline__ void bwd_epilogue(const BwdArgs& A, int64_t i, float4
     for (int m = 1; m < G; m <<= 1) s += __shfl_xor_sync(FULL, s, m);
     if (own && q == 0) {
         float tot = s;
-        if (A.chunk > 0) tot += A.bgs[i];
-        if (A.chunk + 1 < A.nchunks) {
+        if (!A.first) tot += A.bgs[i];
+        if (!A.last) {
             A.bgs[i] = tot;
         } else if (A.fused) {
             const float v = A.mu * A.bias_mom_prev[i] - A.lr * tot;
@@ -400,13 +469,16 @@ __device__ __forceinline__ void bwd_epilogue(const BwdArgs& A, int64_t i, float4
 template <int CB, bool HAS_DPREV>
 __global__ void __launch_bounds__(256) bwd_kernel(BwdArgs A) {
     constexpr int G = CB / 4, P = 32 / G;
+    if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     constexpr int U = G < 8 ? G : 8;
     const int lane = threadIdx.x & 31;
     const int g = lane / G, q = lane % G, gbase = g * G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int nseg = A.meta->n_bseg;
-    const bool first_chunk = A.chunk == 0, last_chunk = A.chunk + 1 == A.nchunks;
+    const bool first_chunk = A.first != 0, last_chunk = A.last != 0;
+    const uint64_t pol_s = policy_evict_first();
+    const uint64_t pol_g = A.gather_evict_last ? policy_evict_last() : policy_evict_normal();
     for (int s0 = warp * P; s0 < nseg; s0 += nwarps * P) {
         const int s = s0 + g;
         const bool active = s < nseg;
@@ -414,22 +486,22 @@ __global__ void __launch_bounds__(256) bwd_kernel(BwdArgs A) {
         const int64_t i = sg.x;
         const int beg = sg.y, end = sg.z;
         const int maxblk = __reduce_max_sync(FULL, (end - beg + G - 1) / G);
-        const float4 ai = active ? ldg4(A.a_prev + i * CB + q * 4) : f4zero();
+        const float4 ai = active ? ldro_f4(A.a_prev + i * CB + q * 4, pol_s) : f4zero();
         float4 dacc = f4zero();
         int k = beg + q;
         int jcol = 0;
         float w = 0.f;
         if (k < end) {
-            jcol = __ldg(A.col + k);
-            w = A.val[k];
+            jcol = ldro_i32(A.col + k, pol_s);
+            w = ldrw_f32(A.val + k, pol_s);
         }
         for (int b = 0; b < maxblk; ++b) {
             const int kn = k + G;                      // prefetch the next block's entries
             int jcol_n = 0;
             float w_n = 0.f;
             if (kn < end) {
-                jcol_n = __ldg(A.col + kn);
-                w_n = A.val[kn];
+                jcol_n = ldro_i32(A.col + kn, pol_s);
+                w_n = ldrw_f32(A.val + kn, pol_s);
             }
             const int base = beg + b * G;
             float p[G];
@@ -441,7 +513,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(BwdArgs A) {
                 for (int u = 0; u < U; ++u) {
                     const int jj = __shfl_sync(FULL, jcol, gbase + u0 + u);
                     wv[u] = __shfl_sync(FULL, w, gbase + u0 + u);
-                    dx[u] = (base + u0 + u < end) ? ldg4(A.d_out + (int64_t)jj * CB + q * 4) : f4zero();
+                    dx[u] = (base + u0 + u < end) ? ldg_row4(A.d_out + (int64_t)jj * CB + q * 4, pol_g) : f4zero();
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -463,15 +535,13 @@ __global__ void __launch_bounds__(256) bwd_kernel(BwdArgs A) {
             }
             if (k < end) {
                 float gk = p[0];
-                if (!first_chunk) gk += A.grad[k];
+                if (!first_chunk) gk += ldrw_f32(A.grad + k, pol_s);
                 if (!last_chunk || !A.fused) {
-                    A.grad[k] = gk;
+                    st_f32(A.grad + k, gk, pol_s);
                 } else {
-                    const float v = A.mu * A.mom[k] - A.lr * (gk + A.wd * w);
-                    const float wn = w + v;
-                    A.mom[k] = v;
-                    A.val[k] = wn;
-                    A.mval[__ldg(A.minv + k)] = wn;
+                    const float v = A.mu * ldrw_f32(A.mom + k, pol_s) - A.lr * (gk + A.wd * w);
+                    st_f32(A.mom + k, v, pol_s);
+                    st_f32(A.val + k, w + v, pol_s);
                 }
             }
             k = kn;
@@ -488,6 +558,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(BwdArgs A) {
 template <int CB>
 __global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
     constexpr int G = CB / 4, P = 32 / G;
+    if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -502,6 +573,639 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
             acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
         }
         bwd_epilogue<CB>(A, m.x, acc, active, lane);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// narrow output layer (l = L, n_L <= NARROW_MAX): both passes walk the canonical CSR rows i of
+// W^(L) in order, so a_{L-1} is streamed once instead of gathered once per output neuron.
+// Lane t of a warp owns VEC = max(1, CB/32) consecutive batch columns; a warp takes RU rows at
+// a time (all loads first, then the math) to keep enough bytes in flight.  The row's <= n_L
+// entries sit one per lane; the weight of output jj is fetched by ballot + shuffle.
+//   fwd: per-warp partial logits acc[jj][cols] -> per-CTA fixed-order sum -> the last CTA to
+//        finish sums the CTA partials in CTA order and adds b_L (deterministic, no float atomics)
+//   bwd: delta_L chunk held in registers; delta_{L-1}[i] = (sum_jj w_ij delta_L[jj]) * f' * keep,
+//        g_ij = warp-sum over the chunk's columns of a_{L-1}[i] delta_L[j], Eq. 1 update of the
+//        row's entries (coalesced), bias gradient of layer L-1
+// ------------------------------------------------------------------------------------------
+struct NarrowArgs {
+    const int32_t* row_ptr;
+    const int32_t* col;
+    float* val;
+    float* mom;
+    float* grad;
+    const float* a_prev;      // chunk base [n_in][CB]
+    float* a_out;             // fwd: chunk base [n_out][CB] (logits)
+    const float* bias;        // fwd: b_L
+    float* ws;                // fwd: [gridDim][NOUT][CB] CTA partials
+    const float* d_out;       // bwd: delta_L chunk base [n_out][CB]
+    float* d_prev;            // bwd: delta_{L-1} chunk base [n_in][CB]
+    const uint4* zmask_prev;
+    const uint4* kmask_prev;
+    float* bgs;
+    float* bias_prev;
+    float* bias_mom_prev;
+    float* bias_grad_prev;
+    int64_t n_in;
+    int n_out;
+    const LayerMeta* meta;    // device nnz: complete layer (nnz = n_in n_out) -> row i = [i n_out, (i+1) n_out)
+    float neg_slope_prev;
+    float keep_scale_prev;
+    int dropout_prev;
+    int first, last;
+    int fused;
+    float lr, mu, wd;
+};
+
+template <int VEC>
+__device__ __forceinline__ void ldvec(float (&d)[VEC], const float* p) {
+    if constexpr (VEC == 4) {
+        const float4 t = ldg4(p);
+        d[0] = t.x; d[1] = t.y; d[2] = t.z; d[3] = t.w;
+    } else if constexpr (VEC == 2) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+        d[0] = t.x; d[1] = t.y;
+    } else {
+        d[0] = __ldg(p);
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void stvec(float* p, const float (&d)[VEC]) {
+    if constexpr (VEC == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(d[0], d[1], d[2], d[3]);
+    } else if constexpr (VEC == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(d[0], d[1]);
+    } else {
+        p[0] = d[0];
+    }
+}
+
+
+// Row bounds of canonical row i: a dense-capped narrow layer has exactly n_out entries per row at
+// i * n_out (no dependent row_ptr load on the critical path).
+__device__ __forceinline__ void narrow_row(const NarrowArgs& A, bool dense, int64_t i, int& beg, int& len) {
+    if (dense) {
+        beg = (int)(i * A.n_out);
+        len = A.n_out;
+    } else {
+        beg = __ldg(A.row_ptr + i);
+        len = __ldg(A.row_ptr + i + 1) - beg;
+    }
+}
+
+template <int CB, int NOUT>
+__global__ void __launch_bounds__(NARROW_WARPS * 32) fwd_narrow_kernel(NarrowArgs A) {
+    constexpr int VEC = CB >= 32 ? CB / 32 : 1;
+    constexpr int RU = VEC == 4 ? 4 : 8;
+    __shared__ float red[NOUT * CB];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool colok = lane * VEC < CB;
+    const int64_t r0 = (A.n_in * blockIdx.x) / gridDim.x, r1 = (A.n_in * (blockIdx.x + 1)) / gridDim.x;
+    const bool dense = (int64_t)A.meta->nnz == A.n_in * (int64_t)A.n_out;   // graph-stable (device count)
+    float acc[NOUT][VEC];
+#pragma unroll
+    for (int jj = 0; jj < NOUT; ++jj)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[jj][v] = 0.f;
+    for (int64_t i0 = r0 + (int64_t)warp * RU; i0 < r1; i0 += (int64_t)NARROW_WARPS * RU) {
+        int cj[RU];
+        float w[RU], a[RU][VEC];
+        // all loads of the RU rows first (independent for dense rows), then the math
+#pragma unroll
+        for (int r = 0; r < RU; ++r) {
+            const int64_t i = i0 + r;
+            cj[r] = -1;
+            w[r] = 0.f;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) a[r][v] = 0.f;
+            if (i < r1) {
+                int beg, len;
+                narrow_row(A, dense, i, beg, len);
+                if (lane < len) {
+                    cj[r] = __ldg(A.col + beg + lane);
+                    w[r] = A.val[beg + lane];
+                }
+                if (colok) ldvec<VEC>(a[r], A.a_prev + i * CB + lane * VEC);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RU; ++r) {
+#pragma unroll
+            for (int jj = 0; jj < NOUT; ++jj) {
+                if (jj < A.n_out) {
+                    const unsigned m = __ballot_sync(FULL, cj[r] == jj);
+                    if (m) {
+                        const float wj = __shfl_sync(FULL, w[r], __ffs(m) - 1);
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) acc[jj][v] = fmaf(wj, a[r][v], acc[jj][v]);
+                    }
+                }
+            }
+        }
+    }
+    // per-CTA fixed-order reduction over the warps: ((w0 + w1) + w2) + ...
+    for (int wv = 0; wv < NARROW_WARPS; ++wv) {
+        if (warp == wv && colok) {
+#pragma unroll
+            for (int jj = 0; jj < NOUT; ++jj)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) {
+                    float& r = red[jj * CB + lane * VEC + v];
+                    r = wv == 0 ? acc[jj][v] : r + acc[jj][v];
+                }
+        }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < NOUT * CB; e += blockDim.x) A.ws[(int64_t)blockIdx.x * NOUT * CB + e] = red[e];
+}
+
+// one warp per logit element e = jj * CB + b: fixed-order sum of the CTA partials (lane-strided,
+// then an xor tree) + b_L
+template <int CB, int NOUT>
+__global__ void __launch_bounds__(32) fwd_narrow_finish_kernel(NarrowArgs A, int nparts) {
+    const int e = blockIdx.x, lane = threadIdx.x;
+    float s = 0.f;
+    for (int b = lane; b < nparts; b += 32) s += A.ws[(int64_t)b * NOUT * CB + e];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (lane == 0) A.a_out[e] = s + __ldg(A.bias + e / CB);
+}
+
+template <int CB, int NOUT>
+__global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_kernel(NarrowArgs A) {
+    constexpr int VEC = CB >= 32 ? CB / 32 : 1;
+    constexpr int RU = VEC == 4 ? 2 : (VEC == 2 ? 4 : 8);
+    const int lane = threadIdx.x & 31;
+    const bool colok = lane * VEC < CB;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const bool dense = (int64_t)A.meta->nnz == A.n_in * (int64_t)A.n_out;   // graph-stable (device count)
+    float dL[NOUT][VEC];
+#pragma unroll
+    for (int jj = 0; jj < NOUT; ++jj) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) dL[jj][v] = 0.f;
+        if (jj < A.n_out && colok) ldvec<VEC>(dL[jj], A.d_out + jj * CB + lane * VEC);
+    }
+    for (int64_t i0 = gw * RU; i0 < A.n_in; i0 += nw * RU) {
+        int cj[RU], beg[RU];
+        float w[RU], gacc[RU], a[RU][VEC];
+        uint4 zb[RU], kb[RU];
+        // all loads of the RU rows first (independent for dense rows), then the math
+#pragma unroll
+        for (int r = 0; r < RU; ++r) {
+            const int64_t i = i0 + r;
+            cj[r] = -1;
+            w[r] = 0.f;
+            gacc[r] = 0.f;
+            beg[r] = 0;
+            zb[r] = make_uint4(0, 0, 0, 0);
+            kb[r] = make_uint4(FULL, FULL, FULL, FULL);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) a[r][v] = 0.f;
+            if (i < A.n_in) {
+                int len;
+                narrow_row(A, dense, i, beg[r], len);
+                if (lane < len) {
+                    cj[r] = __ldg(A.col + beg[r] + lane);
+                    w[r] = A.val[beg[r] + lane];
+                    if (!A.first) gacc[r] = A.grad[beg[r] + lane];
+                }
+                if (colok) ldvec<VEC>(a[r], A.a_prev + i * CB + lane * VEC);
+                if (A.d_prev) {
+                    zb[r] = __ldg(A.zmask_prev + i);
+                    if (A.dropout_prev) kb[r] = __ldg(A.kmask_prev + i);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RU; ++r) {
+            const int64_t i = i0 + r;
+            float dp[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) dp[v] = 0.f;
+            float gmine = 0.f;
+#pragma unroll
+            for (int jj = 0; jj < NOUT; ++jj) {
+                if (jj < A.n_out) {
+                    const unsigned m = __ballot_sync(FULL, cj[r] == jj);
+                    if (m) {
+                        const float wj = __shfl_sync(FULL, w[r], __ffs(m) - 1);
+                        float s = 0.f;
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) {
+                            dp[v] = fmaf(wj, dL[jj][v], dp[v]);
+                            s = fmaf(a[r][v], dL[jj][v], s);
+                        }
+#pragma unroll
+                        for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+                        if (cj[r] == jj) gmine = s;
+                    }
+                }
+            }
+            if (i >= A.n_in) continue;   // warp-uniform
+            if (cj[r] >= 0) {             // lane owns entry k = beg + lane: accumulate / apply Eq. 1
+                const int64_t k = beg[r] + lane;
+                const float gk = gmine + gacc[r];
+                if (!A.last || !A.fused) {
+                    A.grad[k] = gk;
+                } else {
+                    const float vk = A.mu * A.mom[k] - A.lr * (gk + A.wd * w[r]);
+                    A.mom[k] = vk;
+                    A.val[k] = w[r] + vk;
+                }
+            }
+            if (A.d_prev) {
+                float o[VEC];
+                float bsum = 0.f;
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) {
+                    const int b = lane * VEC + v;
+                    const bool pos = (word(zb[r], b & 3) >> (b >> 2)) & 1u;
+                    const bool keep = (word(kb[r], b & 3) >> (b >> 2)) & 1u;
+                    const float x = dp[v] * (pos ? 1.f : A.neg_slope_prev);
+                    o[v] = colok ? (A.dropout_prev ? (keep ? x * A.keep_scale_prev : 0.f) : x) : 0.f;
+                    bsum += o[v];
+                }
+                if (colok) stvec<VEC>(A.d_prev + i * CB + lane * VEC, o);
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) bsum += __shfl_xor_sync(FULL, bsum, off);
+                if (lane == 0) {
+                    float tot = bsum;
+                    if (!A.first) tot += A.bgs[i];
+                    if (!A.last) {
+                        A.bgs[i] = tot;
+                    } else if (A.fused) {
+                        const float vb = A.mu * A.bias_mom_prev[i] - A.lr * tot;
+                        A.bias_mom_prev[i] = vb;
+                        A.bias_prev[i] = A.bias_prev[i] + vb;
+                    } else {
+                        A.bias_grad_prev[i] = tot;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Narrow DENSE-CAPPED output layer, backward with one lane per canonical row i (32 rows per warp
+// tile): the row's <= 16 weights, old gradients and masks sit in the lane's registers, the
+// activation rows are staged through a per-warp shared-memory transpose (coalesced 16-B loads,
+// conflict-free 16-B reads with a 36-float row stride) and delta_{L-1} goes back the same way.
+// delta_L (n_L x CB) is broadcast from shared memory.  Rows of a dense-capped layer are either
+// complete (j = 0..n_L-1 in order) or empty (outgoing row of a pruned neuron), so entry jj of a
+// row is output jj.  ~10 warp instructions per row instead of ~200 with one row per warp.
+template <int CB, int NOUT>
+__global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_rows_kernel(NarrowArgs A) {
+    constexpr int CS = CB < 32 ? CB : 32;     // columns per slice
+    constexpr int NS = CB / CS;
+    constexpr int TS = CS + 1;                // odd smem row stride: lane-per-row access is conflict-free
+    constexpr int C4 = CS / 4;                // float4 per row slice
+    __shared__ float dLs[NOUT][CB];
+    __shared__ float tile[NARROW_WARPS][32][TS];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    for (int e = threadIdx.x; e < NOUT * CB; e += blockDim.x)
+        dLs[e / CB][e % CB] = (e / CB < A.n_out) ? __ldg(A.d_out + e) : 0.f;
+    __syncthreads();
+    const uint64_t pol_s = policy_evict_first();
+    const bool dense = (int64_t)A.meta->nnz == A.n_in * (int64_t)A.n_out;
+    const int64_t ntiles = (A.n_in + 31) / 32;
+    float* tl = &tile[wib][0][0];
+    for (int64_t t = (int64_t)blockIdx.x * NARROW_WARPS + wib; t < ntiles; t += (int64_t)gridDim.x * NARROW_WARPS) {
+        const int64_t r0 = t * 32, i = r0 + lane;
+        const bool valid = i < A.n_in;
+        int beg = 0, len = 0;
+        if (valid) narrow_row(A, dense, i, beg, len);
+        float w[NOUT], gacc[NOUT], g[NOUT];
+#pragma unroll
+        for (int jj = 0; jj < NOUT; ++jj) {
+            const bool has = jj < len;
+            w[jj] = has ? ldrw_f32(A.val + beg + jj, pol_s) : 0.f;
+            gacc[jj] = (has && !A.first) ? ldrw_f32(A.grad + beg + jj, pol_s) : 0.f;
+            g[jj] = 0.f;
+        }
+        uint4 zb = make_uint4(0, 0, 0, 0), kb = make_uint4(FULL, FULL, FULL, FULL);
+        if (A.d_prev && valid) {
+            zb = __ldg(A.zmask_prev + i);
+            if (A.dropout_prev) kb = __ldg(A.kmask_prev + i);
+        }
+        float bsum = 0.f;
+        for (int sl = 0; sl < NS; ++sl) {
+#pragma unroll
+            for (int m = 0; m < C4; ++m) {        // coalesced: 32 rows x CS columns of a_{L-1}
+                const int e = lane + 32 * m, rr = e / C4, cc = e % C4;
+                const int64_t row = r0 + rr;
+                const float4 v = row < A.n_in ? ldro_f4(A.a_prev + row * CB + sl * CS + 4 * cc, pol_s) : f4zero();
+                float* d = tl + rr * TS + 4 * cc;
+                d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+            }
+            __syncwarp();
+#pragma unroll 4
+            for (int c = 0; c < CS; ++c) {
+                const int b = sl * CS + c;
+                const float av = tl[lane * TS + c];
+                float dp = 0.f;
+#pragma unroll
+                for (int jj = 0; jj < NOUT; ++jj) {
+                    const float d = dLs[jj][b];
+                    dp = fmaf(w[jj], d, dp);              // delta_L W^(L)T, outputs in order
+                    g[jj] = fmaf(av, d, g[jj]);           // SDDMM over the chunk's columns
+                }
+                if (A.d_prev) {
+                    const bool pos = (word(zb, b & 3) >> (b >> 2)) & 1u;
+                    const bool keep = (word(kb, b & 3) >> (b >> 2)) & 1u;
+                    const float x = dp * (pos ? 1.f : A.neg_slope_prev);
+                    const float o = A.dropout_prev ? (keep ? x * A.keep_scale_prev : 0.f) : x;
+                    bsum += o;
+                    tl[lane * TS + c] = o;
+                }
+            }
+            __syncwarp();
+            if (A.d_prev) {
+#pragma unroll
+                for (int m = 0; m < C4; ++m) {    // coalesced store of delta_{L-1}
+                    const int e = lane + 32 * m, rr = e / C4, cc = e % C4;
+                    const int64_t row = r0 + rr;
+                    const float* d = tl + rr * TS + 4 * cc;
+                    if (row < A.n_in) st4(A.d_prev + row * CB + sl * CS + 4 * cc, make_float4(d[0], d[1], d[2], d[3]));
+                }
+                __syncwarp();
+            }
+        }
+        if (!valid) continue;
+#pragma unroll
+        for (int jj = 0; jj < NOUT; ++jj) {       // Eq. 1 / gradient accumulation of the row's entries
+            if (jj < len) {
+                const int64_t k = beg + jj;
+                const float gk = g[jj] + gacc[jj];
+                if (!A.last || !A.fused) {
+                    st_f32(A.grad + k, gk, pol_s);
+                } else {
+                    const float vk = A.mu * ldrw_f32(A.mom + k, pol_s) - A.lr * (gk + A.wd * w[jj]);
+                    st_f32(A.mom + k, vk, pol_s);
+                    st_f32(A.val + k, w[jj] + vk, pol_s);
+                }
+            }
+        }
+        if (A.d_prev) {                           // bias gradient of layer L-1, accumulated over chunks
+            float tot = bsum;
+            if (!A.first) tot += A.bgs[i];
+            if (!A.last) {
+                A.bgs[i] = tot;
+            } else if (A.fused) {
+                const float vb = A.mu * A.bias_mom_prev[i] - A.lr * tot;
+                A.bias_mom_prev[i] = vb;
+                A.bias_prev[i] = A.bias_prev[i] + vb;
+            } else {
+                A.bias_grad_prev[i] = tot;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// binary-input path of the first weight layer W^(2) (C5's inputs are {0,1}, stored fp32).
+// When every staged input value is 0 or 1 (a device flag set by stage_input, so no host sync),
+// a_1[b, i] is one bit and layer 2 needs no activation gather at all: the bit-packed input
+// (16 B per input neuron for B <= 128, 1 MB for n_1 = 65536) is L1/L2-resident.  The result is
+// bit-identical to the fp32 gather path: fmaf(w, x, acc) with x in {0, 1} in the same order.
+//   fwd_bits: one warp per mirror row j covering ALL batch columns (lane q owns global columns
+//             4q..4q+3 = chunk 4q/CB); epilogue as fwd_epilogue with group g = chunk g.
+//   bwd_bits: one warp per mirror row j: delta_2[j] (all columns) in registers; per entry
+//             g_ij = sum_b bit(b) delta_2[b, j] by a 32-entry transpose reduction, scattered to
+//             the canonical grad slot mperm[t]; the Eq. 1 update then runs in canonical order.
+// The fp32 chunk kernels of layer 2 return at once when the flag says binary, and these kernels
+// return at once when it does not.
+// ------------------------------------------------------------------------------------------
+struct BitsArgs {
+    const uint32_t* xbits;    // [n_1][XBITS_WORDS]
+    const int32_t* nonbinary; // device flag
+    const int32_t* mrow_ptr;
+    const int32_t* msrc;
+    const int32_t* mperm;
+    const float* mval;
+    const float* bias;
+    float* a_out;             // act[2] base (all chunks)
+    uint4* zmask;             // zmask[2] base
+    uint4* kmask;
+    const float* d_out;       // delta[2] base (all chunks)
+    float* grad;              // canonical grad slice of W^(2)
+    float* gmirror;           // [cap] gradient of W^(2) in mirror order (bwd_bits output)
+    int64_t n_out;
+    int nchunks;
+    float neg_slope;
+    int dropout_on;
+    uint32_t drop_thr;
+    float keep_scale;
+    uint64_t seed;
+    int rank;
+    uint32_t step_lo;
+    const uint64_t* step_ptr;
+};
+
+// Work unit of the bits kernels: BITS_ROWS consecutive mirror rows, streamed as one contiguous
+// entry range in blocks of 32 entries (no per-row index latency; row ends come from the row
+// pointers loaded once per unit).  Per block, lane t loads entry t's (src, w) (coalesced) and the
+// 16-B bit row of its input neuron, and publishes (w, word k) pairs in shared memory; every lane
+// then reads, per entry, the one pair holding its 4 columns' bits (broadcast, conflict-free).
+constexpr int BITS_ROWS = 32;
+
+template <int CB>
+__global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
+    constexpr int G = CB / 4;                       // lanes per chunk
+    __shared__ float2 rec[WARPS_PER_BLOCK][32][XBITS_WORDS];
+    if (*A.nonbinary) return;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int g = lane / G, q = lane % G;            // chunk g, chunk-local lane q
+    const bool colok = g < A.nchunks;
+    const int wsel = lane >> 3, sh = (lane * 4) & 31;
+    const uint32_t step_lo = A.step_ptr ? (uint32_t)(*A.step_ptr) : A.step_lo;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nunits = (A.n_out + BITS_ROWS - 1) / BITS_ROWS;
+    const uint4* xb4 = reinterpret_cast<const uint4*>(A.xbits);
+    for (int64_t u0 = warp; u0 < nunits; u0 += nwarps) {
+        const int64_t j0 = u0 * BITS_ROWS;
+        const int nrows = (int)(A.n_out - j0 < BITS_ROWS ? A.n_out - j0 : BITS_ROWS);
+        const int rp_l = __ldg(A.mrow_ptr + j0 + min(lane, nrows));       // lane t: start of local row t
+        const int E0 = __shfl_sync(FULL, rp_l, 0), E1 = __ldg(A.mrow_ptr + j0 + nrows);
+        int row = 0;
+        int row_end = nrows > 1 ? __shfl_sync(FULL, rp_l, 1) : E1;
+        float4 acc = f4zero();
+        auto finish_row = [&]() {
+            const int64_t j = j0 + row;
+            const float bj = __ldg(A.bias + j);
+            const float4 z = make_float4(acc.x + bj, acc.y + bj, acc.z + bj, acc.w + bj);
+            uint32_t zb[4], kb[4];
+            float out[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float zc = comp(z, c);
+                const bool pos = zc > 0.f;
+                zb[c] = group_bits<G>(__ballot_sync(FULL, colok && pos), g);
+                float a = pos ? zc : A.neg_slope * zc;
+                bool keep = true;
+                if (A.dropout_on) {
+                    const uint64_t b = (uint64_t)(lane * 4 + c);
+                    const uint64_t e = b * (uint64_t)A.n_out + (uint64_t)j;
+                    const uint4 r = rng_stream(A.seed, P_DROPOUT, A.rank, 2, step_lo, e >> 2);
+                    keep = word(r, (int)(e & 3)) >= A.drop_thr;
+                    a = keep ? a * A.keep_scale : 0.f;
+                }
+                kb[c] = group_bits<G>(__ballot_sync(FULL, colok && keep), g);
+                out[c] = a;
+            }
+            if (colok) {
+                st4(A.a_out + ((int64_t)g * A.n_out + j) * CB + q * 4, make_float4(out[0], out[1], out[2], out[3]));
+                if (q == 0) {
+                    A.zmask[(int64_t)g * A.n_out + j] = make_uint4(zb[0], zb[1], zb[2], zb[3]);
+                    if (A.dropout_on) A.kmask[(int64_t)g * A.n_out + j] = make_uint4(kb[0], kb[1], kb[2], kb[3]);
+                }
+            }
+            acc = f4zero();
+            ++row;
+            row_end = __shfl_sync(FULL, rp_l, min(row + 1, 31));
+            if (row + 1 > 31) row_end = E1;
+        };
+        int k = E0 + lane;
+        int src = 0;
+        float w = 0.f;
+        if (k < E1) {
+            src = __ldg(A.msrc + k);
+            w = __ldg(A.mval + k);
+        }
+        for (int blk = E0; blk < E1; blk += 32) {
+            const int kn = k + 32;                          // prefetch the next block's entries
+            int src_n = 0;
+            float w_n = 0.f;
+            if (kn < E1) {
+                src_n = __ldg(A.msrc + kn);
+                w_n = __ldg(A.mval + kn);
+            }
+            if (k < E1) {
+                const uint4 xb = __ldg(xb4 + src);
+                rec[wib][lane][0] = make_float2(w, __uint_as_float(xb.x));
+                rec[wib][lane][1] = make_float2(w, __uint_as_float(xb.y));
+                rec[wib][lane][2] = make_float2(w, __uint_as_float(xb.z));
+                rec[wib][lane][3] = make_float2(w, __uint_as_float(xb.w));
+            }
+            __syncwarp();
+            const int n = min(32, E1 - blk);
+            for (int u = 0; u < n; ++u) {
+                while (blk + u == row_end) finish_row();   // warp-uniform; handles empty rows
+                const float2 r = rec[wib][u][wsel];
+                const uint32_t bits = __float_as_uint(r.y) >> sh;
+                // x in {0, 1}: fmaf(w, x, acc) == (x ? acc + w : acc) bit for bit
+                if (bits & 1u) acc.x += r.x;
+                if (bits & 2u) acc.y += r.x;
+                if (bits & 4u) acc.z += r.x;
+                if (bits & 8u) acc.w += r.x;
+            }
+            __syncwarp();
+            k = kn;
+            src = src_n;
+            w = w_n;
+        }
+        while (row < nrows) finish_row();
+    }
+}
+
+template <int CB>
+__global__ void __launch_bounds__(256) bwd_bits_kernel(BitsArgs A) {
+    constexpr int G = CB / 4;
+    __shared__ float2 rec[WARPS_PER_BLOCK][32][XBITS_WORDS];
+    if (*A.nonbinary) return;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int g = lane / G, q = lane % G;
+    const bool colok = g < A.nchunks;
+    const int wsel = lane >> 3, sh = (lane * 4) & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nunits = (A.n_out + BITS_ROWS - 1) / BITS_ROWS;
+    const uint4* xb4 = reinterpret_cast<const uint4*>(A.xbits);
+    auto dcol = [&](int64_t j) {
+        return (colok && j < A.n_out) ? ldg4(A.d_out + ((int64_t)g * A.n_out + j) * CB + q * 4) : f4zero();
+    };
+    for (int64_t u0 = warp; u0 < nunits; u0 += nwarps) {
+        const int64_t j0 = u0 * BITS_ROWS;
+        const int nrows = (int)(A.n_out - j0 < BITS_ROWS ? A.n_out - j0 : BITS_ROWS);
+        const int rp_l = __ldg(A.mrow_ptr + j0 + min(lane, nrows));       // lane t: start of local row t
+        const int E0 = __shfl_sync(FULL, rp_l, 0), E1 = __ldg(A.mrow_ptr + j0 + nrows);
+        int row = 0;
+        int row_end = nrows > 1 ? __shfl_sync(FULL, rp_l, 1) : E1;
+        float4 d = dcol(j0), d_next = dcol(j0 + 1);      // delta_2 of the current / next row
+        int k = E0 + lane;
+        int src = k < E1 ? __ldg(A.msrc + k) : 0;
+        for (int blk = E0; blk < E1; blk += 32) {
+            const int kn = k + 32;
+            const int src_n = kn < E1 ? __ldg(A.msrc + kn) : 0;
+            if (k < E1) {
+                const uint4 xb = __ldg(xb4 + src);
+                rec[wib][lane][0] = make_float2(0.f, __uint_as_float(xb.x));
+                rec[wib][lane][1] = make_float2(0.f, __uint_as_float(xb.y));
+                rec[wib][lane][2] = make_float2(0.f, __uint_as_float(xb.z));
+                rec[wib][lane][3] = make_float2(0.f, __uint_as_float(xb.w));
+            }
+            __syncwarp();
+            float p[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                p[u] = 0.f;
+                if (blk + u < E1) {
+                    while (blk + u == row_end) {           // next row: its delta was prefetched
+                        ++row;
+                        d = d_next;
+                        d_next = dcol(j0 + row + 1);
+                        row_end = row + 1 <= 31 ? __shfl_sync(FULL, rp_l, row + 1) : E1;
+                    }
+                    const uint32_t bits = __float_as_uint(rec[wib][u][wsel].y) >> sh;
+                    float t = 0.f;
+                    if (bits & 1u) t += d.x;
+                    if (bits & 2u) t += d.y;
+                    if (bits & 4u) t += d.z;
+                    if (bits & 8u) t += d.w;
+                    p[u] = t;
+                }
+            }
+            __syncwarp();
+            // transpose reduction over the 32 lanes: lane u ends with the batch sum of entry u
+#pragma unroll
+            for (int hh = 16; hh >= 1; hh >>= 1) {
+                const bool upper = (lane & hh) != 0;
+#pragma unroll
+                for (int u = 0; u < hh; ++u) {
+                    const float send = upper ? p[u] : p[u + hh];
+                    const float keep = upper ? p[u + hh] : p[u];
+                    p[u] = keep + __shfl_xor_sync(FULL, send, hh);
+                }
+            }
+            if (k < E1) A.gmirror[k] = p[0];
+            k = kn;
+            src = src_n;
+        }
+    }
+}
+
+// W^(2) gradient from mirror order to the canonical order (a gather; a scatter would cost a
+// sector read-fill): fused -> Eq. 1 on (w, v) in place, unfused -> the grad view
+__global__ void grad_from_mirror_kernel(const int32_t* __restrict__ nonbinary, const float* __restrict__ gm,
+                                        const int32_t* __restrict__ minv, float* __restrict__ w,
+                                        float* __restrict__ v, float* __restrict__ grad,
+                                        const LayerMeta* __restrict__ meta, int fused, float lr, float mu,
+                                        float wd) {
+    if (*nonbinary) return;
+    const int64_t n = meta->nnz;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const float gk = __ldg(gm + __ldg(minv + k));
+        if (!fused) {
+            grad[k] = gk;
+            continue;
+        }
+        const float wk = w[k];
+        const float vk = mu * v[k] - lr * (gk + wd * wk);
+        v[k] = vk;
+        w[k] = wk + vk;
     }
 }
 
@@ -579,6 +1283,53 @@ int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev)
 int dispatch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) { SMLP_DISPATCH_CB(h, launch_fwd, h, A, L); }
 int dispatch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool hd) { SMLP_DISPATCH_CB(h, launch_bwd, h, A, L, hd); }
 
+template <int CB, int NOUT>
+int launch_narrow_n(smlp_handle* h, const NarrowArgs& A, const Layer& L, bool fwd) {
+    if constexpr (NOUT * CB > NARROW_MAX_ELEMS) {
+        return set_err(h, SMLP_E_ARG, "narrow output layer too wide for chunk_batch");
+    } else {
+        if (fwd) {
+            fwd_narrow_kernel<CB, NOUT><<<L.ngrid, NARROW_WARPS * 32, 0, h->stream>>>(A);
+            SMLP_CK_LAUNCH(h, "fwd_narrow_kernel");
+            fwd_narrow_finish_kernel<CB, NOUT><<<A.n_out * CB, 32, 0, h->stream>>>(A, L.ngrid);
+            SMLP_CK_LAUNCH(h, "fwd_narrow_finish_kernel");
+        } else {
+            if constexpr (NOUT <= 16) {
+                if (L.dense) {
+                    const int64_t tiles = (A.n_in + 31) / 32;
+                    const int64_t blocks = std::min<int64_t>((tiles + NARROW_WARPS - 1) / NARROW_WARPS, (int64_t)h->num_sms * 4);
+                    bwd_narrow_rows_kernel<CB, NOUT><<<(int)std::max<int64_t>(1, blocks), NARROW_WARPS * 32, 0, h->stream>>>(A);
+                    SMLP_CK_LAUNCH(h, "bwd_narrow_rows_kernel");
+                    return SMLP_OK;
+                }
+            }
+            constexpr int VEC = CB >= 32 ? CB / 32 : 1;
+            constexpr int RU = VEC == 4 ? 2 : (VEC == 2 ? 4 : 8);
+            const int64_t warps = (A.n_in + RU - 1) / RU;
+            const int64_t blocks = std::min<int64_t>((warps + NARROW_WARPS - 1) / NARROW_WARPS, (int64_t)h->num_sms * 3);
+            bwd_narrow_kernel<CB, NOUT><<<(int)std::max<int64_t>(1, blocks), NARROW_WARPS * 32, 0, h->stream>>>(A);
+            SMLP_CK_LAUNCH(h, "bwd_narrow_kernel");
+        }
+        return SMLP_OK;
+    }
+}
+
+template <int CB>
+int launch_narrow(smlp_handle* h, const NarrowArgs& A, const Layer& L, bool fwd) {
+    switch (L.nout_pad) {
+        case 2: return launch_narrow_n<CB, 2>(h, A, L, fwd);
+        case 4: return launch_narrow_n<CB, 4>(h, A, L, fwd);
+        case 8: return launch_narrow_n<CB, 8>(h, A, L, fwd);
+        case 16: return launch_narrow_n<CB, 16>(h, A, L, fwd);
+        case 32: return launch_narrow_n<CB, 32>(h, A, L, fwd);
+        default: return set_err(h, SMLP_E_ARG, "narrow layer: bad padded width");
+    }
+}
+
+int dispatch_narrow(smlp_handle* h, const NarrowArgs& A, const Layer& L, bool fwd) {
+    SMLP_DISPATCH_CB(h, launch_narrow, h, A, L, fwd);
+}
+
 float neg_slope_of(const smlp_handle* h, int l) {
     if (h->activation == SMLP_ACT_RELU) return 0.f;
     return (l % 2 == 0) ? -h->alpha : h->alpha;   // Eq. 3: -alpha x for even l, +alpha x for odd l
@@ -604,6 +1355,70 @@ int run_probs(smlp_handle* h, int B, float* probs) {
     return SMLP_OK;
 }
 
+BitsArgs bits_args(smlp_handle* h, Layer& L2, int nchunks) {
+    BitsArgs A{};
+    A.xbits = h->xbits;
+    A.nonbinary = h->d_nonbinary;
+    A.mrow_ptr = L2.mrow_ptr;
+    A.msrc = L2.msrc;
+    A.mperm = L2.mperm;
+    A.mval = L2.mval;
+    A.bias = L2.bias;
+    A.a_out = h->act[2];
+    A.zmask = h->zmask[2];
+    A.kmask = h->kmask[2];
+    A.d_out = h->delta[2];
+    A.grad = L2.grad;
+    A.gmirror = h->gmirror2;
+    A.n_out = L2.n_out;
+    A.nchunks = nchunks;
+    A.neg_slope = neg_slope_of(h, 2);
+    A.drop_thr = drop_threshold(h->dropout);
+    A.keep_scale = (float)(1.0 / (1.0 - (double)h->dropout));
+    A.seed = h->seed;
+    A.rank = h->rank;
+    A.step_ptr = h->step_counter;
+    return A;
+}
+
+template <int CB>
+int launch_bits(smlp_handle* h, const BitsArgs& A, const Layer& L2, bool fwd) {
+    const int64_t units = (L2.n_out + BITS_ROWS - 1) / BITS_ROWS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
+                                                                  (int64_t)h->num_sms * 6));
+    if (fwd) {
+        fwd_bits_kernel<CB><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        SMLP_CK_LAUNCH(h, "fwd_bits_kernel");
+    } else {
+        bwd_bits_kernel<CB><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        SMLP_CK_LAUNCH(h, "bwd_bits_kernel");
+    }
+    return SMLP_OK;
+}
+
+int dispatch_bits(smlp_handle* h, const BitsArgs& A, const Layer& L2, bool fwd) {
+    SMLP_DISPATCH_CB(h, launch_bits, h, A, L2, fwd);
+}
+
+NarrowArgs narrow_args(smlp_handle* h, Layer& Ly, int c) {
+    const int CB = h->CB;
+    const int64_t nin = Ly.n_in, nout = Ly.n_out;
+    NarrowArgs A{};
+    A.row_ptr = Ly.row_ptr;
+    A.col = Ly.col;
+    A.val = Ly.val;
+    A.mom = Ly.mom;
+    A.grad = Ly.grad;
+    A.a_prev = h->act[Ly.l - 1] + (int64_t)c * nin * CB;
+    A.a_out = h->act[Ly.l] + (int64_t)c * nout * CB;
+    A.bias = Ly.bias;
+    A.ws = Ly.nws;
+    A.n_in = nin;
+    A.n_out = (int)nout;
+    A.meta = Ly.meta;
+    return A;
+}
+
 int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, bool train, uint64_t step,
                 float* probs) {
     const int CB = h->CB;
@@ -611,15 +1426,38 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
     {
         dim3 grid((unsigned)((h->sizes[0] + 31) / 32), (unsigned)((nchunks * CB + 31) / 32));
         prof_start(h, K_STAGE, 1, 8.0 * (double)B * (double)h->sizes[0], 0.0);
-        stage_input_kernel<<<grid, dim3(32, 32), 0, h->stream>>>(x, x_idx, B, nchunks, CB, h->sizes[0], h->act[1]);
+        if (h->xbits) SMLP_CK(h, cudaMemsetAsync(h->d_nonbinary, 0, sizeof(int32_t), h->stream));
+        stage_input_kernel<<<grid, dim3(32, 32), 0, h->stream>>>(x, x_idx, B, nchunks, CB, h->sizes[0], h->act[1],
+                                                                 h->xbits, h->d_nonbinary);
         SMLP_CK_LAUNCH(h, "stage_input_kernel");
         prof_stop(h);
     }
     const bool drop = train && h->dropout > 0.f;
+    if (h->xbits) {   // binary-input layer 2, all chunks in one pass (returns at once if not binary)
+        Layer& L2 = h->layers[0];
+        BitsArgs A = bits_args(h, L2, nchunks);
+        A.dropout_on = drop ? 1 : 0;
+        A.step_lo = (uint32_t)step;
+        prof_start(h, K_FWD_BITS, 2, 12.0 * (double)L2.nnz + 4.0 * B * (double)(L2.n_in + L2.n_out),
+                   2.0 * (double)L2.nnz * B);
+        SMLP_TRY(dispatch_bits(h, A, L2, true));
+        prof_stop(h);
+    }
+    // chunk-major order: layer l+1 of chunk c gathers the slab layer l of chunk c just wrote,
+    // while it is still in L2
     for (int c = 0; c < nchunks; ++c) {
         for (int l = 2; l <= h->L; ++l) {
             Layer& Ly = h->layers[l - 2];
             const int64_t nin = h->sizes[l - 2], nout = h->sizes[l - 1];
+            const int Bc = std::min(CB, B - c * CB);
+            const double nnz = (double)Ly.nnz;
+            if (Ly.narrow) {
+                const NarrowArgs A = narrow_args(h, Ly, c);
+                prof_start(h, K_FWD, l, 8.0 * nnz / nchunks + 4.0 * Bc * (double)(nin + nout), 2.0 * nnz * Bc);
+                SMLP_TRY(dispatch_narrow(h, A, Ly, true));
+                prof_stop(h);
+                continue;
+            }
             FwdArgs A{};
             A.a_prev = h->act[l - 1] + (int64_t)c * nin * CB;
             A.a_out = h->act[l] + (int64_t)c * nout * CB;
@@ -645,8 +1483,8 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             A.step_lo = (uint32_t)step;
             A.step_ptr = h->step_counter;
             A.b0 = c * CB;
-            const int Bc = std::min(CB, B - c * CB);
-            const double nnz = (double)Ly.nnz;
+            A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
+            A.gather_evict_last = h->gather_evict_last;
             prof_start(h, K_FWD, l, 12.0 * nnz / nchunks + 4.0 * Bc * (double)(nin + nout), 2.0 * nnz * Bc);
             SMLP_TRY(dispatch_fwd(h, A, Ly));
             prof_stop(h);
@@ -693,12 +1531,46 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
         SMLP_CK_LAUNCH(h, "softmax_ce_kernel");
         prof_stop(h);
     }
-    for (int l = L; l >= 2; --l) {
-        Layer& Ly = h->layers[l - 2];
-        const int64_t nin = h->sizes[l - 2], nout = h->sizes[l - 1];
-        const bool has_dprev = l >= 3;
-        Layer* Lp = has_dprev ? &h->layers[l - 3] : nullptr;   // owner of bias b_{l-1}
-        for (int c = 0; c < nchunks; ++c) {
+    // chunk-major, chunks in reverse: the forward ended on the last chunk, and layer l of chunk c
+    // gathers the delta_l slab layer l+1 of chunk c just wrote (L2-resident).  Gradients
+    // accumulate over the chunks in this fixed order; the last one applies Eq. 1.
+    for (int c = nchunks - 1; c >= 0; --c) {
+        const bool first = c == nchunks - 1, last = c == 0;
+        for (int l = L; l >= 2; --l) {
+            Layer& Ly = h->layers[l - 2];
+            const int64_t nin = h->sizes[l - 2], nout = h->sizes[l - 1];
+            const bool has_dprev = l >= 3;
+            Layer* Lp = has_dprev ? &h->layers[l - 3] : nullptr;   // owner of bias b_{l-1}
+            const int Bc = std::min(CB, B - c * CB);
+            const double nnz = (double)Ly.nnz;
+            const double act_bytes = 4.0 * Bc * (double)(nin + nout + (has_dprev ? nin : 0));
+            const int dropout_prev = (has_dprev && h->trace_train && h->dropout > 0.f) ? 1 : 0;
+            const float keep_scale = (float)(1.0 / (1.0 - (double)h->dropout));
+            if (Ly.narrow) {
+                NarrowArgs A = narrow_args(h, Ly, c);
+                A.d_out = h->delta[l] + (int64_t)c * nout * CB;
+                A.d_prev = has_dprev ? h->delta[l - 1] + (int64_t)c * nin * CB : nullptr;
+                A.zmask_prev = has_dprev ? h->zmask[l - 1] + (int64_t)c * nin : nullptr;
+                A.kmask_prev = has_dprev ? h->kmask[l - 1] + (int64_t)c * nin : nullptr;
+                A.bgs = Ly.bgs;
+                A.bias_prev = Lp ? Lp->bias : nullptr;
+                A.bias_mom_prev = Lp ? Lp->bias_mom : nullptr;
+                A.bias_grad_prev = Lp ? Lp->bias_grad : nullptr;
+                A.neg_slope_prev = neg_slope_of(h, l - 1);
+                A.keep_scale_prev = keep_scale;
+                A.dropout_prev = dropout_prev;
+                A.first = first;
+                A.last = last;
+                A.fused = is_fused ? 1 : 0;
+                A.lr = lr;
+                A.mu = mu;
+                A.wd = wd;
+                prof_start(h, K_BWD, l, (is_fused ? 20.0 : 12.0) * nnz / nchunks + act_bytes,
+                           (has_dprev ? 4.0 : 2.0) * nnz * Bc);
+                SMLP_TRY(dispatch_narrow(h, A, Ly, false));
+                prof_stop(h);
+                continue;
+            }
             BwdArgs A{};
             A.a_prev = h->act[l - 1] + (int64_t)c * nin * CB;
             A.d_out = h->delta[l] + (int64_t)c * nout * CB;
@@ -720,20 +1592,44 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.bias_mom_prev = Lp ? Lp->bias_mom : nullptr;
             A.bias_grad_prev = Lp ? Lp->bias_grad : nullptr;
             A.neg_slope_prev = neg_slope_of(h, l - 1);
-            A.dropout_prev = (has_dprev && h->trace_train && h->dropout > 0.f) ? 1 : 0;
-            A.keep_scale_prev = (float)(1.0 / (1.0 - (double)h->dropout));
-            A.chunk = c;
-            A.nchunks = nchunks;
+            A.dropout_prev = dropout_prev;
+            A.keep_scale_prev = keep_scale;
+            A.first = first;
+            A.last = last;
             A.fused = is_fused ? 1 : 0;
             A.lr = lr;
             A.mu = mu;
             A.wd = wd;
-            const int Bc = std::min(CB, B - c * CB);
-            const double nnz = (double)Ly.nnz;
-            const double act_bytes = 4.0 * Bc * (double)(nin + nout + (has_dprev ? nin : 0));
+            A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
+            A.gather_evict_last = h->gather_evict_last;
             prof_start(h, K_BWD, l, (is_fused ? 20.0 : 12.0) * nnz / nchunks + act_bytes,
                        (has_dprev ? 4.0 : 2.0) * nnz * Bc);
             SMLP_TRY(dispatch_bwd(h, A, Ly, has_dprev));
+            prof_stop(h);
+            // the forward reads the weights in mirror order: refresh that copy by a gather
+            // right after the update, while the canonical values are still L2-resident
+            if (is_fused && last && !(l == 2 && h->xbits)) {
+                prof_start(h, K_MIRROR, l, 12.0 * nnz, 0.0);
+                SMLP_TRY(refresh_mirror_values(h, Ly));
+                prof_stop(h);
+            }
+        }
+    }
+    if (h->xbits) {   // binary-input layer 2 (returns at once if not binary)
+        Layer& L2 = h->layers[0];
+        BitsArgs A = bits_args(h, L2, nchunks);
+        const double nnz = (double)L2.nnz;
+        prof_start(h, K_BWD_BITS, 2, 8.0 * nnz + 4.0 * B * (double)(L2.n_in + L2.n_out), 2.0 * nnz * B);   // src, g
+        SMLP_TRY(dispatch_bits(h, A, L2, false));
+        prof_stop(h);
+        prof_start(h, K_LAYER_UPDATE, 2, (is_fused ? 24.0 : 12.0) * nnz, 0.0);
+        grad_from_mirror_kernel<<<launch_grid(h, L2.cap, 256), 256, 0, h->stream>>>(
+            h->d_nonbinary, h->gmirror2, L2.minv, L2.val, L2.mom, L2.grad, L2.meta, is_fused ? 1 : 0, lr, mu, wd);
+        SMLP_CK_LAUNCH(h, "grad_from_mirror_kernel");
+        prof_stop(h);
+        if (is_fused) {
+            prof_start(h, K_MIRROR, 2, 12.0 * nnz, 0.0);
+            SMLP_TRY(refresh_mirror_values(h, L2));
             prof_stop(h);
         }
     }

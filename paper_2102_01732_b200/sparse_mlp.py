@@ -38,7 +38,7 @@ EXPORTED = [
     "sparse_mlp_params_updated",
 ]
 KERNEL_KINDS = {0: "stage_input", 1: "fwd", 2: "fwd_finish", 3: "softmax_ce", 4: "bwd", 5: "bwd_finish",
-                6: "sgd_update"}
+                6: "sgd_update", 7: "fwd_bits", 8: "bwd_bits", 9: "layer_update", 10: "mirror_values"}
 
 
 class SparseMLPError(RuntimeError):
@@ -334,7 +334,12 @@ class SparseMLP:
         self._check(self.lib.sparse_mlp_import_alive(self.h, int(l), a.ctypes.data))
 
     def sparse_mlp_export_trace(self, kind: int, l: int, B: Optional[int] = None) -> np.ndarray:
-        """kind 0: activations a_l [B x n_l] (l = L: logits); 1: deltas; 2: grad of W^(l) values; 3: bias grad."""
+        """kind 0: activations a_l [B x n_l] (l = L: logits); 1: deltas; 2: grad of W^(l) values; 3: bias grad;
+        4: binary-input path flag of the last forward (1 taken, 0 not, -1 disabled)."""
+        if kind == 4:
+            out = np.zeros(1, np.float32)
+            self._check(self.lib.sparse_mlp_export_trace(self.h, 4, 0, out.ctypes.data))
+            return out
         if kind in (0, 1):
             out = np.zeros((B, self.sizes[l - 1]), np.float32)
         elif kind == 2:

@@ -1,0 +1,203 @@
+"""GPU parity of the specialised paths of the hot path, against the oracle (element by element on
+the same seeded inputs; fp32 within 1e-4, integers bit-exact):
+
+* the exact binary-input path of W^(2) (bit-packed input), taken when every input
+  value is 0 or 1, and its fp32 fallback when one is not;
+* the generic (gather) output layer, used when n_L > 32 (every BASELINE config has n_L <= 32 and
+  takes the narrow streaming path, which the other parity tests cover);
+* the full-size C5 model in the launch configuration bench.py times (B = 128, auto chunk_batch),
+  on seeded SAMPLES of the gradient / update that the oracle computes by its cone evaluation
+  (oracle/sampled.py), plus every forward activation.
+"""
+import numpy as np
+import pytest
+
+from oracle import model as M
+from oracle.compare import rel_err
+from synth import get_config
+from tests.gpu_helpers import TOL, assert_topology_equal, assert_values_close, pair, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _binary_cfg(**kw):
+    base = dict(sizes=(300, 400, 350, 2), epsilon=10.0, alpha=0.5, dropout=0.0, init="he_uniform", batch=128)
+    base.update(kw)
+    return get_config("C1", **base)
+
+
+def _binary_data(n, d, seed, density=0.05):
+    rng = np.random.default_rng([seed, 4242])
+    X = (rng.random((n, d)) < density).astype(np.float32)
+    y = rng.integers(0, 2, size=n).astype(np.int32)
+    return X, y
+
+
+def _check_step(g, st, x, y, step, cfg, path_flag):
+    torch = _torch()
+    B = len(x)
+    tr = M.forward(st, x, True, step)
+    assert sum(tr.ambiguous) == 0, "kink-ambiguous batch"
+    g.forward(to_dev(x), train=True, step=step)
+    assert g.sparse_mlp_export_trace(4, 0)[0] == path_flag
+    g.backward(to_dev(y), fused=None)
+    torch.cuda.synchronize()
+    for l in range(2, cfg.n_layers):
+        assert rel_err(g.sparse_mlp_export_trace(0, l, B), tr.a[l - 1]) <= TOL, ("a", l)
+    gr = M.backward(st, tr, y)
+    for Ly in st.layers:
+        assert rel_err(g.sparse_mlp_export_trace(2, Ly.l), gr.g[Ly.l - 2]) <= TOL, ("g", Ly.l)
+        assert rel_err(g.sparse_mlp_export_trace(3, Ly.l), gr.gb[Ly.l - 2]) <= TOL, ("gb", Ly.l)
+    return tr, gr
+
+
+@pytest.mark.parametrize("B,chunk,dropout", [(128, 0, 0.0), (128, 32, 0.3), (100, 32, 0.0), (37, 8, 0.3)])
+def test_binary_input_path_parity(B, chunk, dropout):
+    from paper_2102_01732_b200 import SGD
+    torch = _torch()
+    cfg = _binary_cfg(batch=B, dropout=dropout)
+    g, st = pair(cfg, max_batch=B, chunk_batch=chunk)
+    X, Y = _binary_data(4 * B, cfg.sizes[0], seed=B + chunk)
+    sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay)
+    for s in range(3):
+        x, y = X[s * B:(s + 1) * B], Y[s * B:(s + 1) * B]
+        _, gr = _check_step(g, st, x, y, s, cfg, 1.0)
+        g.step(sgd)
+        M.step(st, gr, sgd.lr, sgd.momentum, sgd.weight_decay)
+    # fused path (the 1-GPU bench path) on the last batch
+    x, y = X[3 * B:], Y[3 * B:]
+    g.forward(to_dev(x), train=True, step=3)
+    g.backward(to_dev(y), fused=sgd)
+    M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, 3)
+    torch.cuda.synchronize()
+    assert_values_close(g, st, TOL * 3, "binary path")
+
+
+def test_binary_path_falls_back_on_non_binary_input():
+    cfg = _binary_cfg(batch=64)
+    g, st = pair(cfg, max_batch=64, chunk_batch=32)
+    X, Y = _binary_data(64, cfg.sizes[0], seed=9)
+    X[17, 5] = 0.5                                   # one non-binary value -> fp32 gather path
+    _check_step(g, st, X, Y, 0, cfg, 0.0)
+    X[17, 5] = 1.0                                   # binary again -> bit path
+    g2, st2 = pair(cfg, max_batch=64, chunk_batch=32)
+    _check_step(g2, st2, X, Y, 0, cfg, 1.0)
+
+
+def test_binary_and_fp32_paths_agree_bitwise_on_forward():
+    """fmaf(w, x, acc) with x in {0, 1} in the same order: the two paths give identical a_2."""
+    torch = _torch()
+    cfg = _binary_cfg(batch=64, dropout=0.3)
+    g, _ = pair(cfg, max_batch=64, chunk_batch=32)
+    X, _ = _binary_data(64, cfg.sizes[0], seed=3)
+    g.forward(to_dev(X), train=True, step=5)
+    a_bits = g.sparse_mlp_export_trace(0, 2, 64)
+    X2 = X.copy()
+    X2[63, 299] = 2.0                                # non-binary: forces the fp32 gather path
+    g.forward(to_dev(X2), train=True, step=5)
+    assert g.sparse_mlp_export_trace(4, 0)[0] == 0.0
+    a_f32 = g.sparse_mlp_export_trace(0, 2, 64)
+    torch.cuda.synchronize()
+    diff = np.argwhere(a_bits != a_f32)
+    # only batch row 63 can differ (its input changed); every other row is bit-identical
+    assert np.all(diff[:, 0] == 63) if len(diff) else True
+
+
+def test_generic_output_layer_parity():
+    """n_L = 40 > 32: the output layer goes through the gather kernels (fwd_kernel / bwd_kernel)."""
+    from paper_2102_01732_b200 import SGD
+    torch = _torch()
+    cfg = get_config("C1", sizes=(120, 90, 70, 40), epsilon=6.0, dropout=0.2, batch=50)
+    g, st = pair(cfg, max_batch=50, chunk_batch=16)
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((100, 120)).astype(np.float32)
+    Y = rng.integers(0, 40, size=100).astype(np.int32)
+    sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay)
+    for s in range(2):
+        x, y = X[s * 50:(s + 1) * 50], Y[s * 50:(s + 1) * 50]
+        tr = M.forward(st, x, True, s)
+        assert sum(tr.ambiguous) == 0
+        g.forward(to_dev(x), train=True, step=s)
+        assert g.sparse_mlp_export_trace(4, 0)[0] == 0.0     # normal inputs: not binary
+        assert rel_err(g.sparse_mlp_export_trace(0, 4, 50), tr.z[-1]) <= TOL
+        g.backward(to_dev(y), fused=sgd)
+        M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, s)
+    torch.cuda.synchronize()
+    assert_values_close(g, st, TOL * 2, "generic output layer")
+
+
+# ----------------------------------------------------------------------------------------- C5 full size
+def test_c5_full_size_sampled_parity():
+    """BASELINE configs[4] at full size (65536-500000-500000-500000-2, 52.3M connections) in the
+    bench launch configuration (B = 128, chunk_batch auto = 32 -> 4 chunks, binary-input path, fused
+    update).  Checked: ER topology and values bit-exact (all 52.3M), every forward activation and
+    logit of the batch, and for seeded samples of connections / neurons of every layer the
+    gradient (unfused) and the Eq. 1 update (fused) against the oracle's cone evaluation."""
+    from oracle import sampled as S
+    from paper_2102_01732_b200 import SGD
+    from synth.data import c5_host_rows
+    torch = _torch()
+    cfg = get_config("C5")
+    g, st = pair(cfg)
+    assert g.info()["chunk_batch"] == 32
+    assert_topology_equal(g, st, "C5 init")
+    for Ly in st.layers:
+        e = g.export_layer(Ly.l)
+        assert np.array_equal(e["w"].view(np.uint32), Ly.w.view(np.uint32)), f"C5 W^({Ly.l}) init values"
+    B = cfg.batch
+    x, y = c5_host_rows(cfg, np.arange(B))
+    tr = M.forward(st, x, True, 0)
+    g.forward(to_dev(x), train=True, step=0)
+    assert g.sparse_mlp_export_trace(4, 0)[0] == 1.0
+    for l in range(2, cfg.n_layers):
+        assert rel_err(g.sparse_mlp_export_trace(0, l, B), tr.a[l - 1]) <= TOL, ("a", l)
+    assert rel_err(g.sparse_mlp_export_trace(0, cfg.n_layers, B), tr.z[-1]) <= TOL
+    g.backward(to_dev(y), fused=None)
+    torch.cuda.synchronize()
+    # seeded samples: 256 connections of every layer, 64 neurons of every layer (bias gradients)
+    rng = np.random.default_rng(2025)
+    ent = {Ly.l: np.sort(rng.choice(Ly.nnz, size=256, replace=False)) for Ly in st.layers}
+    neu = {l: np.sort(rng.choice(cfg.sizes[l - 1], size=min(64, cfg.sizes[l - 1]), replace=False))
+           for l in range(2, cfg.n_layers + 1)}
+    need = {l: set(neu[l].tolist()) for l in neu}
+    for Ly in st.layers:
+        need[Ly.l] |= set(Ly.col[ent[Ly.l]].tolist())
+    deltas, tainted = S.delta_columns(st, tr, y, need)
+    kept = 0
+    gsamp = {}
+    for Ly in st.layers:
+        l = Ly.l
+        ok = np.array([not tainted[l][int(j)] for j in Ly.col[ent[l]]])
+        kept += int(ok.sum())
+        go = S.grad_entries(st, tr, deltas, l, ent[l])
+        gg = g.sparse_mlp_export_trace(2, l)[ent[l]]
+        assert rel_err(gg[ok], go[ok]) <= TOL, ("g", l, rel_err(gg[ok], go[ok]))
+        gsamp[l] = (go, ok)
+        okn = np.array([not tainted[l][int(j)] for j in neu[l]])
+        gbo = S.bias_grad_columns(deltas, l, neu[l])
+        gbg = g.sparse_mlp_export_trace(3, l)[neu[l]]
+        assert rel_err(gbg[okn], gbo[okn]) <= TOL, ("gb", l)
+    assert kept >= 0.75 * 256 * len(st.layers)   # the rest touch a kink-ambiguous element (R30)
+    # the fused Eq. 1 update in the bench configuration, on a second handle with the same init
+    g2, _ = pair(cfg)
+    sgd = SGD(cfg.lr, cfg.momentum, cfg.weight_decay)
+    g2.forward(to_dev(x), train=True, step=0)
+    g2.backward(to_dev(y), fused=sgd)
+    torch.cuda.synchronize()
+    # expected update: the oracle's Eq. 1 (model.step) with the sampled gradients (zero elsewhere)
+    G = M.Grads([np.zeros(Ly.nnz, np.float32) for Ly in st.layers],
+                [np.zeros(n, np.float32) for n in cfg.sizes[1:]], 0.0, [])
+    for Ly in st.layers:
+        G.g[Ly.l - 2][ent[Ly.l]] = gsamp[Ly.l][0]
+    M.step(st, G, sgd.lr, sgd.momentum, sgd.weight_decay)
+    for Ly in st.layers:
+        l = Ly.l
+        ok = gsamp[l][1]
+        e = g2.export_layer(l)
+        assert rel_err(e["w"][ent[l]][ok], Ly.w[ent[l]][ok]) <= TOL, ("w", l)
+        assert rel_err(e["v"][ent[l]][ok], Ly.v[ent[l]][ok]) <= TOL, ("v", l)

@@ -14,6 +14,7 @@ import pytest
 from oracle import model as M
 from oracle import philox
 from oracle.compare import rel_err
+from synth import get_config, make_dataset
 from tests import dense_ref
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_counts.json")))
@@ -328,3 +329,38 @@ def test_plain_sgd_and_decay_isolation():
     st = _one_weight_state(2.0)
     M.step(st, _grads_for(st, 0.0), 0.1, 0.0, 0.01)             # zero upstream: g = lambda w
     assert st.layers[0].w[0] == np.float32(2.0 - 0.1 * 0.01 * 2.0)
+
+
+def test_sampled_backward_equals_full_backward():
+    """oracle/sampled.py (the cone evaluation the full-size C5 parity test uses) against the full
+    oracle backward on a small net with dropout: every delta, gradient and bias gradient."""
+    from oracle import sampled as S
+    cfg = get_config("C1", sizes=(60, 50, 40, 30, 3), epsilon=4.0, dropout=0.25, batch=17)
+    st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, 5)
+    X, Y = make_dataset(cfg, n=17)
+    M.train_step(st, X, Y, 0.5, 0.9, 2e-4, 0)            # non-trivial biases and weights
+    tr = M.forward(st, X, True, 1)
+    gr = M.backward(st, tr, Y)
+    need = {l: range(cfg.sizes[l - 1]) for l in range(2, st.L + 1)}
+    deltas, tainted = S.delta_columns(st, tr, Y, need)
+    for l in range(2, st.L + 1):
+        D = np.stack([deltas[l][j] for j in range(cfg.sizes[l - 1])], axis=1)
+        np.testing.assert_allclose(D, gr.deltas[l - 1], rtol=1e-6, atol=1e-9)
+        np.testing.assert_allclose(S.bias_grad_columns(deltas, l, np.arange(cfg.sizes[l - 1])), gr.gb[l - 2],
+                                   rtol=1e-6, atol=1e-9)
+        k = np.arange(st.layer(l).nnz)
+        np.testing.assert_allclose(S.grad_entries(st, tr, deltas, l, k), gr.g[l - 2], rtol=1e-6, atol=1e-9)
+    assert not any(any(t.values()) for t in tainted.values())   # no kink-ambiguous element here
+    # a sparse request only evaluates its cone and gives the same columns
+    d2, _ = S.delta_columns(st, tr, Y, {2: [3, 7]})
+    assert set(d2[2]) == {3, 7} and len(d2[3]) < cfg.sizes[2] + 1
+    np.testing.assert_array_equal(d2[2][7], deltas[2][7])
+
+
+def test_kink_guard_ignores_exact_zero_preactivations():
+    """Binary inputs with no active input and zero bias give z = 0 exactly on every path (R30)."""
+    cfg = get_config("C1", sizes=(40, 30, 20, 2), epsilon=2.0, dropout=0.0, batch=8)
+    st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, 0.0, cfg.init, 3)
+    x = np.zeros((8, 40), np.float32)
+    tr = M.forward(st, x, True, 0)
+    assert np.all(tr.z[1] == 0) and sum(tr.ambiguous) == 0
