@@ -197,8 +197,9 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
     // --- neuron-layer buffers
     for (int l = 1; l <= L; ++l) {
         const size_t n = (size_t)h->sizes[l - 1];
-        h->act[l] = zalloc<float>(h, (size_t)h->max_chunks * n * CB, &rc);
-        if (l >= 2) h->delta[l] = zalloc<float>(h, (size_t)h->max_chunks * n * CB, &rc);
+        // + one zero row after the last chunk: the padding target of the row kernels' gather slots
+        h->act[l] = zalloc<float>(h, ((size_t)h->max_chunks * n + 1) * CB, &rc);
+        if (l >= 2) h->delta[l] = zalloc<float>(h, ((size_t)h->max_chunks * n + 1) * CB, &rc);
         if (l >= 2 && l < L) {
             h->zmask[l] = zalloc<uint4>(h, (size_t)h->max_chunks * n, &rc);
             h->kmask[l] = zalloc<uint4>(h, (size_t)h->max_chunks * n, &rc);
@@ -300,6 +301,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     }
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
     if (const char* e = std::getenv("SMLP_GATHER_EVICT_LAST")) h->gather_evict_last = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMLP_KVER")) h->kver = std::atoi(e);
     const int rc = build_handle(h, cfg);
     if (rc != SMLP_OK) {
         g_create_error = h->err;

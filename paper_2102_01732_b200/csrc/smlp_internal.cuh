@@ -28,7 +28,7 @@
 
 namespace smlp {
 
-constexpr int SEG_NNZ = 512;              // max nnz per work segment (long-row split)
+constexpr int SEG_NNZ = 64;               // max nnz per work segment (long-row split; one row-kernel window)
 constexpr int WARPS_PER_BLOCK = 8;        // 256-thread blocks for the warp-per-row kernels
 constexpr int NARROW_MAX = 32;            // output layers with n_L <= 32 take the narrow path
 constexpr int NARROW_MAX_ELEMS = 2048;    // ... if next_pow2(n_L) x chunk_batch <= this
@@ -155,6 +155,7 @@ struct smlp_handle {
     std::vector<smlp::ProfRec> prof_recs;
     std::vector<cudaEvent_t> ev_pool;
     int num_sms = 148;
+    int kver = 3;                   // tuning knob (env SMLP_KVER): 3 = warp-per-row kernels, 2 = group kernels
     int gather_evict_last = 0;      // tuning knob (env SMLP_GATHER_EVICT_LAST): L2 policy of row gathers
     int64_t launches = 0;
     std::string err;

@@ -174,6 +174,7 @@ struct FwdArgs {
     int b0;                   // global batch index of column 0 of this chunk
     const int32_t* skip_if_binary;   // layer 2 with the binary-input path: return if *flag == 0
     int gather_evict_last;           // L2 policy of the gathered rows: evict_last (1) or normal (0)
+    int zero_row;                    // row index (relative to a_prev) of the zero row after the last chunk
 };
 
 // Epilogue of one output row j per group: all 32 lanes call it (ballots); `own` marks the
@@ -307,6 +308,250 @@ __global__ void __launch_bounds__(256) fwd_finish_kernel(FwdArgs A) {
 }
 
 // ------------------------------------------------------------------------------------------
+// "row" kernels (default): one WARP per segment.  The P = 32/G groups of a warp take interleaved
+// entries of the SAME row (entry e of a batch sits in slot u = e / P of group g = e % P), so no
+// group idles while another finishes a longer row, and a whole batch of EB = U*P entries (64 for
+// CB <= 32: a whole Poisson(40) row of C5) has its gathers in flight at once.  Each warp owns a
+// contiguous range of segments, whose entry ranges are then contiguous too; the segment
+// descriptor is loaded two segments ahead, the (index, weight) pairs and the row operand one
+// segment ahead, so a row costs ~one gather round trip.  FMAs are packed (fma.rn.f32x2, bit-for-bit
+// two fmaf).  Partial sums over the groups are combined by a fixed xor butterfly (every lane ends
+// with the same bits), so results stay deterministic.
+// ------------------------------------------------------------------------------------------
+template <int CB>
+struct RowCfg {
+    static constexpr int G = CB / 4;                       // lanes per entry row (one float4 each)
+    static constexpr int P = 32 / G;                       // entries per gather instruction
+    static constexpr int U = (32 / P) < 8 ? (32 / P) : 8;  // gather slots per batch (8 x 16 B in flight per lane)
+    static constexpr int EB = U * P;                       // entries per batch
+    static constexpr int NW = SEG_NNZ / 32;                // window registers per lane (a segment = one window)
+    static constexpr int NB = SEG_NNZ / EB;                // batches per window
+    static constexpr int QS = U < 4 ? U : 4;               // slots per "quad" (issue granularity)
+    static constexpr int NQ = U / QS;                      // quads per batch
+    static constexpr int NR = P >= 4 ? 1 : 4 / P;          // epilogue components per lane
+    static constexpr int S = G >= 8 ? G + 4 : G;           // smem stride of an entry's G partials
+};
+static_assert(SEG_NNZ % 32 == 0, "a segment is a whole number of 32-entry window registers");
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return r;
+}
+// acc += w x (4 fmaf as 2 FFMA2)
+__device__ __forceinline__ void fma4p(float4& acc, float w, const float4& x) {
+    const float2 lo = ffma2(make_float2(w, w), make_float2(x.x, x.y), make_float2(acc.x, acc.y));
+    const float2 hi = ffma2(make_float2(w, w), make_float2(x.z, x.w), make_float2(acc.z, acc.w));
+    acc = make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+// <a, x> over a lane's 4 columns in a fixed order: (a.x x.x + a.z x.z) + (a.y x.y + a.w x.w)
+__device__ __forceinline__ float dot4p(const float4& a, const float4& x) {
+    const float2 m = ffma2(make_float2(a.z, a.w), make_float2(x.z, x.w),
+                           make_float2(a.x * x.x, a.y * x.y));
+    return m.x + m.y;
+}
+__device__ __forceinline__ float4 f4add(const float4& a, const float4& b) {
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 shfl_xor4(const float4& v, int m) {
+    return make_float4(__shfl_xor_sync(FULL, v.x, m), __shfl_xor_sync(FULL, v.y, m),
+                       __shfl_xor_sync(FULL, v.z, m), __shfl_xor_sync(FULL, v.w, m));
+}
+// sum over the P groups of a warp (lanes q, q+G, q+2G, ...): fixed butterfly, identical in all lanes
+template <int G>
+__device__ __forceinline__ float4 group_allreduce(float4 v) {
+#pragma unroll
+    for (int m = G; m < 32; m <<= 1) v = f4add(v, shfl_xor4(v, m));
+    return v;
+}
+
+// cp.async (LDGSTS): global -> shared without a register destination, zero-filled when !valid
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Segment pipeline of the row kernels: the (index, weight) window of segment [beg, end)
+// (<= SEG_NNZ entries) goes to the warp's shared-memory buffer as int2 (row, weight bits) by
+// cp.async one segment ahead, so the prefetch holds no registers.  Entries past the end are
+// zero-filled and then pointed at the zero row after the last chunk (weight 0), so every gather
+// slot of a quad is unconditional.
+__device__ __forceinline__ void window_async(int2* win, const int32_t* __restrict__ idx, const float* __restrict__ wv,
+                                             int beg, int end, int lane) {
+#pragma unroll
+    for (int r = 0; r < SEG_NNZ / 32; ++r) {
+        const int e = lane + 32 * r, k = beg + e;
+        const bool ok = k < end;
+        cp_async4(smem_u32(&win[e].x), idx + (ok ? k : beg), ok);
+        cp_async4(smem_u32(&win[e].y), wv + (ok ? k : beg), ok);
+    }
+}
+__device__ __forceinline__ void window_pad(int2* win, int n, int lane, int zero_row) {
+#pragma unroll
+    for (int r = 0; r < SEG_NNZ / 32; ++r) {
+        const int e = lane + 32 * r;
+        if (e >= n) win[e].x = zero_row;
+    }
+}
+
+// forward epilogue of one complete row j (acc = the row's sum, identical in every lane): lane
+// (g, q) finishes components c = r P + g of its float4 (columns 4q + c), so all 32 lanes share
+// the bias / All-ReLU / dropout / mask work and the store is one coalesced row.
+template <int CB>
+__device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, const float4& acc, float bj, int lane,
+                                                  uint32_t step_lo) {
+    using C = RowCfg<CB>;
+    constexpr int G = C::G, P = C::P, NR = C::NR;
+    const int g = lane / G, q = lane % G;
+    uint32_t bal_p[NR], bal_k[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        const int c = r * P + g;
+        const bool valid = c < 4;
+        const float z = comp(acc, c & 3) + bj;
+        float* dst = A.a_out + j * CB + q * 4 + (c & 3);
+        if (!A.hidden) {
+            if (valid) *dst = z;
+            continue;
+        }
+        const bool pos = z > 0.f;
+        float a = pos ? z : A.neg_slope * z;
+        bool keep = true;
+        if (A.dropout_on && valid) {
+            const uint64_t b = (uint64_t)(A.b0 + q * 4 + c);
+            const uint64_t e = b * (uint64_t)A.n_out + (uint64_t)j;
+            const uint4 rr = rng_stream(A.seed, P_DROPOUT, A.rank, A.layer, step_lo, e >> 2);
+            keep = word(rr, (int)(e & 3)) >= A.drop_thr;
+            a = keep ? a * A.keep_scale : 0.f;
+        }
+        if (valid) *dst = a;
+        bal_p[r] = __ballot_sync(FULL, valid && pos);
+        bal_k[r] = __ballot_sync(FULL, valid && keep);
+    }
+    if (A.hidden && lane == 0) {
+        uint32_t zb[4], kb[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {   // word c, bit q = column 4q + c, held by group c % P of ballot c / P
+            zb[c] = group_bits<G>(bal_p[(c / P) % NR], c % P);
+            kb[c] = group_bits<G>(bal_k[(c / P) % NR], c % P);
+        }
+        A.zmask[j] = make_uint4(zb[0], zb[1], zb[2], zb[3]);
+        if (A.dropout_on) A.kmask[j] = make_uint4(kb[0], kb[1], kb[2], kb[3]);
+    }
+}
+
+// NS gather slots of a batch, all issued before the first FMA (entry u P + g of the window in slot u)
+template <int CB, int NS>
+__device__ __forceinline__ void fwd_slots(const float* __restrict__ a_prev, const int2* win, int g, int q,
+                                          float4& acc) {
+    constexpr int P = RowCfg<CB>::P;
+    float4 x[NS];
+    float wv[NS];
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+        const int2 e = win[u * P + g];
+        wv[u] = __int_as_float(e.y);
+        x[u] = ldg4(a_prev + (int64_t)e.x * CB + q * 4);
+    }
+#pragma unroll
+    for (int u = 0; u < NS; ++u) fma4p(acc, wv[u], x[u]);
+}
+
+// one batch of nb <= EB entries: the smallest number of quads covering it (warp-uniform switch,
+// one fully unrolled body per length class; the padding slots gather the zero row)
+template <int CB>
+__device__ __forceinline__ void fwd_batch(const float* __restrict__ a_prev, const int2* win, int nb, int g, int q,
+                                          float4& acc) {
+    using C = RowCfg<CB>;
+    if constexpr (C::NQ == 1) {
+        fwd_slots<CB, C::QS>(a_prev, win, g, q, acc);
+    } else {
+        if (nb > C::QS * C::P) fwd_slots<CB, C::U>(a_prev, win, g, q, acc);
+        else fwd_slots<CB, C::QS>(a_prev, win, g, q, acc);
+    }
+}
+
+// register-prefetched window (the forward keeps its LSU for the gathers: no LDGSTS)
+template <int NW>
+__device__ __forceinline__ void load_window(const int32_t* __restrict__ idx, const float* __restrict__ wv, int beg,
+                                            int end, int lane, int (&ix)[NW], float (&w)[NW]) {
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+        const int k = beg + lane + 32 * r;
+        ix[r] = k < end ? __ldg(idx + k) : 0;
+        w[r] = k < end ? __ldg(wv + k) : 0.f;
+    }
+}
+template <int NW>
+__device__ __forceinline__ void stage_window(int2* win, const int (&ix)[NW], const float (&w)[NW], int n, int lane,
+                                             int zero_row) {
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+        const int e = lane + 32 * r;
+        win[e] = e < n ? make_int2(ix[r], __float_as_int(w[r])) : make_int2(zero_row, 0);
+    }
+}
+
+template <int CB>
+__global__ void __launch_bounds__(256, 4) fwd_rows_kernel(FwdArgs A) {
+    using C = RowCfg<CB>;
+    constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB;
+    __shared__ int2 win_all[WARPS_PER_BLOCK][SEG_NNZ];
+    if (A.skip_if_binary && *A.skip_if_binary == 0) return;
+    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
+    int2* win = win_all[threadIdx.x >> 5];
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nseg = A.meta->n_fseg;
+    const int64_t s_lo = warp * nseg / nwarps, s_hi = (warp + 1) * nseg / nwarps;
+    if (s_lo >= s_hi) return;
+    const uint32_t step_lo = A.step_ptr ? (uint32_t)(*A.step_ptr) : A.step_lo;
+    const int4 none = make_int4(0, 0, 0, -2);
+    int4 cur = A.seg[s_lo];
+    int4 nxt = s_lo + 1 < s_hi ? A.seg[s_lo + 1] : none;
+    int ix[NW];
+    float w[NW];
+    load_window<NW>(A.msrc, A.mval, cur.y, cur.z, lane, ix, w);
+    for (int64_t s = s_lo; s < s_hi; ++s) {
+        const int4 nn = s + 2 < s_hi ? A.seg[s + 2] : none;      // descriptor two ahead
+        int ix_n[NW];
+        float w_n[NW];
+        load_window<NW>(A.msrc, A.mval, nxt.y, nxt.z, lane, ix_n, w_n);   // indices one ahead
+        const float bj = cur.w < 0 ? __ldg(A.bias + cur.x) : 0.f;         // consumed after the gathers
+        const int n = cur.z - cur.y;
+        __syncwarp();
+        stage_window<NW>(win, ix, w, n, lane, A.zero_row);
+        __syncwarp();
+        float4 acc = f4zero();
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+            if (b * EB < n) fwd_batch<CB>(A.a_prev, win + b * EB, n - b * EB, g, q, acc);
+        acc = group_allreduce<G>(acc);
+        if (cur.w < 0) {
+            fwd_rows_epilogue<CB>(A, cur.x, acc, bj, lane, step_lo);
+        } else if (g == 0) {
+            st4(A.ws + (int64_t)cur.w * CB + q * 4, acc);
+        }
+        cur = nxt;
+        nxt = nn;
+#pragma unroll
+        for (int r = 0; r < NW; ++r) {
+            ix[r] = ix_n[r];
+            w[r] = w_n[r];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // softmax cross-entropy (single block, fixed-order reductions)
 // ------------------------------------------------------------------------------------------
 struct SoftmaxArgs {
@@ -425,6 +670,7 @@ struct BwdArgs {
     float lr, mu, wd;
     const int32_t* skip_if_binary;   // layer 2 with the binary-input path: return if *flag == 0
     int gather_evict_last;           // L2 policy of the gathered rows: evict_last (1) or normal (0)
+    int zero_row;                    // row index (relative to d_out) of the zero row after the last chunk
 };
 
 // delta_{l-1} of input row i per group: f'(z) from the sign bits, dropout keep bits, store, and
@@ -575,6 +821,223 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
         bwd_epilogue<CB>(A, m.x, acc, active, lane);
     }
 }
+
+// backward epilogue of one complete input row i (d = sum_j w_ij delta_l[j], identical in every
+// lane): f'_{l-1} from the sign bits, dropout keep bits, store of delta_{l-1}[i], and the bias
+// gradient of layer l-1 (a fixed 32-lane butterfly, then accumulated over chunks in order)
+struct BwdSide {            // per-row operands of the backward epilogue (loaded before the gathers)
+    uint4 zb, kb;           // sign / keep bits of layer l-1, row i
+    float bgs, bmom, bval;  // lane 0: bias-grad accumulator, bias momentum and bias of neuron i
+};
+template <bool DROP>
+__device__ __forceinline__ BwdSide bwd_side(const BwdArgs& A, int64_t i, bool valid, int lane) {
+    BwdSide t;
+    t.zb = make_uint4(0, 0, 0, 0);
+    t.kb = make_uint4(FULL, FULL, FULL, FULL);
+    t.bgs = t.bmom = t.bval = 0.f;
+    if (!valid) return t;
+    t.zb = A.zmask_prev[i];
+    if (DROP) t.kb = A.kmask_prev[i];
+    if (lane == 0) {
+        if (!A.first) t.bgs = A.bgs[i];
+        if (A.last && A.fused) {
+            t.bmom = A.bias_mom_prev[i];
+            t.bval = A.bias_prev[i];
+        }
+    }
+    return t;
+}
+
+template <int CB>
+__device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, const float4& d, const BwdSide& sd,
+                                                  int lane) {
+    using C = RowCfg<CB>;
+    constexpr int G = C::G, P = C::P, NR = C::NR;
+    const int g = lane / G, q = lane % G;
+    const uint4 zb = sd.zb, kb = sd.kb;
+    float s = 0.f;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        const int c = r * P + g;
+        if (c < 4) {
+            const bool pos = (word(zb, c) >> q) & 1u;
+            const bool keep = (word(kb, c) >> q) & 1u;
+            const float v = comp(d, c) * (pos ? 1.f : A.neg_slope_prev);
+            const float o = A.dropout_prev ? (keep ? v * A.keep_scale_prev : 0.f) : v;
+            A.d_prev[i * CB + q * 4 + c] = o;
+            s += o;
+        }
+    }
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) s += __shfl_xor_sync(FULL, s, m);
+    if (lane == 0) {
+        float tot = s;
+        if (!A.first) tot += A.bgs[i];
+        if (!A.last) {
+            A.bgs[i] = tot;
+        } else if (A.fused) {
+            const float v = A.mu * A.bias_mom_prev[i] - A.lr * tot;
+            A.bias_mom_prev[i] = v;
+            A.bias_prev[i] = A.bias_prev[i] + v;
+        } else {
+            A.bias_grad_prev[i] = tot;
+        }
+    }
+}
+
+// NS slots of a backward batch: gathers first, then delta_{l-1} += w delta_l[j] (a4) and the
+// partial SDDMM dot <a_{l-1}[i], delta_l[j]> over the lane's 4 columns into shared memory (a5)
+template <int CB, int NS, bool HAS_DPREV>
+__device__ __forceinline__ void bwd_slots(const float* __restrict__ d_out, const int2* win, float* red,
+                                          const float4& ai, int g, int q, float4& dacc) {
+    using C = RowCfg<CB>;
+    constexpr int P = C::P, S = C::S;
+    float4 dx[NS];
+    float wv[NS];
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+        const int2 e = win[u * P + g];
+        wv[u] = __int_as_float(e.y);
+        dx[u] = ldg4(d_out + (int64_t)e.x * CB + q * 4);
+    }
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+        if (HAS_DPREV) fma4p(dacc, wv[u], dx[u]);
+        red[(u * P + g) * S + q] = dot4p(ai, dx[u]);
+    }
+}
+
+template <int CB, bool HAS_DPREV>
+__device__ __forceinline__ void bwd_batch(const float* __restrict__ d_out, const int2* win, float* red, int nb,
+                                          const float4& ai, int g, int q, float4& dacc) {
+    using C = RowCfg<CB>;
+    if constexpr (C::NQ == 1) {
+        bwd_slots<CB, C::QS, HAS_DPREV>(d_out, win, red, ai, g, q, dacc);
+    } else {
+        if (nb > C::QS * C::P) bwd_slots<CB, C::U, HAS_DPREV>(d_out, win, red, ai, g, q, dacc);
+        else bwd_slots<CB, C::QS, HAS_DPREV>(d_out, win, red, ai, g, q, dacc);
+    }
+}
+
+// GOLD: add the gradient accumulated by earlier chunks; UPD: last chunk of the fused path (Eq. 1
+// on (w, v) in place); DROP: dropout on layer l-1
+template <int CB, bool HAS_DPREV, bool GOLD, bool UPD, bool DROP>
+__global__ void __launch_bounds__(256, 3) bwd_rows_kernel(BwdArgs A) {
+    using C = RowCfg<CB>;
+    constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB, S = C::S;
+    __shared__ int2 win_all[WARPS_PER_BLOCK][2][SEG_NNZ];
+    __shared__ __align__(16) float4 ai_all[WARPS_PER_BLOCK][2][G];
+    __shared__ __align__(16) float red_all[WARPS_PER_BLOCK][EB * S];
+    if (A.skip_if_binary && *A.skip_if_binary == 0) return;
+    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
+    const int wib = threadIdx.x >> 5;
+    int2 (*win)[SEG_NNZ] = win_all[wib];
+    float4 (*ais)[G] = ai_all[wib];
+    float* red = red_all[wib];
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nseg = A.meta->n_bseg;
+    const int64_t s_lo = warp * nseg / nwarps, s_hi = (warp + 1) * nseg / nwarps;
+    if (s_lo >= s_hi) return;
+    const int4 none = make_int4(0, 0, 0, -2);
+    // window + a_{l-1}[i] of a segment into buffer b (cp.async, one segment ahead)
+    auto prefetch = [&](const int4& sg, int b) {
+        window_async(win[b], A.col, A.val, sg.y, sg.z, lane);
+        if (lane < G) cp_async16(smem_u32(&ais[b][lane]), A.a_prev + (int64_t)(sg.w != -2 ? sg.x : 0) * CB + lane * 4,
+                                 sg.w != -2);
+        cp_async_commit();
+    };
+    int4 cur = A.seg[s_lo];
+    int4 nxt = s_lo + 1 < s_hi ? A.seg[s_lo + 1] : none;
+    prefetch(cur, 0);
+    int buf = 0;
+    for (int64_t s = s_lo; s < s_hi; ++s) {
+        const int4 nn = s + 2 < s_hi ? A.seg[s + 2] : none;
+        prefetch(nxt, buf ^ 1);
+        // operands consumed after the gathers: the lane's entries' weight / gradient / momentum,
+        // and the row's epilogue side data
+        const int n = cur.z - cur.y;
+        float w[NW], gold[NW], mold[NW];
+#pragma unroll
+        for (int r = 0; r < NW; ++r) {
+            const int k = cur.y + lane + 32 * r;
+            const bool ok = lane + 32 * r < n;
+            w[r] = UPD && ok ? __ldg(A.val + k) : 0.f;
+            gold[r] = GOLD && ok ? A.grad[k] : 0.f;
+            mold[r] = UPD && ok ? A.mom[k] : 0.f;
+        }
+        const BwdSide sd = bwd_side<DROP>(A, cur.x, HAS_DPREV && cur.w < 0, lane);
+        cp_async_wait1();
+        __syncwarp();
+        window_pad(win[buf], n, lane, A.zero_row);
+        __syncwarp();
+        const float4 ai = ais[buf][q];
+        float4 dacc = f4zero();
+        float gsum[NW];
+#pragma unroll
+        for (int r = 0; r < NW; ++r) gsum[r] = 0.f;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            if (b * EB < n) {
+                const int nb = min(EB, n - b * EB);
+                bwd_batch<CB, HAS_DPREV>(A.d_out, win[buf] + b * EB, red, nb, ai, g, q, dacc);
+                __syncwarp();
+                // window entry e = lane + 32 r is entry e - b EB of this batch: fixed-order sum of its
+                // G lane partials
+#pragma unroll
+                for (int r = 0; r < NW; ++r) {
+                    const int e = lane + 32 * r - b * EB;
+                    if (e >= 0 && e < nb) {
+                        const float* pr = red + e * S;
+                        float t;
+                        if constexpr (G % 4 == 0) {
+                            float4 a4 = *reinterpret_cast<const float4*>(pr);
+                            t = (a4.x + a4.y) + (a4.z + a4.w);
+#pragma unroll
+                            for (int v = 4; v < G; v += 4) {
+                                a4 = *reinterpret_cast<const float4*>(pr + v);
+                                t += (a4.x + a4.y) + (a4.z + a4.w);
+                            }
+                        } else {
+                            t = pr[0];
+#pragma unroll
+                            for (int v = 1; v < G; ++v) t += pr[v];
+                        }
+                        gsum[r] = t;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < NW; ++r) {
+            const int k = cur.y + lane + 32 * r;
+            if (lane + 32 * r < n) {
+                const float gk = gsum[r] + gold[r];
+                if (!UPD) {
+                    A.grad[k] = gk;
+                } else {
+                    const float v = A.mu * mold[r] - A.lr * (gk + A.wd * w[r]);
+                    A.mom[k] = v;
+                    A.val[k] = w[r] + v;
+                }
+            }
+        }
+        if (HAS_DPREV) {
+            dacc = group_allreduce<G>(dacc);
+            if (cur.w < 0) {
+                bwd_rows_epilogue<CB>(A, cur.x, dacc, sd, lane);
+            } else if (g == 0) {
+                st4(A.ws + (int64_t)cur.w * CB + q * 4, dacc);
+            }
+        }
+        __syncwarp();
+        cur = nxt;
+        nxt = nn;
+        buf ^= 1;
+    }
+}
+
 
 // ------------------------------------------------------------------------------------------
 // narrow output layer (l = L, n_L <= NARROW_MAX): both passes walk the canonical CSR rows i of
@@ -1237,12 +1700,30 @@ int persistent_grid(const smlp_handle* h, int64_t groups, int groups_per_warp) {
     return (int)std::max<int64_t>(1, std::min(need, cap));
 }
 
+// one resident wave of a row kernel: blocks/SM from the occupancy calculator (cached per kernel)
+template <typename K>
+int rows_grid(const smlp_handle* h, K kernel, int64_t segs) {
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, WARPS_PER_BLOCK * 32, 0) != cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+    }
+    const int64_t need = (segs + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)per_sm * h->num_sms));
+}
+
 template <int CB>
 int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
     constexpr int P = 32 / (CB / 4);
-    const int grid = persistent_grid(h, L.fseg_cap, P);
-    fwd_kernel<CB><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
-    SMLP_CK_LAUNCH(h, "fwd_kernel");
+    if (h->kver >= 3) {
+        fwd_rows_kernel<CB><<<rows_grid(h, fwd_rows_kernel<CB>, L.fseg_cap), WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        SMLP_CK_LAUNCH(h, "fwd_rows_kernel");
+    } else {
+        const int grid = persistent_grid(h, L.fseg_cap, P);
+        fwd_kernel<CB><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        SMLP_CK_LAUNCH(h, "fwd_kernel");
+    }
     if (L.fslot_cap > 0) {
         const int g2 = persistent_grid(h, std::max<int64_t>(1, L.fslot_cap / 2), P);
         fwd_finish_kernel<CB><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
@@ -1254,13 +1735,40 @@ int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
 template <int CB>
 int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev) {
     constexpr int P = 32 / (CB / 4);
-    const int grid = persistent_grid(h, L.bseg_cap, P);
-    if (has_dprev) {
-        bwd_kernel<CB, true><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+    if (h->kver >= 3) {
+        const bool gold = !A.first, upd = A.last && A.fused, drop = A.dropout_prev != 0;
+        const int mode = (has_dprev ? 8 : 0) | (gold ? 4 : 0) | (upd ? 2 : 0) | (drop ? 1 : 0);
+#define SMLP_BWD_ROWS(HD, GO, UP, DR)                                                                          \
+    case (HD ? 8 : 0) | (GO ? 4 : 0) | (UP ? 2 : 0) | (DR ? 1 : 0):                                         \
+        bwd_rows_kernel<CB, HD, GO, UP, DR><<<rows_grid(h, bwd_rows_kernel<CB, HD, GO, UP, DR>, L.bseg_cap),      \
+                                              WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);                      \
+        break;
+        switch (mode) {
+            SMLP_BWD_ROWS(true, false, false, false)
+            SMLP_BWD_ROWS(true, false, false, true)
+            SMLP_BWD_ROWS(true, false, true, false)
+            SMLP_BWD_ROWS(true, false, true, true)
+            SMLP_BWD_ROWS(true, true, false, false)
+            SMLP_BWD_ROWS(true, true, false, true)
+            SMLP_BWD_ROWS(true, true, true, false)
+            SMLP_BWD_ROWS(true, true, true, true)
+            SMLP_BWD_ROWS(false, false, false, false)
+            SMLP_BWD_ROWS(false, false, true, false)
+            SMLP_BWD_ROWS(false, true, false, false)
+            SMLP_BWD_ROWS(false, true, true, false)
+            default: return set_err(h, SMLP_E_ARG, "bwd_rows_kernel: bad mode");
+        }
+#undef SMLP_BWD_ROWS
+        SMLP_CK_LAUNCH(h, "bwd_rows_kernel");
     } else {
-        bwd_kernel<CB, false><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        const int grid = persistent_grid(h, L.bseg_cap, P);
+        if (has_dprev) {
+            bwd_kernel<CB, true><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        } else {
+            bwd_kernel<CB, false><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        }
+        SMLP_CK_LAUNCH(h, "bwd_kernel");
     }
-    SMLP_CK_LAUNCH(h, "bwd_kernel");
     if (has_dprev && L.bslot_cap > 0) {
         const int g2 = persistent_grid(h, std::max<int64_t>(1, L.bslot_cap / 2), P);
         bwd_finish_kernel<CB><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
@@ -1485,6 +1993,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             A.b0 = c * CB;
             A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
             A.gather_evict_last = h->gather_evict_last;
+            A.zero_row = (int)((int64_t)(h->max_chunks - c) * nin);
             prof_start(h, K_FWD, l, 12.0 * nnz / nchunks + 4.0 * Bc * (double)(nin + nout), 2.0 * nnz * Bc);
             SMLP_TRY(dispatch_fwd(h, A, Ly));
             prof_stop(h);
@@ -1602,6 +2111,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.wd = wd;
             A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
             A.gather_evict_last = h->gather_evict_last;
+            A.zero_row = (int)((int64_t)(h->max_chunks - c) * nout);
             prof_start(h, K_BWD, l, (is_fused ? 20.0 : 12.0) * nnz / nchunks + act_bytes,
                        (has_dprev ? 4.0 : 2.0) * nnz * Bc);
             SMLP_TRY(dispatch_bwd(h, A, Ly, has_dprev));

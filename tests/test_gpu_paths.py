@@ -89,8 +89,9 @@ def test_binary_path_falls_back_on_non_binary_input():
     _check_step(g2, st2, X, Y, 0, cfg, 1.0)
 
 
-def test_binary_and_fp32_paths_agree_bitwise_on_forward():
-    """fmaf(w, x, acc) with x in {0, 1} in the same order: the two paths give identical a_2."""
+def test_binary_and_fp32_paths_agree_on_forward():
+    """The bit path and the fp32 gather path compute the same a_2 up to the summation order
+    (each is a fixed order, R27): every batch row but the changed one agrees to fp32 rounding."""
     torch = _torch()
     cfg = _binary_cfg(batch=64, dropout=0.3)
     g, _ = pair(cfg, max_batch=64, chunk_batch=32)
@@ -103,9 +104,12 @@ def test_binary_and_fp32_paths_agree_bitwise_on_forward():
     assert g.sparse_mlp_export_trace(4, 0)[0] == 0.0
     a_f32 = g.sparse_mlp_export_trace(0, 2, 64)
     torch.cuda.synchronize()
-    diff = np.argwhere(a_bits != a_f32)
-    # only batch row 63 can differ (its input changed); every other row is bit-identical
-    assert np.all(diff[:, 0] == 63) if len(diff) else True
+    keep = np.ones(a_bits.shape[0], bool)
+    keep[63] = False                                 # only batch row 63's input changed
+    a, b = a_bits[keep].astype(np.float64), a_f32[keep].astype(np.float64)
+    scale = np.maximum(np.abs(a), 1e-3 * np.abs(a).max())
+    assert np.max(np.abs(a - b) / scale) < 1e-5
+    assert not np.array_equal(a_bits[63], a_f32[63])
 
 
 def test_generic_output_layer_parity():

@@ -1,0 +1,666 @@
+// spmm_bench.cu — design microbenchmark for the C5 hidden-layer forward SpMM.
+//
+// z[j][0..CB) = sum_{k in row j} w_k * a[src_k][0..CB) over an output-major CSR with Poisson(40)
+// rows (500000 x 500000, 20M nnz, the C5 hidden layers), a chunk slab a[n_in][CB] fp32.
+// Variants compare how the random 4*CB-byte row gathers are kept in flight:
+//   bench   : the plain gather loop of tools/gather_bench.cu over the same index stream (ceiling)
+//   group   : G = CB/4 lanes per row, P = 32/G rows per warp in lock-step, 8 gathers per lane per block
+//   row<NS> : one warp per row, (src, w) window staged in shared memory, NS gather slots per lane
+//             (row padded to the slot count with a zero row), all issued before the first FMA
+//   rowpol  : row<16> with L2 hints: gathers evict_last, index stream evict_first
+//   tma     : one warp per row, rows gathered into a per-warp shared-memory ring by TMA
+//             gather4 (cp.async.bulk.tensor.2d.tile::gather4), NST stages in flight, mbarrier per stage
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o spmm_bench tools/spmm_bench.cu
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#define CK(x)                                                                       \
+    do {                                                                            \
+        cudaError_t e = (x);                                                        \
+        if (e != cudaSuccess) {                                                     \
+            printf("%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e)); \
+            exit(1);                                                                \
+        }                                                                           \
+    } while (0)
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int MAXROW = 64;   // rows are clipped to 64 entries (the real path splits longer rows)
+
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ uint64_t pol_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float4 ldg4_pol(const float* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int ldg_i_pol(const int* p, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ldg_f_pol(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void fma4(float4& a, float w, const float4& x) {
+    a.x = fmaf(w, x.x, a.x);
+    a.y = fmaf(w, x.y, a.y);
+    a.z = fmaf(w, x.z, a.z);
+    a.w = fmaf(w, x.w, a.w);
+}
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+template <int G>
+__device__ __forceinline__ float4 allred(float4 v) {
+#pragma unroll
+    for (int m = G; m < 32; m <<= 1)
+        v = f4add(v, make_float4(__shfl_xor_sync(FULL, v.x, m), __shfl_xor_sync(FULL, v.y, m),
+                                 __shfl_xor_sync(FULL, v.z, m), __shfl_xor_sync(FULL, v.w, m)));
+    return v;
+}
+
+struct Csr {
+    const int* rp;
+    const int* src;
+    const float* w;
+    const float* a;
+    float* z;
+    int n_out;
+    int zero_row;
+};
+
+template <int MODE>
+__device__ __forceinline__ float4 ldmode(const float* p) {
+    float4 v;
+    if constexpr (MODE == 0) {
+        v = __ldg(reinterpret_cast<const float4*>(p));
+    } else if constexpr (MODE == 1) {
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    } else if constexpr (MODE == 2) {
+        asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    } else {
+        asm volatile("ld.global.nc.L2::128B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    }
+    return v;
+}
+
+// ---- bench: plain gathers over the index stream (no rows)
+template <int CB, int MODE = 0>
+__global__ void __launch_bounds__(256) k_bench(Csr C, long nnz) {
+    constexpr int G = CB / 4, P = 32 / G, U = 8;
+    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
+    const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * (long)blockDim.x) >> 5;
+    float4 acc = make_float4(0, 0, 0, 0);
+    for (long base = warp * 32; base < nnz; base += nw * 32) {
+        const int my = base + lane < nnz ? C.src[base + lane] : 0;
+#pragma unroll
+        for (int t0 = 0; t0 < 32; t0 += P * U) {
+            float4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int r = __shfl_sync(FULL, my, (t0 + u * P + g) & 31);
+                x[u] = ldmode<MODE>(C.a + (long)r * CB + q * 4);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc = f4add(acc, x[u]);
+        }
+    }
+    if (acc.x == 1234.5f) C.z[0] = acc.y;
+}
+
+// ---- group: G lanes per row, P rows per warp in lock-step (the v2 library kernel's scheme)
+template <int CB>
+__global__ void __launch_bounds__(256) k_group(Csr C) {
+    constexpr int G = CB / 4, P = 32 / G, U = G < 8 ? G : 8;
+    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G, gb = g * G;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r0 = warp * P; r0 < C.n_out; r0 += nw * P) {
+        const int j = r0 + g;
+        const bool act = j < C.n_out;
+        const int beg = act ? C.rp[j] : 0, end = act ? C.rp[j + 1] : 0;
+        const int maxblk = __reduce_max_sync(FULL, (end - beg + G - 1) / G);
+        float4 acc = make_float4(0, 0, 0, 0);
+        int k = beg + q;
+        int s = k < end ? C.src[k] : 0;
+        float w = k < end ? C.w[k] : 0.f;
+        for (int b = 0; b < maxblk; ++b) {
+            const int kn = k + G;
+            const int sn = kn < end ? C.src[kn] : 0;
+            const float wn = kn < end ? C.w[kn] : 0.f;
+            const int base = beg + b * G;
+#pragma unroll
+            for (int u0 = 0; u0 < G; u0 += U) {
+                float4 x[U];
+                float wv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int ss = __shfl_sync(FULL, s, gb + u0 + u);
+                    wv[u] = __shfl_sync(FULL, w, gb + u0 + u);
+                    x[u] = base + u0 + u < end ? ldg4(C.a + (long)ss * CB + q * 4) : make_float4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) fma4(acc, wv[u], x[u]);
+            }
+            k = kn;
+            s = sn;
+            w = wn;
+        }
+        if (act) *reinterpret_cast<float4*>(C.z + (long)j * CB + q * 4) = acc;
+    }
+}
+
+// ---- row<NS>: one warp per row, smem window, NS slots, quad-granular switch
+template <int CB, int NS, bool POL>
+__device__ __forceinline__ void row_slots(const Csr& C, const int2* win, int g, int q, float4& acc, uint64_t pg) {
+    constexpr int P = 32 / (CB / 4);
+    float4 x[NS];
+    float wv[NS];
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+        const int2 e = win[u * P + g];
+        wv[u] = __int_as_float(e.y);
+        x[u] = POL ? ldg4_pol(C.a + (long)e.x * CB + q * 4, pg) : ldg4(C.a + (long)e.x * CB + q * 4);
+    }
+#pragma unroll
+    for (int u = 0; u < NS; ++u) fma4(acc, wv[u], x[u]);
+}
+
+template <int CB, int U, bool POL, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_row(Csr C) {
+    constexpr int G = CB / 4, P = 32 / G, QS = U < 4 ? U : 4;
+    __shared__ int2 win_all[8][MAXROW];
+    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
+    int2* win = win_all[threadIdx.x >> 5];
+    const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * (long)blockDim.x) >> 5;
+    const long r_lo = warp * C.n_out / nw, r_hi = (warp + 1) * C.n_out / nw;
+    if (r_lo >= r_hi) return;
+    const uint64_t pf = POL ? pol_first() : 0, pg = POL ? pol_last() : 0;
+    auto ldi = [&](int k, int end, int& s, float& w) {
+        if (POL) {
+            s = k < end ? ldg_i_pol(C.src + k, pf) : 0;
+            w = k < end ? ldg_f_pol(C.w + k, pf) : 0.f;
+        } else {
+            s = k < end ? __ldg(C.src + k) : 0;
+            w = k < end ? __ldg(C.w + k) : 0.f;
+        }
+    };
+    int beg = C.rp[r_lo], end = C.rp[r_lo + 1];
+    int end_n = r_lo + 1 < r_hi ? C.rp[r_lo + 2] : end;
+    int s0, s1;
+    float w0, w1;
+    ldi(beg + lane, end, s0, w0);
+    ldi(beg + 32 + lane, end, s1, w1);
+    for (long r = r_lo; r < r_hi; ++r) {
+        const int end_nn = r + 2 < r_hi ? C.rp[r + 3] : end_n;
+        int t0, t1;
+        float v0, v1;
+        ldi(end + lane, end_n, t0, v0);
+        ldi(end + 32 + lane, end_n, t1, v1);
+        __syncwarp();
+        win[lane] = beg + lane < end ? make_int2(s0, __float_as_int(w0)) : make_int2(C.zero_row, 0);
+        win[lane + 32] = beg + lane + 32 < end ? make_int2(s1, __float_as_int(w1)) : make_int2(C.zero_row, 0);
+        __syncwarp();
+        const int n = end - beg;
+        float4 acc = make_float4(0, 0, 0, 0);
+        for (int bo = 0; bo < n; bo += U * P) {        // batches of U slots (rows longer than U*P loop)
+            const int nb = min(U * P, n - bo);
+            const int nq = (nb + QS * P - 1) / (QS * P);
+            const int2* wb = win + bo;
+            if (nq <= 1) row_slots<CB, QS, POL>(C, wb, g, q, acc, pg);
+            else if (nq == 2) { if constexpr (U >= 2 * QS) row_slots<CB, 2 * QS, POL>(C, wb, g, q, acc, pg); }
+            else if (nq == 3) { if constexpr (U >= 3 * QS) row_slots<CB, 3 * QS, POL>(C, wb, g, q, acc, pg); }
+            else { if constexpr (U >= 4 * QS) row_slots<CB, 4 * QS, POL>(C, wb, g, q, acc, pg); }
+        }
+        acc = allred<G>(acc);
+        if (g == 0) *reinterpret_cast<float4*>(C.z + r * CB + q * 4) = acc;
+        beg = end;
+        end = end_n;
+        end_n = end_nn;
+        s0 = t0; s1 = t1; w0 = v0; w1 = v1;
+    }
+}
+
+// ---- row2: one warp per row, (src, w) broadcast by shuffles from the prefetched registers
+template <int CB, int NS, int MODE>
+__device__ __forceinline__ void row2_slots(const Csr& C, int s0, int s1, float w0, float w1, int bo, int g, int q,
+                                           float4& acc) {
+    constexpr int P = 32 / (CB / 4);
+    float4 x[NS];
+    float wv[NS];
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+        const int e = bo + u * P + g;            // window entry (0..63): register e / 32 of lane e % 32
+        const int sa = __shfl_sync(FULL, s0, e & 31), sb = __shfl_sync(FULL, s1, e & 31);
+        const float wa = __shfl_sync(FULL, w0, e & 31), wb = __shfl_sync(FULL, w1, e & 31);
+        const int ss = e < 32 ? sa : sb;
+        wv[u] = e < 32 ? wa : wb;
+        x[u] = ldmode<MODE>(C.a + (long)ss * CB + q * 4);
+    }
+#pragma unroll
+    for (int u = 0; u < NS; ++u) fma4(acc, wv[u], x[u]);
+}
+
+template <int CB, int U, int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_row2(Csr C) {
+    constexpr int G = CB / 4, P = 32 / G, QS = U < 4 ? U : 4;
+    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
+    const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * (long)blockDim.x) >> 5;
+    const long r_lo = warp * C.n_out / nw, r_hi = (warp + 1) * C.n_out / nw;
+    if (r_lo >= r_hi) return;
+    auto ldi = [&](int k, int end, int& s, float& w) {
+        s = k < end ? __ldg(C.src + k) : C.zero_row;
+        w = k < end ? __ldg(C.w + k) : 0.f;
+    };
+    int beg = C.rp[r_lo], end = C.rp[r_lo + 1];
+    int end_n = r_lo + 1 < r_hi ? C.rp[r_lo + 2] : end;
+    int s0, s1;
+    float w0, w1;
+    ldi(beg + lane, end, s0, w0);
+    ldi(beg + 32 + lane, end, s1, w1);
+    for (long r = r_lo; r < r_hi; ++r) {
+        const int end_nn = r + 2 < r_hi ? C.rp[r + 3] : end_n;
+        int t0, t1;
+        float v0, v1;
+        ldi(end + lane, end_n, t0, v0);
+        ldi(end + 32 + lane, end_n, t1, v1);
+        const int n = end - beg;
+        float4 acc = make_float4(0, 0, 0, 0);
+#pragma unroll
+        for (int bo = 0; bo < MAXROW; bo += U * P) {
+            if (bo < n) {
+                const int nb = min(U * P, n - bo);
+                const int nq = (nb + QS * P - 1) / (QS * P);
+                if (nq <= 1) row2_slots<CB, QS, MODE>(C, s0, s1, w0, w1, bo, g, q, acc);
+                else if (nq == 2) { if constexpr (U >= 2 * QS) row2_slots<CB, 2 * QS, MODE>(C, s0, s1, w0, w1, bo, g, q, acc); }
+                else if (nq == 3) { if constexpr (U >= 3 * QS) row2_slots<CB, 3 * QS, MODE>(C, s0, s1, w0, w1, bo, g, q, acc); }
+                else { if constexpr (U >= 4 * QS) row2_slots<CB, 4 * QS, MODE>(C, s0, s1, w0, w1, bo, g, q, acc); }
+            }
+        }
+        acc = allred<G>(acc);
+        if (g == 0) *reinterpret_cast<float4*>(C.z + r * CB + q * 4) = acc;
+        beg = end;
+        end = end_n;
+        end_n = end_nn;
+        s0 = t0; s1 = t1; w0 = v0; w1 = v1;
+    }
+}
+
+// ---- stream: the warp's contiguous entry range in batches of 32 entries (8 gather slots, entry
+// 4u + g of the batch in slot u), independent of row boundaries; a group accumulates its entries
+// into the running row sum and the warp flushes a row (group all-reduce + store) when the entry
+// stream crosses its end (warp-uniform test per slot; ~1 flush per 10 slots)
+template <int CB, int MINB, bool PF, bool RW, int ST = 0>
+__global__ void __launch_bounds__(256, MINB) k_stream(Csr C) {
+    constexpr int G = CB / 4, P = 32 / G, NS = 32 / P;
+    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
+    const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * (long)blockDim.x) >> 5;
+    const long r_lo = warp * C.n_out / nw, r_hi = (warp + 1) * C.n_out / nw;
+    if (r_lo >= r_hi) return;
+    const int E0 = C.rp[r_lo], E1 = C.rp[r_hi];
+    // row ends of the next 32 rows, one per lane
+    long rw = r_lo;                                   // first row of the window
+    int rend = r_lo + lane < r_hi ? C.rp[r_lo + lane + 1] : E1;
+    int wi = 0;                                       // current row = rw + wi
+    int cur_end = __shfl_sync(FULL, rend, 0);
+    float4 acc = make_float4(0, 0, 0, 0);
+    auto flush = [&]() {
+        const float4 t = allred<G>(acc);
+        float* zp = C.z + (rw + wi) * CB + q * 4;
+        if (ST == 0) {
+            if (g == 0) *reinterpret_cast<float4*>(zp) = t;
+        } else if (ST == 1) {
+            if (g == 0) asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(zp), "f"(t.x), "f"(t.y), "f"(t.z), "f"(t.w) : "memory");
+        } else {
+            if (g == 0 && t.x == 1234.5f) *zp = t.y;   // effectively no store
+        }
+        acc = make_float4(0, 0, 0, 0);
+        ++wi;
+        if (wi == 32) {
+            rw += 32;
+            wi = 0;
+            rend = rw + lane < r_hi ? C.rp[rw + lane + 1] : E1;
+        }
+        cur_end = (rw + wi < r_hi) ? __shfl_sync(FULL, rend, wi) : 0x7fffffff;
+    };
+    int s0 = E0 + lane < E1 ? __ldg(C.src + E0 + lane) : C.zero_row;
+    float w0 = E0 + lane < E1 ? __ldg(C.w + E0 + lane) : 0.f;
+    for (int base = E0; base < E1; base += 32) {
+        const int kn = base + 32 + lane;
+        int s1 = 0;
+        float w1 = 0.f;
+        if (PF) {
+            s1 = kn < E1 ? __ldg(C.src + kn) : C.zero_row;
+            w1 = kn < E1 ? __ldg(C.w + kn) : 0.f;
+        } else if (base != E0) {
+            s0 = base + lane < E1 ? __ldg(C.src + base + lane) : C.zero_row;
+            w0 = base + lane < E1 ? __ldg(C.w + base + lane) : 0.f;
+        }
+        float4 x[NS];
+        float wv[NS];
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {
+            const int ss = __shfl_sync(FULL, s0, u * P + g);
+            if (!RW) wv[u] = __shfl_sync(FULL, w0, u * P + g);
+            x[u] = ldg4(C.a + (long)ss * CB + q * 4);
+        }
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {
+            if (RW) wv[u] = __shfl_sync(FULL, w0, u * P + g);
+            const int e = base + u * P + g;          // this group's entry
+            if (cur_end < base + u * P + P) {        // warp-uniform: a row ends inside this slot
+                while (cur_end <= base + u * P + P - 1 && cur_end < 0x7fffffff) {
+                    // entries of this slot before cur_end belong to the finishing row
+                    const float wo = e < cur_end ? wv[u] : 0.f;
+                    fma4(acc, wo, x[u]);
+                    wv[u] -= wo;
+                    flush();
+                }
+            }
+            fma4(acc, wv[u], x[u]);
+        }
+        if (PF) {
+            s0 = s1;
+            w0 = w1;
+        }
+    }
+    while (rw + wi < r_hi) flush();   // trailing rows (incl. empty ones)
+}
+
+// ---- tma: per-warp ring of NST stages; lanes issue TMA gather4 for the row NST-1 ahead
+__device__ __forceinline__ void mbar_init(uint32_t a, int cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int c0, int r0, int r1, int r2, int r3,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst), "l"(map), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+        "r"(bar)
+        : "memory");
+}
+
+template <int CB, int NST, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_tma(Csr C, const __grid_constant__ CUtensorMap map) {
+    constexpr int G = CB / 4, P = 32 / G;
+    constexpr int STB = MAXROW * CB * 4;     // stage bytes
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, g = lane / G, q = lane % G;
+    float* sbuf = reinterpret_cast<float*>(smem + (size_t)wib * NST * STB);                 // [NST][MAXROW][CB]
+    float* swt = reinterpret_cast<float*>(smem + (size_t)WPB * NST * STB) + wib * NST * MAXROW;   // [NST][MAXROW]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)WPB * NST * (STB + MAXROW * 4)) + wib * NST;
+    const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(sbuf);
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
+    const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * (long)blockDim.x) >> 5;
+    const long r_lo = warp * C.n_out / nw, r_hi = (warp + 1) * C.n_out / nw;
+    if (lane < NST) mbar_init(bar0 + 8 * lane, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    if (r_lo >= r_hi) return;
+    // issue the gathers of row r into stage st
+    auto issue = [&](long r, int st) {
+        const int beg = C.rp[r], end = C.rp[r + 1];
+        const int n = end - beg;
+        const int s0 = lane < n ? __ldg(C.src + beg + lane) : C.zero_row;
+        const int s1 = lane + 32 < n ? __ldg(C.src + beg + 32 + lane) : C.zero_row;
+        const float w0 = lane < n ? __ldg(C.w + beg + lane) : 0.f;
+        const float w1 = lane + 32 < n ? __ldg(C.w + beg + 32 + lane) : 0.f;
+        swt[st * MAXROW + lane] = w0;
+        swt[st * MAXROW + 32 + lane] = w1;
+        const int n4 = ((n + P - 1) / P) * P / 4;   // whole slots: entries past n gather the zero row
+        if (lane == 0) mbar_expect(bar0 + 8 * st, (uint32_t)(max(n4, 1) * 4 * CB * 4));
+        __syncwarp();
+        // lane t (< n4) gathers entries 4t..4t+3
+        int e[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int ent = 4 * lane + c;   // entry index (0..127); entries >= 32 live in s1
+            const int v0 = __shfl_sync(FULL, s0, ent & 31);
+            const int v1 = __shfl_sync(FULL, s1, ent & 31);
+            e[c] = ent < 32 ? v0 : v1;
+        }
+        if (lane < max(n4, 1))
+            tma_gather4(sb0 + st * STB + lane * 4 * CB * 4, &map, 0, e[0], e[1], e[2], e[3], bar0 + 8 * st);
+    };
+    uint32_t phase = 0;   // bit st = parity of stage st
+#pragma unroll 1
+    for (int t = 0; t < NST - 1; ++t)
+        if (r_lo + t < r_hi) issue(r_lo + t, t);
+    int st = 0;
+    for (long r = r_lo; r < r_hi; ++r) {
+        const long ra = r + NST - 1;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // our reads of that stage -> TMA writes
+        if (ra < r_hi) issue(ra, (st + NST - 1) % NST);
+        const int n = C.rp[r + 1] - C.rp[r];
+        mbar_wait(bar0 + 8 * st, (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const float* buf = sbuf + st * MAXROW * CB;
+        const float* wt = swt + st * MAXROW;
+        float4 acc = make_float4(0, 0, 0, 0);
+        for (int u = 0; u * P < n; ++u) {
+            const int ent = u * P + g;
+            const float4 x = *reinterpret_cast<const float4*>(buf + ent * CB + q * 4);
+            fma4(acc, wt[ent], x);
+        }
+        acc = allred<G>(acc);
+        if (g == 0) *reinterpret_cast<float4*>(C.z + r * CB + q * 4) = acc;
+        __syncwarp();
+        st = (st + 1) % NST;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+template <typename F>
+float timeit(F f, int reps = 5) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    f();
+    CK(cudaDeviceSynchronize());
+    float best = 1e30f;
+    for (int i = 0; i < reps; ++i) {
+        cudaEventRecord(a);
+        f();
+        cudaEventRecord(b);
+        CK(cudaEventSynchronize(b));
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        best = std::min(best, ms);
+    }
+    CK(cudaGetLastError());
+    return best;
+}
+
+template <int CB>
+void run_cb(int n, double mean, int sms) {
+    // CSR with Poisson(mean) rows clipped to MAXROW, uniform random sources
+    std::mt19937_64 rng(1234 + CB);
+    std::poisson_distribution<int> pois(mean);
+    std::vector<int> rp(n + 1, 0);
+    for (int j = 0; j < n; ++j) rp[j + 1] = rp[j] + std::min(MAXROW, pois(rng));
+    const long nnz = rp[n];
+    std::vector<int> src(nnz);
+    std::vector<float> w(nnz);
+    std::uniform_int_distribution<int> ui(0, n - 1);
+    for (long k = 0; k < nnz; ++k) {
+        src[k] = ui(rng);
+        w[k] = (float)((k % 7) - 3) * 0.01f;
+    }
+    for (int j = 0; j < n; ++j) std::sort(src.begin() + rp[j], src.begin() + rp[j + 1]);
+    int *d_rp, *d_src;
+    float *d_w, *d_a, *d_z, *d_ref;
+    CK(cudaMalloc(&d_rp, (n + 1) * 4));
+    CK(cudaMalloc(&d_src, nnz * 4));
+    CK(cudaMalloc(&d_w, nnz * 4));
+    CK(cudaMalloc(&d_a, ((size_t)n + 1) * CB * 4));
+    CK(cudaMalloc(&d_z, (size_t)n * CB * 4));
+    CK(cudaMalloc(&d_ref, (size_t)n * CB * 4));
+    CK(cudaMemcpy(d_rp, rp.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_src, src.data(), nnz * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_w, w.data(), nnz * 4, cudaMemcpyHostToDevice));
+    {
+        std::vector<float> a(((size_t)n + 1) * CB, 0.f);
+        for (size_t i = 0; i < (size_t)n * CB; ++i) a[i] = (float)((i * 2654435761u) % 1000) * 1e-3f - 0.5f;
+        CK(cudaMemcpy(d_a, a.data(), a.size() * 4, cudaMemcpyHostToDevice));
+    }
+    Csr C{d_rp, d_src, d_w, d_a, d_z, n, n};
+    const double gb = (double)nnz * CB * 4 / 1e9;
+    auto report = [&](const char* name, float ms, bool check) {
+        double err = 0;
+        if (check) {
+            std::vector<float> z((size_t)n * CB), r((size_t)n * CB);
+            CK(cudaMemcpy(z.data(), d_z, z.size() * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(r.data(), d_ref, r.size() * 4, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < z.size(); i += 97) err = std::max(err, (double)fabsf(z[i] - r[i]));
+        }
+        printf("CB=%d %-26s %8.1f us  %6.2f TB/s gather  maxerr %.2e\n", CB, name, ms * 1e3, gb / ms, err);
+        fflush(stdout);
+    };
+    if (getenv("ONLY_ROW")) {   // one launch of row U8 minb4 (for ncu)
+        int nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row<CB, 8, false, 4>, 256, 0);
+        k_row<CB, 8, false, 4><<<sms * nb, 256>>>(C);
+        CK(cudaDeviceSynchronize());
+        return;
+    }
+    // reference = group kernel
+    float ms = timeit([&] { k_group<CB><<<sms * 8, 256>>>(C); });
+    CK(cudaMemcpy(d_ref, d_z, (size_t)n * CB * 4, cudaMemcpyDeviceToDevice));
+    report("group (v2)", ms, false);
+    ms = timeit([&] { k_bench<CB, 0><<<sms * 4, 256>>>(C, nnz); });
+    report("bench ldg", ms, false);
+    ms = timeit([&] { k_bench<CB, 1><<<sms * 4, 256>>>(C, nnz); });
+    report("bench nc.L1::no_allocate", ms, false);
+    ms = timeit([&] { k_bench<CB, 2><<<sms * 4, 256>>>(C, nnz); });
+    report("bench ld.cg", ms, false);
+    ms = timeit([&] { k_bench<CB, 3><<<sms * 4, 256>>>(C, nnz); });
+    report("bench nc.L2::128B", ms, false);
+    ms = timeit([&] { k_bench<CB, 0><<<sms * 8, 256>>>(C, nnz); });
+    report("bench ldg 8 blk/SM", ms, false);
+#define STREAM(MINB, PF, RW, ST)                                                                   \
+    {                                                                                              \
+        int nb = 0;                                                                                \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_stream<CB, MINB, PF, RW, ST>, 256, 0); \
+        ms = timeit([&] { k_stream<CB, MINB, PF, RW, ST><<<sms * nb, 256>>>(C); });                \
+        char nm[64];                                                                               \
+        snprintf(nm, 64, "stream minb%d pf%d rw%d st%d x%d", MINB, (int)PF, (int)RW, ST, nb);      \
+        report(nm, ms, ST != 2);                                                                   \
+    }
+    STREAM(3, true, false, 0);
+    STREAM(3, true, false, 1);
+    STREAM(3, true, false, 2);
+    STREAM(2, true, false, 0);
+    STREAM(2, true, false, 2);
+    STREAM(4, true, true, 0);
+    STREAM(4, true, true, 2);
+#define ROW2(U, MODE, MINB, NAME)                                                                  \
+    {                                                                                              \
+        int nb = 0;                                                                                \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row2<CB, U, MODE, MINB>, 256, 0);      \
+        ms = timeit([&] { k_row2<CB, U, MODE, MINB><<<sms * nb, 256>>>(C); });                     \
+        char nm[64];                                                                               \
+        snprintf(nm, 64, "%s x%d", NAME, nb);                                                      \
+        report(nm, ms, true);                                                                      \
+    }
+    ROW2(8, 0, 4, "row2 U8 ldg");
+    ROW2(8, 1, 4, "row2 U8 noalloc");
+    ROW2(8, 2, 4, "row2 U8 cg");
+    ROW2(4, 0, 6, "row2 U4 ldg");
+    ROW2(16, 0, 2, "row2 U16 ldg");
+#define ROW(U, POL, MINB, NAME)                                                                    \
+    {                                                                                              \
+        int nb = 0;                                                                                \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_row<CB, U, POL, MINB>, 256, 0);        \
+        ms = timeit([&] { k_row<CB, U, POL, MINB><<<sms * nb, 256>>>(C); });                       \
+        char nm[64];                                                                               \
+        snprintf(nm, 64, "%s x%d", NAME, nb);                                                      \
+        report(nm, ms, true);                                                                      \
+    }
+    CK(cudaFuncSetAttribute(k_row<CB, 8, false, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    ROW(8, false, 4, "row U8 minb4 carve0");
+    CK(cudaFuncSetAttribute(k_row<CB, 8, false, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    ROW(8, false, 4, "row U8 minb4 carve100");
+    CK(cudaFuncSetAttribute(k_row<CB, 8, false, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, -1));
+    ROW(4, false, 6, "row U4 minb6");
+    ROW(4, false, 8, "row U4 minb8");
+    ROW(8, false, 4, "row U8 minb4");
+    ROW(8, false, 5, "row U8 minb5");
+    ROW(8, false, 3, "row U8 minb3");
+    ROW(12, false, 3, "row U12 minb3");
+    ROW(16, false, 2, "row U16 minb2");
+    ROW(8, true, 4, "rowpol U8 minb4");
+    // TMA gather4
+    static EncodeFn enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult qr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &qr));
+    }
+    CUtensorMap map;
+    cuuint64_t dims[2] = {(cuuint64_t)CB, (cuuint64_t)n + 1};
+    cuuint64_t strides[1] = {(cuuint64_t)CB * 4};
+    cuuint32_t box[2] = {(cuuint32_t)CB, 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d_a, dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) {
+        printf("tensor map encode failed %d\n", (int)cr);
+        return;
+    }
+#define TMA(NST, WPB)                                                                               \
+    {                                                                                               \
+        const size_t sm = (size_t)WPB * NST * (MAXROW * CB * 4 + MAXROW * 4 + 16);                  \
+        CK(cudaFuncSetAttribute(k_tma<CB, NST, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+        int nb = 0;                                                                                 \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tma<CB, NST, WPB>, WPB * 32, sm);      \
+        ms = timeit([&] { k_tma<CB, NST, WPB><<<sms * std::max(nb, 1), WPB * 32, sm>>>(C, map); });  \
+        char nm[64];                                                                                \
+        snprintf(nm, 64, "tma nst%d wpb%d x%d", NST, WPB, nb);                                      \
+        report(nm, ms, true);                                                                       \
+    }
+    TMA(2, 12);
+    cudaFree(d_rp); cudaFree(d_src); cudaFree(d_w); cudaFree(d_a); cudaFree(d_z); cudaFree(d_ref);
+}
+
+int main(int argc, char** argv) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int n = argc > 1 ? atoi(argv[1]) : 500000;
+    const double mean = argc > 2 ? atof(argv[2]) : 40.0;
+    printf("# SMs %d, n %d, mean row %.1f\n", sms, n, mean);
+    run_cb<32>(n, mean, sms);
+    if (getenv("ONLY_ROW")) return 0;
+    run_cb<16>(n, mean, sms);
+    return 0;
+}
