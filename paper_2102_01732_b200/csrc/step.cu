@@ -922,7 +922,7 @@ __device__ __forceinline__ void bwd_batch(const float* __restrict__ d_out, const
 // GOLD: add the gradient accumulated by earlier chunks; UPD: last chunk of the fused path (Eq. 1
 // on (w, v) in place); DROP: dropout on layer l-1
 template <int CB, bool HAS_DPREV, bool GOLD, bool UPD, bool DROP>
-__global__ void __launch_bounds__(256, 3) bwd_rows_kernel(BwdArgs A) {
+__global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     using C = RowCfg<CB>;
     constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB, S = C::S;
     __shared__ int2 win_all[WARPS_PER_BLOCK][2][SEG_NNZ];
@@ -1474,11 +1474,16 @@ struct BitsArgs {
 // then reads, per entry, the one pair holding its 4 columns' bits (broadcast, conflict-free).
 constexpr int BITS_ROWS = 32;
 
-template <int CB>
+template <int CB, bool DROP>
 __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
     constexpr int G = CB / 4;                       // lanes per chunk
     __shared__ float2 rec[WARPS_PER_BLOCK][32][XBITS_WORDS];
+    __shared__ float4 lut[16];                      // nibble -> its 4 bits as floats {0, 1}
     if (*A.nonbinary) return;
+    if (threadIdx.x < 16)
+        lut[threadIdx.x] = make_float4((float)(threadIdx.x & 1), (float)((threadIdx.x >> 1) & 1),
+                                       (float)((threadIdx.x >> 2) & 1), (float)((threadIdx.x >> 3) & 1));
+    __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane / G, q = lane % G;            // chunk g, chunk-local lane q
     const bool colok = g < A.nchunks;
@@ -1488,17 +1493,19 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nunits = (A.n_out + BITS_ROWS - 1) / BITS_ROWS;
     const uint4* xb4 = reinterpret_cast<const uint4*>(A.xbits);
+    const float2* myrec = &rec[wib][0][wsel];
     for (int64_t u0 = warp; u0 < nunits; u0 += nwarps) {
         const int64_t j0 = u0 * BITS_ROWS;
         const int nrows = (int)(A.n_out - j0 < BITS_ROWS ? A.n_out - j0 : BITS_ROWS);
         const int rp_l = __ldg(A.mrow_ptr + j0 + min(lane, nrows));       // lane t: start of local row t
+        const float b_l = lane < nrows ? __ldg(A.bias + j0 + lane) : 0.f;  // lane t: bias of local row t
         const int E0 = __shfl_sync(FULL, rp_l, 0), E1 = __ldg(A.mrow_ptr + j0 + nrows);
         int row = 0;
         int row_end = nrows > 1 ? __shfl_sync(FULL, rp_l, 1) : E1;
         float4 acc = f4zero();
         auto finish_row = [&]() {
             const int64_t j = j0 + row;
-            const float bj = __ldg(A.bias + j);
+            const float bj = __shfl_sync(FULL, b_l, row);
             const float4 z = make_float4(acc.x + bj, acc.y + bj, acc.z + bj, acc.w + bj);
             uint32_t zb[4], kb[4];
             float out[4];
@@ -1509,21 +1516,21 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
                 zb[c] = group_bits<G>(__ballot_sync(FULL, colok && pos), g);
                 float a = pos ? zc : A.neg_slope * zc;
                 bool keep = true;
-                if (A.dropout_on) {
+                if (DROP) {
                     const uint64_t b = (uint64_t)(lane * 4 + c);
                     const uint64_t e = b * (uint64_t)A.n_out + (uint64_t)j;
                     const uint4 r = rng_stream(A.seed, P_DROPOUT, A.rank, 2, step_lo, e >> 2);
                     keep = word(r, (int)(e & 3)) >= A.drop_thr;
                     a = keep ? a * A.keep_scale : 0.f;
+                    kb[c] = group_bits<G>(__ballot_sync(FULL, colok && keep), g);
                 }
-                kb[c] = group_bits<G>(__ballot_sync(FULL, colok && keep), g);
                 out[c] = a;
             }
             if (colok) {
                 st4(A.a_out + ((int64_t)g * A.n_out + j) * CB + q * 4, make_float4(out[0], out[1], out[2], out[3]));
                 if (q == 0) {
                     A.zmask[(int64_t)g * A.n_out + j] = make_uint4(zb[0], zb[1], zb[2], zb[3]);
-                    if (A.dropout_on) A.kmask[(int64_t)g * A.n_out + j] = make_uint4(kb[0], kb[1], kb[2], kb[3]);
+                    if (DROP) A.kmask[(int64_t)g * A.n_out + j] = make_uint4(kb[0], kb[1], kb[2], kb[3]);
                 }
             }
             acc = f4zero();
@@ -1531,44 +1538,48 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
             row_end = __shfl_sync(FULL, rp_l, min(row + 1, 31));
             if (row + 1 > 31) row_end = E1;
         };
-        int k = E0 + lane;
-        int src = 0;
-        float w = 0.f;
-        if (k < E1) {
-            src = __ldg(A.msrc + k);
-            w = __ldg(A.mval + k);
-        }
+        // pipeline: (src, w) two blocks ahead, the 16-B bit row of each entry one block ahead
+        auto ld_entry = [&](int k, int& sr, float& wv) {
+            sr = k < E1 ? __ldg(A.msrc + k) : 0;
+            wv = k < E1 ? __ldg(A.mval + k) : 0.f;
+        };
+        int src, src_n;
+        float w, w_n;
+        ld_entry(E0 + lane, src, w);
+        ld_entry(E0 + 32 + lane, src_n, w_n);
+        uint4 xb = E0 + lane < E1 ? __ldg(xb4 + src) : make_uint4(0, 0, 0, 0);
         for (int blk = E0; blk < E1; blk += 32) {
-            const int kn = k + 32;                          // prefetch the next block's entries
-            int src_n = 0;
-            float w_n = 0.f;
-            if (kn < E1) {
-                src_n = __ldg(A.msrc + kn);
-                w_n = __ldg(A.mval + kn);
-            }
-            if (k < E1) {
-                const uint4 xb = __ldg(xb4 + src);
-                rec[wib][lane][0] = make_float2(w, __uint_as_float(xb.x));
-                rec[wib][lane][1] = make_float2(w, __uint_as_float(xb.y));
-                rec[wib][lane][2] = make_float2(w, __uint_as_float(xb.z));
-                rec[wib][lane][3] = make_float2(w, __uint_as_float(xb.w));
-            }
+            int src_nn;
+            float w_nn;
+            ld_entry(blk + 64 + lane, src_nn, w_nn);
+            const uint4 xb_n = blk + 32 + lane < E1 ? __ldg(xb4 + src_n) : make_uint4(0, 0, 0, 0);
+            rec[wib][lane][0] = make_float2(w, __uint_as_float(xb.x));
+            rec[wib][lane][1] = make_float2(w, __uint_as_float(xb.y));
+            rec[wib][lane][2] = make_float2(w, __uint_as_float(xb.z));
+            rec[wib][lane][3] = make_float2(w, __uint_as_float(xb.w));
             __syncwarp();
             const int n = min(32, E1 - blk);
-            for (int u = 0; u < n; ++u) {
-                while (blk + u == row_end) finish_row();   // warp-uniform; handles empty rows
-                const float2 r = rec[wib][u][wsel];
-                const uint32_t bits = __float_as_uint(r.y) >> sh;
-                // x in {0, 1}: fmaf(w, x, acc) == (x ? acc + w : acc) bit for bit
-                if (bits & 1u) acc.x += r.x;
-                if (bits & 2u) acc.y += r.x;
-                if (bits & 4u) acc.z += r.x;
-                if (bits & 8u) acc.w += r.x;
+            // the block's entries row by row: a tight loop up to the next row end, then the row's
+            // epilogue (warp-uniform; empty rows finish at once)
+            int u = 0;
+            for (;;) {
+                while (blk + u == row_end && row < nrows) finish_row();
+                if (u >= n) break;
+                const int stop = min(n, row_end - blk);
+                for (; u < stop; ++u) {
+                    const float2 r = myrec[u * XBITS_WORDS];
+                    // x in {0, 1}: fmaf(w, x, acc) is acc + w for x = 1 and acc for x = 0, bit for bit
+                    const float4 m = lut[(__float_as_uint(r.y) >> sh) & 15u];
+                    const float2 lo = ffma2(make_float2(r.x, r.x), make_float2(m.x, m.y), make_float2(acc.x, acc.y));
+                    const float2 hi = ffma2(make_float2(r.x, r.x), make_float2(m.z, m.w), make_float2(acc.z, acc.w));
+                    acc = make_float4(lo.x, lo.y, hi.x, hi.y);
+                }
             }
             __syncwarp();
-            k = kn;
-            src = src_n;
             w = w_n;
+            src_n = src_nn;
+            w_n = w_nn;
+            xb = xb_n;
         }
         while (row < nrows) finish_row();
     }
@@ -1647,6 +1658,72 @@ __global__ void __launch_bounds__(256) bwd_bits_kernel(BitsArgs A) {
             k = kn;
             src = src_n;
         }
+    }
+}
+
+// Backward of the binary-input layer, one lane per mirror entry (i -> j): since x[b, i] is 0 or 1,
+// g_ij = sum_b x[b, i] delta_2[b, j] is the sum of delta_2[b, j] over the SET bits b of input
+// neuron i (5% of the batch at C5), added in ascending b (a fixed order).  The warp stages the
+// row's delta_2[:, j] (<= 128 values, 4 chunks of CB) in shared memory once per output row j, and
+// each lane walks its entry's 128-bit input row with ffs.  ~6 dependent adds per entry instead
+// of 128 bit tests.  Rows are contiguous per warp; the next row's delta and entries are
+// prefetched.  Output: the gradient in mirror order (gmirror), moved to the canonical order by
+// grad_from_mirror_kernel.
+template <int CB>
+__global__ void __launch_bounds__(256) bwd_bits_rows_kernel(BitsArgs A) {
+    __shared__ __align__(16) float dsm_all[WARPS_PER_BLOCK][2][32 * XBITS_WORDS];
+    if (*A.nonbinary) return;
+    const int lane = threadIdx.x & 31;
+    float (*dsm)[32 * XBITS_WORDS] = dsm_all[threadIdx.x >> 5];
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t r_lo = warp * A.n_out / nwarps, r_hi = (warp + 1) * A.n_out / nwarps;
+    if (r_lo >= r_hi) return;
+    const uint4* xb4 = reinterpret_cast<const uint4*>(A.xbits);
+    // lane t stages columns 4t..4t+3 (chunk 4t / CB); columns past the batch are 0
+    const int col = 4 * lane, chunk = col / CB;
+    const bool colok = chunk < A.nchunks;
+    auto dload = [&](int64_t j) -> float4 {
+        return (colok && j < r_hi) ? ldg4(A.d_out + ((int64_t)chunk * A.n_out + j) * CB + (col % CB)) : f4zero();
+    };
+    int beg = A.mrow_ptr[r_lo];
+    int end = A.mrow_ptr[r_lo + 1];
+    int end_n = r_lo + 1 < r_hi ? A.mrow_ptr[r_lo + 2] : end;
+    float4 d = dload(r_lo);
+    int src = beg + lane < end ? __ldg(A.msrc + beg + lane) : 0;
+    uint4 xb = beg + lane < end ? __ldg(xb4 + src) : make_uint4(0, 0, 0, 0);
+    int buf = 0;
+    for (int64_t j = r_lo; j < r_hi; ++j) {
+        // prefetch the next row: delta column, first 32 entries and their bit rows
+        const int end_nn = j + 2 < r_hi ? A.mrow_ptr[j + 3] : end_n;
+        const float4 d_n = dload(j + 1);
+        const int src_n = end + lane < end_n ? __ldg(A.msrc + end + lane) : 0;
+        *reinterpret_cast<float4*>(&dsm[buf][col]) = d;
+        __syncwarp();
+        for (int base = beg; base < end; base += 32) {
+            if (base != beg) {                                      // rows longer than 32
+                src = base + lane < end ? __ldg(A.msrc + base + lane) : 0;
+                xb = base + lane < end ? __ldg(xb4 + src) : make_uint4(0, 0, 0, 0);
+            }
+            float acc = 0.f;
+#pragma unroll
+            for (int c = 0; c < XBITS_WORDS; ++c) {
+                uint32_t m = c == 0 ? xb.x : (c == 1 ? xb.y : (c == 2 ? xb.z : xb.w));
+                while (m) {
+                    acc += dsm[buf][c * 32 + __ffs(m) - 1];
+                    m &= m - 1u;
+                }
+            }
+            if (base + lane < end) A.gmirror[base + lane] = acc;
+        }
+        const uint4 xb_n = end + lane < end_n ? __ldg(xb4 + src_n) : make_uint4(0, 0, 0, 0);
+        beg = end;
+        end = end_n;
+        end_n = end_nn;
+        d = d_n;
+        src = src_n;
+        xb = xb_n;
+        buf ^= 1;
     }
 }
 
@@ -1895,8 +1972,20 @@ int launch_bits(smlp_handle* h, const BitsArgs& A, const Layer& L2, bool fwd) {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK,
                                                                   (int64_t)h->num_sms * 6));
     if (fwd) {
-        fwd_bits_kernel<CB><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        // units are grid-strided: one resident wave (blocks/SM from the occupancy calculator)
+        if (A.dropout_on)
+            fwd_bits_kernel<CB, true><<<rows_grid(h, fwd_bits_kernel<CB, true>, units), WARPS_PER_BLOCK * 32, 0,
+                                        h->stream>>>(A);
+        else
+            fwd_bits_kernel<CB, false><<<rows_grid(h, fwd_bits_kernel<CB, false>, units), WARPS_PER_BLOCK * 32, 0,
+                                         h->stream>>>(A);
         SMLP_CK_LAUNCH(h, "fwd_bits_kernel");
+    } else if (h->kver >= 3) {
+        const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((L2.n_out + 8 * WARPS_PER_BLOCK - 1) /
+                                                                     (8 * WARPS_PER_BLOCK),
+                                                                 (int64_t)h->num_sms * 8));
+        bwd_bits_rows_kernel<CB><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        SMLP_CK_LAUNCH(h, "bwd_bits_rows_kernel");
     } else {
         bwd_bits_kernel<CB><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
         SMLP_CK_LAUNCH(h, "bwd_bits_kernel");

@@ -385,6 +385,62 @@ __global__ void __launch_bounds__(256, MINB) k_stream(Csr C) {
     while (rw + wi < r_hi) flush();   // trailing rows (incl. empty ones)
 }
 
+// ---- cpa: one warp per row; the NEXT row's gathers go global -> shared by cp.async.cg (16 B per
+// lane, no register destination, L1 bypassed) while the current row is computed from shared memory
+template <int CB, int WPB, int NST>
+__global__ void __launch_bounds__(WPB * 32) k_cpa(Csr C) {
+    constexpr int G = CB / 4, P = 32 / G;
+    extern __shared__ __align__(16) float sm_cpa[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, g = lane / G, q = lane % G;
+    float* stg = sm_cpa + (size_t)wib * NST * MAXROW * CB;          // [NST][MAXROW][CB]
+    float* swt = sm_cpa + (size_t)WPB * NST * MAXROW * CB + (size_t)wib * NST * MAXROW;   // [NST][MAXROW]
+    const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * (long)blockDim.x) >> 5;
+    const long r_lo = warp * C.n_out / nw, r_hi = (warp + 1) * C.n_out / nw;
+    if (r_lo >= r_hi) return;
+    auto issue = [&](long r, int st) {        // gathers of row r into stage st (+ its weights)
+        const int beg = C.rp[r], n = C.rp[r + 1] - beg;
+        const int s0 = lane < n ? __ldg(C.src + beg + lane) : 0;
+        const int s1 = lane + 32 < n ? __ldg(C.src + beg + 32 + lane) : 0;
+        swt[st * MAXROW + lane] = lane < n ? __ldg(C.w + beg + lane) : 0.f;
+        swt[st * MAXROW + 32 + lane] = lane + 32 < n ? __ldg(C.w + beg + 32 + lane) : 0.f;
+        const uint32_t base = (uint32_t)__cvta_generic_to_shared(stg + st * MAXROW * CB);
+        for (int u = 0; u * P < n; ++u) {
+            const int e = u * P + g;
+            const int sa = __shfl_sync(FULL, s0, e & 31), sb = __shfl_sync(FULL, s1, e & 31);
+            const int sr = e < 32 ? sa : sb;
+            const bool ok = e < n;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(base + (e * CB + q * 4) * 4),
+                         "l"(C.a + (long)(ok ? sr : 0) * CB + q * 4), "r"(ok ? 16 : 0) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll 1
+    for (int t = 0; t < NST - 1; ++t) {
+        if (r_lo + t < r_hi) issue(r_lo + t, t);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    int st = 0;
+    for (long r = r_lo; r < r_hi; ++r) {
+        const long ra = r + NST - 1;
+        if (ra < r_hi) issue(ra, (st + NST - 1) % NST);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(NST - 1) : "memory");
+        __syncwarp();
+        const int n = C.rp[r + 1] - C.rp[r];
+        const float* buf = stg + st * MAXROW * CB;
+        const float* wt = swt + st * MAXROW;
+        float4 acc = make_float4(0, 0, 0, 0);
+        for (int u = 0; u * P < n; ++u) {
+            const int e = u * P + g;
+            if (e < n) fma4(acc, wt[e], *reinterpret_cast<const float4*>(buf + e * CB + q * 4));
+        }
+        acc = allred<G>(acc);
+        if (g == 0) *reinterpret_cast<float4*>(C.z + r * CB + q * 4) = acc;
+        __syncwarp();
+        st = (st + 1) % NST;
+    }
+}
+
 // ---- tma: per-warp ring of NST stages; lanes issue TMA gather4 for the row NST-1 ahead
 __device__ __forceinline__ void mbar_init(uint32_t a, int cnt) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt));
@@ -620,6 +676,23 @@ void run_cb(int n, double mean, int sms) {
     ROW(12, false, 3, "row U12 minb3");
     ROW(16, false, 2, "row U16 minb2");
     ROW(8, true, 4, "rowpol U8 minb4");
+#define CPA(WPB, NST)                                                                              \
+    {                                                                                              \
+        const size_t sm = (size_t)WPB * NST * (MAXROW * CB * 4 + MAXROW * 4);                      \
+        CK(cudaFuncSetAttribute(k_cpa<CB, WPB, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+        int nb = 0;                                                                                \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cpa<CB, WPB, NST>, WPB * 32, sm);      \
+        ms = timeit([&] { k_cpa<CB, WPB, NST><<<sms * std::max(nb, 1), WPB * 32, sm>>>(C); });      \
+        char nm[64];                                                                               \
+        snprintf(nm, 64, "cpa wpb%d nst%d x%d", WPB, NST, nb);                                     \
+        report(nm, ms, true);                                                                      \
+    }
+    CPA(4, 2);
+    CPA(4, 3);
+    CPA(8, 2);
+    CPA(6, 2);
+    CPA(2, 4);
+    CPA(12, 2);
     // TMA gather4
     static EncodeFn enc = nullptr;
     if (!enc) {
