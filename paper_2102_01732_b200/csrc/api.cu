@@ -302,6 +302,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
     if (const char* e = std::getenv("SMLP_GATHER_EVICT_LAST")) h->gather_evict_last = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_KVER")) h->kver = std::atoi(e);
+    if (const char* e = std::getenv("SMLP_MIRROR_SCATTER")) h->mirror_scatter = std::atoi(e) != 0;
     const int rc = build_handle(h, cfg);
     if (rc != SMLP_OK) {
         g_create_error = h->err;

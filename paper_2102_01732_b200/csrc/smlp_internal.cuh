@@ -156,7 +156,8 @@ struct smlp_handle {
     std::vector<cudaEvent_t> ev_pool;
     int num_sms = 148;
     int kver = 3;                   // tuning knob (env SMLP_KVER): 3 = warp-per-row kernels, 2 = group kernels
-    int gather_evict_last = 0;      // tuning knob (env SMLP_GATHER_EVICT_LAST): L2 policy of row gathers
+    int gather_evict_last = 0;
+    int mirror_scatter = 0;         // tuning knob (env SMLP_MIRROR_SCATTER): fused update scatters into mval      // tuning knob (env SMLP_GATHER_EVICT_LAST): L2 policy of row gathers
     int64_t launches = 0;
     std::string err;
 };

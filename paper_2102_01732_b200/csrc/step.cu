@@ -657,6 +657,7 @@ struct BwdArgs {
     float* grad;
     float* mval;              // mirror-ordered copy of w (refreshed by the fused update)
     const int32_t* minv;      // canonical index -> mirror position
+    int mval_scatter;         // the fused update also scatters w into mval (no separate refresh)
     float* ws;
     float* bgs;               // [n_in] bias-grad accumulator over chunks
     float* bias_prev;
@@ -848,9 +849,38 @@ __device__ __forceinline__ BwdSide bwd_side(const BwdArgs& A, int64_t i, bool va
     return t;
 }
 
+// Sum of a float4 over the P groups of a warp, scattered: lane (g, q) ends with the components
+// c = r P + g (r < NR) it finishes in the epilogue -- 3 shuffles for P = 4 instead of 8 for an
+// all-reduce.  Fixed pairing, so the result is deterministic.
 template <int CB>
-__device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, const float4& d, const BwdSide& sd,
-                                                  int lane) {
+__device__ __forceinline__ void group_reduce_scatter(float4 v, int g, float (&out)[RowCfg<CB>::NR]) {
+    using C = RowCfg<CB>;
+    constexpr int G = C::G, P = C::P;
+    if constexpr (P == 1) {
+        out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+    } else if constexpr (P == 2) {          // g = 0 keeps (x, z), g = 1 keeps (y, w)
+        const bool hi = g & 1;
+        const float k0 = hi ? v.y : v.x, k1 = hi ? v.w : v.z, s0 = hi ? v.x : v.y, s1 = hi ? v.z : v.w;
+        out[0] = k0 + __shfl_xor_sync(FULL, s0, G);
+        out[1] = k1 + __shfl_xor_sync(FULL, s1, G);
+    } else {
+#pragma unroll
+        for (int m = 4 * G; m < 32; m <<= 1) v = f4add(v, shfl_xor4(v, m));   // groups beyond 4
+        const bool b1 = (g & 2) != 0, b0 = (g & 1) != 0;
+        const float ka = b1 ? v.z : v.x, kb = b1 ? v.w : v.y, sa = b1 ? v.x : v.z, sb = b1 ? v.y : v.w;
+        const float pa = ka + __shfl_xor_sync(FULL, sa, 2 * G);   // component (g & 2) + 0
+        const float pb = kb + __shfl_xor_sync(FULL, sb, 2 * G);   // component (g & 2) + 1
+        const float keep = b0 ? pb : pa, send = b0 ? pa : pb;
+        out[0] = keep + __shfl_xor_sync(FULL, send, G);           // component g & 3
+    }
+}
+
+// backward epilogue of one complete input row i: f'_{l-1} from the sign bits, dropout keep bits,
+// store of delta_{l-1}[i], and the bias gradient of layer l-1 (a fixed 32-lane butterfly, then
+// accumulated over chunks in order).  d[r] = component r P + g of the row's sum.
+template <int CB>
+__device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, const float (&d)[RowCfg<CB>::NR],
+                                                  const BwdSide& sd, int lane) {
     using C = RowCfg<CB>;
     constexpr int G = C::G, P = C::P, NR = C::NR;
     const int g = lane / G, q = lane % G;
@@ -862,7 +892,7 @@ __device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, c
         if (c < 4) {
             const bool pos = (word(zb, c) >> q) & 1u;
             const bool keep = (word(kb, c) >> q) & 1u;
-            const float v = comp(d, c) * (pos ? 1.f : A.neg_slope_prev);
+            const float v = d[r] * (pos ? 1.f : A.neg_slope_prev);
             const float o = A.dropout_prev ? (keep ? v * A.keep_scale_prev : 0.f) : v;
             A.d_prev[i * CB + q * 4 + c] = o;
             s += o;
@@ -872,21 +902,19 @@ __device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, c
     for (int m = 1; m < 32; m <<= 1) s += __shfl_xor_sync(FULL, s, m);
     if (lane == 0) {
         float tot = s;
-        if (!A.first) tot += A.bgs[i];
+        if (!A.first) tot += sd.bgs;
         if (!A.last) {
             A.bgs[i] = tot;
         } else if (A.fused) {
-            const float v = A.mu * A.bias_mom_prev[i] - A.lr * tot;
+            const float v = A.mu * sd.bmom - A.lr * tot;
             A.bias_mom_prev[i] = v;
-            A.bias_prev[i] = A.bias_prev[i] + v;
+            A.bias_prev[i] = sd.bval + v;
         } else {
             A.bias_grad_prev[i] = tot;
         }
     }
 }
 
-// NS slots of a backward batch: gathers first, then delta_{l-1} += w delta_l[j] (a4) and the
-// partial SDDMM dot <a_{l-1}[i], delta_l[j]> over the lane's 4 columns into shared memory (a5)
 template <int CB, int NS, bool HAS_DPREV>
 __device__ __forceinline__ void bwd_slots(const float* __restrict__ d_out, const int2* win, float* red,
                                           const float4& ai, int g, int q, float4& dacc) {
@@ -903,7 +931,7 @@ __device__ __forceinline__ void bwd_slots(const float* __restrict__ d_out, const
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
         if (HAS_DPREV) fma4p(dacc, wv[u], dx[u]);
-        red[(u * P + g) * S + q] = dot4p(ai, dx[u]);
+        red[(u * P + g) * S + q] = dot4p(ai, dx[u]);     // entry u P + g of this batch: lane-q partial
     }
 }
 
@@ -924,10 +952,11 @@ __device__ __forceinline__ void bwd_batch(const float* __restrict__ d_out, const
 template <int CB, bool HAS_DPREV, bool GOLD, bool UPD, bool DROP>
 __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     using C = RowCfg<CB>;
-    constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB, S = C::S;
+    constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB, S = C::S, NR = C::NR;
+    constexpr int RB = NB < 2 ? NB : 2;              // batches per reduction round
     __shared__ int2 win_all[WARPS_PER_BLOCK][2][SEG_NNZ];
     __shared__ __align__(16) float4 ai_all[WARPS_PER_BLOCK][2][G];
-    __shared__ __align__(16) float red_all[WARPS_PER_BLOCK][EB * S];
+    __shared__ __align__(16) float red_all[WARPS_PER_BLOCK][RB * EB * S];
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
     const int wib = threadIdx.x >> 5;
@@ -940,7 +969,7 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     const int64_t s_lo = warp * nseg / nwarps, s_hi = (warp + 1) * nseg / nwarps;
     if (s_lo >= s_hi) return;
     const int4 none = make_int4(0, 0, 0, -2);
-    // window + a_{l-1}[i] of a segment into buffer b (cp.async, one segment ahead)
+    // window + a_{l-1}[i] of a segment into buffer b (cp.async, one segment ahead: no registers held)
     auto prefetch = [&](const int4& sg, int b) {
         window_async(win[b], A.col, A.val, sg.y, sg.z, lane);
         if (lane < G) cp_async16(smem_u32(&ais[b][lane]), A.a_prev + (int64_t)(sg.w != -2 ? sg.x : 0) * CB + lane * 4,
@@ -977,17 +1006,19 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
 #pragma unroll
         for (int r = 0; r < NW; ++r) gsum[r] = 0.f;
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-            if (b * EB < n) {
-                const int nb = min(EB, n - b * EB);
-                bwd_batch<CB, HAS_DPREV>(A.d_out, win[buf] + b * EB, red, nb, ai, g, q, dacc);
+        for (int b0 = 0; b0 < NB; b0 += RB) {
+            if (b0 * EB < n) {
+#pragma unroll
+                for (int b = b0; b < b0 + RB; ++b)
+                    if (b * EB < n)
+                        bwd_batch<CB, HAS_DPREV>(A.d_out, win[buf] + b * EB, red + (b - b0) * EB * S, n - b * EB, ai, g, q,
+                                                 dacc);
                 __syncwarp();
-                // window entry e = lane + 32 r is entry e - b EB of this batch: fixed-order sum of its
-                // G lane partials
+                // window entry e = lane + 32 r of this round: fixed-order sum of its G lane partials
 #pragma unroll
                 for (int r = 0; r < NW; ++r) {
-                    const int e = lane + 32 * r - b * EB;
-                    if (e >= 0 && e < nb) {
+                    const int e = lane + 32 * r - b0 * EB;
+                    if (e >= 0 && e < RB * EB && e + b0 * EB < n) {
                         const float* pr = red + e * S;
                         float t;
                         if constexpr (G % 4 == 0) {
@@ -1009,10 +1040,12 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
                 __syncwarp();
             }
         }
+        // gradient accumulation / Eq. 1 on the lane's own entries (coalesced)
 #pragma unroll
         for (int r = 0; r < NW; ++r) {
-            const int k = cur.y + lane + 32 * r;
-            if (lane + 32 * r < n) {
+            const int e = lane + 32 * r;
+            if (e < n) {
+                const int k = cur.y + e;
                 const float gk = gsum[r] + gold[r];
                 if (!UPD) {
                     A.grad[k] = gk;
@@ -1020,15 +1053,18 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
                     const float v = A.mu * mold[r] - A.lr * (gk + A.wd * w[r]);
                     A.mom[k] = v;
                     A.val[k] = w[r] + v;
+                    if (A.mval_scatter) A.mval[__ldg(A.minv + k)] = w[r] + v;   // the forward's mirror copy
                 }
             }
         }
         if (HAS_DPREV) {
-            dacc = group_allreduce<G>(dacc);
             if (cur.w < 0) {
-                bwd_rows_epilogue<CB>(A, cur.x, dacc, sd, lane);
-            } else if (g == 0) {
-                st4(A.ws + (int64_t)cur.w * CB + q * 4, dacc);
+                float d[NR];
+                group_reduce_scatter<CB>(dacc, g, d);
+                bwd_rows_epilogue<CB>(A, cur.x, d, sd, lane);
+            } else {
+                dacc = group_allreduce<G>(dacc);
+                if (g == 0) st4(A.ws + (int64_t)cur.w * CB + q * 4, dacc);
             }
         }
         __syncwarp();
@@ -2201,13 +2237,14 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
             A.gather_evict_last = h->gather_evict_last;
             A.zero_row = (int)((int64_t)(h->max_chunks - c) * nout);
+            A.mval_scatter = (h->mirror_scatter && h->kver >= 3 && !(l == 2 && h->xbits)) ? 1 : 0;
             prof_start(h, K_BWD, l, (is_fused ? 20.0 : 12.0) * nnz / nchunks + act_bytes,
                        (has_dprev ? 4.0 : 2.0) * nnz * Bc);
             SMLP_TRY(dispatch_bwd(h, A, Ly, has_dprev));
             prof_stop(h);
             // the forward reads the weights in mirror order: refresh that copy by a gather
             // right after the update, while the canonical values are still L2-resident
-            if (is_fused && last && !(l == 2 && h->xbits)) {
+            if (is_fused && last && !(l == 2 && h->xbits) && !A.mval_scatter) {
                 prof_start(h, K_MIRROR, l, 12.0 * nnz, 0.0);
                 SMLP_TRY(refresh_mirror_values(h, Ly));
                 prof_stop(h);
