@@ -318,11 +318,15 @@ __global__ void __launch_bounds__(256) fwd_finish_kernel(FwdArgs A) {
 // two fmaf).  Partial sums over the groups are combined by a fixed xor butterfly (every lane ends
 // with the same bits), so results stay deterministic.
 // ------------------------------------------------------------------------------------------
-template <int CB>
+template <int CB, bool FWD = false>
 struct RowCfg {
     static constexpr int G = CB / 4;                       // lanes per entry row (one float4 each)
     static constexpr int P = 32 / G;                       // entries per gather instruction
-    static constexpr int U = (32 / P) < 8 ? (32 / P) : 8;  // gather slots per batch (8 x 16 B in flight per lane)
+    // gather slots per batch: 8 x 16 B in flight per lane (more slots cost occupancy and measured
+    // slower at every CB: profiles/spmm_bench_r01.txt, r01ae)
+    static constexpr int UMAX = 8;
+    static constexpr int U = (32 / P) < UMAX ? (32 / P) : UMAX;
+    static constexpr int MINB = U > 8 ? 2 : 4;             // resident 256-thread blocks per SM
     static constexpr int EB = U * P;                       // entries per batch
     static constexpr int NW = SEG_NNZ / 32;                // window registers per lane (a segment = one window)
     static constexpr int NB = SEG_NNZ / EB;                // batches per window
@@ -409,7 +413,7 @@ __device__ __forceinline__ void window_pad(int2* win, int n, int lane, int zero_
 template <int CB>
 __device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, const float4& acc, float bj, int lane,
                                                   uint32_t step_lo) {
-    using C = RowCfg<CB>;
+    using C = RowCfg<CB, true>;
     constexpr int G = C::G, P = C::P, NR = C::NR;
     const int g = lane / G, q = lane % G;
     uint32_t bal_p[NR], bal_k[NR];
@@ -453,7 +457,7 @@ __device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, c
 template <int CB, int NS>
 __device__ __forceinline__ void fwd_slots(const float* __restrict__ a_prev, const int2* win, int g, int q,
                                           float4& acc) {
-    constexpr int P = RowCfg<CB>::P;
+    constexpr int P = RowCfg<CB, true>::P;
     float4 x[NS];
     float wv[NS];
 #pragma unroll
@@ -471,7 +475,7 @@ __device__ __forceinline__ void fwd_slots(const float* __restrict__ a_prev, cons
 template <int CB>
 __device__ __forceinline__ void fwd_batch(const float* __restrict__ a_prev, const int2* win, int nb, int g, int q,
                                           float4& acc) {
-    using C = RowCfg<CB>;
+    using C = RowCfg<CB, true>;
     if constexpr (C::NQ == 1) {
         fwd_slots<CB, C::QS>(a_prev, win, g, q, acc);
     } else {
@@ -502,8 +506,8 @@ __device__ __forceinline__ void stage_window(int2* win, const int (&ix)[NW], con
 }
 
 template <int CB>
-__global__ void __launch_bounds__(256, 4) fwd_rows_kernel(FwdArgs A) {
-    using C = RowCfg<CB>;
+__global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(FwdArgs A) {
+    using C = RowCfg<CB, true>;
     constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB;
     __shared__ int2 win_all[WARPS_PER_BLOCK][SEG_NNZ];
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;

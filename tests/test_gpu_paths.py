@@ -138,7 +138,7 @@ def test_generic_output_layer_parity():
 # ----------------------------------------------------------------------------------------- C5 full size
 def test_c5_full_size_sampled_parity():
     """BASELINE configs[4] at full size (65536-500000-500000-500000-2, 52.3M connections) in the
-    bench launch configuration (B = 128, chunk_batch auto = 32 -> 4 chunks, binary-input path, fused
+    bench launch configuration (B = 128, chunk_batch auto = 64 -> 2 chunks, binary-input path, fused
     update).  Checked: ER topology and values bit-exact (all 52.3M), every forward activation and
     logit of the batch, and for seeded samples of connections / neurons of every layer the
     gradient (unfused) and the Eq. 1 update (fused) against the oracle's cone evaluation."""
@@ -148,7 +148,7 @@ def test_c5_full_size_sampled_parity():
     torch = _torch()
     cfg = get_config("C5")
     g, st = pair(cfg)
-    assert g.info()["chunk_batch"] == 32
+    assert g.info()["chunk_batch"] == 64
     assert_topology_equal(g, st, "C5 init")
     for Ly in st.layers:
         e = g.export_layer(Ly.l)
@@ -205,3 +205,45 @@ def test_c5_full_size_sampled_parity():
         e = g2.export_layer(l)
         assert rel_err(e["w"][ent[l]][ok], Ly.w[ent[l]][ok]) <= TOL, ("w", l)
         assert rel_err(e["v"][ent[l]][ok], Ly.v[ent[l]][ok]) <= TOL, ("v", l)
+
+
+@pytest.mark.parametrize("chunk,B,dropout", [(8, 29, 0.2), (16, 64, 0.0), (32, 77, 0.3), (64, 128, 0.0),
+                                             (128, 128, 0.2)])
+def test_long_rows_and_chunk_widths_parity(chunk, B, dropout):
+    """Rows longer than one 64-entry segment in both orientations (partials + fixed-order finish
+    kernels), every chunk width of the row kernels (slot / group layouts, ragged last chunk), the
+    unfused and the fused (Eq. 1 in the backward) update paths."""
+    from paper_2102_01732_b200 import SGD
+    torch = _torch()
+    # W^(2) 30 x 200 is dense-capped (canonical rows of 200 entries: 4 segments); W^(3) 200 x 150
+    # at eps 40 has ~70-entry canonical rows and ~93-entry mirror rows
+    cfg = get_config("C1", sizes=(30, 200, 150, 10), epsilon=40.0, alpha=0.6, dropout=dropout, batch=B)
+    g, st = pair(cfg, max_batch=B, chunk_batch=chunk)
+    assert max(np.diff(st.layers[1].row_ptr)) > 64
+    rng = np.random.default_rng([chunk, B])
+    X = rng.standard_normal((3 * B, 30)).astype(np.float32)
+    Y = rng.integers(0, 10, size=3 * B).astype(np.int32)
+    sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay)
+    for s in range(2):
+        x, y = X[s * B:(s + 1) * B], Y[s * B:(s + 1) * B]
+        tr = M.forward(st, x, True, s)
+        if sum(tr.ambiguous):
+            pytest.skip("kink-ambiguous batch")
+        g.forward(to_dev(x), train=True, step=s)
+        g.backward(to_dev(y), fused=None)
+        torch.cuda.synchronize()
+        for l in range(2, cfg.n_layers):
+            assert rel_err(g.sparse_mlp_export_trace(0, l, B), tr.a[l - 1]) <= TOL, ("a", l)
+        gr = M.backward(st, tr, y)
+        for Ly in st.layers:
+            assert rel_err(g.sparse_mlp_export_trace(2, Ly.l), gr.g[Ly.l - 2]) <= TOL, ("g", Ly.l)
+            assert rel_err(g.sparse_mlp_export_trace(3, Ly.l), gr.gb[Ly.l - 2]) <= TOL, ("gb", Ly.l)
+        g.step(sgd)
+        M.step(st, gr, sgd.lr, sgd.momentum, sgd.weight_decay)
+    x, y = X[2 * B:], Y[2 * B:]
+    g.forward(to_dev(x), train=True, step=2)
+    g.backward(to_dev(y), fused=sgd)
+    M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, 2)
+    torch.cuda.synchronize()
+    assert_values_close(g, st, TOL * 3, "long rows fused")
+    assert_topology_equal(g, st)
