@@ -167,6 +167,18 @@ int sparse_mlp_step(smlp_handle* h, const smlp_sgd* sgd);
 int sparse_mlp_train_step_host(smlp_handle* h, const float* x_host, const int32_t* y_host,
                                int32_t B, uint64_t step, const smlp_sgd* sgd, float* loss_host);
 
+/* sparse_mlp_train_step_host_async — the same step, pipelined: x_host / y_host go to one of two
+ * device staging buffers on an internal copy stream (waiting only for the forward that last
+ * read that buffer, two calls ago), so the H2D of step s+1 overlaps the compute of step s.
+ * ASYNC: returns once enqueued.  x_host, y_host and loss_host must be PINNED host memory and
+ * stay valid / unread until sparse_mlp_sync (loss_host: host float or NULL). */
+int sparse_mlp_train_step_host_async(smlp_handle* h, const float* x_host, const int32_t* y_host,
+                                     int32_t B, uint64_t step, const smlp_sgd* sgd, float* loss_host);
+
+/* sparse_mlp_sync — SYNC: waits for all work enqueued on the handle's stream; reports a
+ * deferred device error (SMLP_E_DATA label out of range). */
+int sparse_mlp_sync(smlp_handle* h);
+
 /* Contiguous device views [values of W^(2..L) at their capacity offsets || biases b_2..b_L],
  * identical layout on every replica, stable for the life of the handle (holes left by
  * pruning are zero).  grad view: filled by an unfused backward (X1 allreduce, SUM).

@@ -304,6 +304,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     if (const char* e = std::getenv("SMLP_GATHER_EVICT_LAST")) h->gather_evict_last = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_KVER")) h->kver = std::atoi(e);
     if (const char* e = std::getenv("SMLP_MIRROR_SCATTER")) h->mirror_scatter = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMLP_L2HINT")) h->l2hint = std::atoi(e);
     const int rc = build_handle(h, cfg);
     if (rc != SMLP_OK) {
         g_create_error = h->err;
@@ -324,7 +325,14 @@ int sparse_mlp_destroy(smlp_handle* h) {
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     for (auto& a : h->allocs) tmp_free(h, a.ptr, a.bytes);
     h->allocs.clear();
-    if (h->x_stage || h->y_stage) { /* tracked above */ }
+    for (int k = 0; k < 2; ++k) {
+        if (h->ev_copied[k]) cudaEventDestroy(h->ev_copied[k]);
+        if (h->ev_consumed[k]) cudaEventDestroy(h->ev_consumed[k]);
+    }
+    if (h->copy_stream) {
+        cudaStreamSynchronize(h->copy_stream);
+        cudaStreamDestroy(h->copy_stream);
+    }
     cudaStreamSynchronize(h->stream);
     delete h;
     return SMLP_OK;
@@ -417,25 +425,58 @@ int sparse_mlp_step(smlp_handle* h, const smlp_sgd* sgd) {
     return rc;
 }
 
-int sparse_mlp_train_step_host(smlp_handle* h, const float* x_host, const int32_t* y_host, int32_t B, uint64_t step,
-                               const smlp_sgd* sgd, float* loss_host) {
+// pipelined host-buffer step: staging buffer k = call parity; its H2D runs on the copy stream
+// (waiting only for the forward that last read buffer k, two calls ago), so the copy of step s+1
+// overlaps the compute of step s
+static int stage_and_step(smlp_handle* h, const float* x_host, const int32_t* y_host, int32_t B, uint64_t step,
+                          const smlp_sgd* sgd, float* loss_host) {
     if (!h || !x_host || !y_host || !sgd) return SMLP_E_ARG;
     if (B < 1 || B > h->max_batch) return set_err(h, SMLP_E_SHAPE, "B out of range");
-    if (!h->x_stage) {
-        h->x_stage = (float*)dev_alloc(h, sizeof(float) * (size_t)h->max_batch * (size_t)h->sizes[0]);
-        h->y_stage = (int32_t*)dev_alloc(h, sizeof(int32_t) * (size_t)h->max_batch);
-        if (!h->x_stage || !h->y_stage) return set_err(h, SMLP_E_NOMEM, "staging buffers");
+    if (!h->x_stage[0]) {
+        for (int k = 0; k < 2; ++k) {
+            h->x_stage[k] = (float*)dev_alloc(h, sizeof(float) * (size_t)h->max_batch * (size_t)h->sizes[0]);
+            h->y_stage[k] = (int32_t*)dev_alloc(h, sizeof(int32_t) * (size_t)h->max_batch);
+            if (!h->x_stage[k] || !h->y_stage[k]) return set_err(h, SMLP_E_NOMEM, "staging buffers");
+            SMLP_CK(h, cudaEventCreateWithFlags(&h->ev_copied[k], cudaEventDisableTiming));
+            SMLP_CK(h, cudaEventCreateWithFlags(&h->ev_consumed[k], cudaEventDisableTiming));
+            SMLP_CK(h, cudaEventRecord(h->ev_consumed[k], h->stream));
+        }
+        SMLP_CK(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
     }
-    SMLP_CK(h, cudaMemcpyAsync(h->x_stage, x_host, sizeof(float) * (size_t)B * (size_t)h->sizes[0],
-                               cudaMemcpyHostToDevice, h->stream));
-    SMLP_CK(h, cudaMemcpyAsync(h->y_stage, y_host, sizeof(int32_t) * (size_t)B, cudaMemcpyHostToDevice, h->stream));
-    SMLP_TRY(sparse_mlp_forward(h, h->x_stage, nullptr, B, 1, step, nullptr));
+    const int k = h->stage_idx;
+    h->stage_idx ^= 1;
+    SMLP_CK(h, cudaStreamWaitEvent(h->copy_stream, h->ev_consumed[k], 0));
+    SMLP_CK(h, cudaMemcpyAsync(h->x_stage[k], x_host, sizeof(float) * (size_t)B * (size_t)h->sizes[0],
+                               cudaMemcpyHostToDevice, h->copy_stream));
+    SMLP_CK(h, cudaMemcpyAsync(h->y_stage[k], y_host, sizeof(int32_t) * (size_t)B, cudaMemcpyHostToDevice,
+                               h->copy_stream));
+    SMLP_CK(h, cudaEventRecord(h->ev_copied[k], h->copy_stream));
+    SMLP_CK(h, cudaStreamWaitEvent(h->stream, h->ev_copied[k], 0));
+    SMLP_TRY(sparse_mlp_forward(h, h->x_stage[k], nullptr, B, 1, step, nullptr));
+    SMLP_CK(h, cudaEventRecord(h->ev_consumed[k], h->stream));
     smlp_sgd f = *sgd;
     f.grad_scale = 1.f;
-    SMLP_TRY(sparse_mlp_backward(h, h->y_stage, nullptr, h->d_loss, &f));
+    SMLP_TRY(sparse_mlp_backward(h, h->y_stage[k], nullptr, h->d_loss, &f));
     if (loss_host) SMLP_CK(h, cudaMemcpyAsync(loss_host, h->d_loss, sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+    return SMLP_OK;
+}
+
+int sparse_mlp_train_step_host(smlp_handle* h, const float* x_host, const int32_t* y_host, int32_t B, uint64_t step,
+                               const smlp_sgd* sgd, float* loss_host) {
+    SMLP_TRY(stage_and_step(h, x_host, y_host, B, step, sgd, loss_host));
     SMLP_CK(h, cudaStreamSynchronize(h->stream));
     return SMLP_OK;
+}
+
+int sparse_mlp_train_step_host_async(smlp_handle* h, const float* x_host, const int32_t* y_host, int32_t B,
+                                     uint64_t step, const smlp_sgd* sgd, float* loss_host) {
+    return stage_and_step(h, x_host, y_host, B, step, sgd, loss_host);
+}
+
+int sparse_mlp_sync(smlp_handle* h) {
+    if (!h) return SMLP_E_ARG;
+    SMLP_CK(h, cudaStreamSynchronize(h->stream));
+    return check_data_flag(h);
 }
 
 int sparse_mlp_grad_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version) {

@@ -138,8 +138,12 @@ struct smlp_handle {
     int32_t* d_nonbinary = nullptr; // set by stage_input when an input value is not 0 or 1
     float* gmirror2 = nullptr;      // [cap of W^(2)] gradient in mirror order (binary-input path)
     float* d_loss = nullptr;        // scratch loss for train_step_host
-    float* x_stage = nullptr;       // [max_batch x n_1] for train_step_host
-    int32_t* y_stage = nullptr;
+    float* x_stage[2] = {nullptr, nullptr};   // [max_batch x n_1] x2 for train_step_host (double-buffered)
+    int32_t* y_stage[2] = {nullptr, nullptr};
+    cudaStream_t copy_stream = nullptr;        // H2D of the next host batch, overlapping the current step
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+    cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
+    int stage_idx = 0;
 
     // trace of the last forward
     bool trace_valid = false;
@@ -157,7 +161,8 @@ struct smlp_handle {
     int num_sms = 148;
     int kver = 3;                   // tuning knob (env SMLP_KVER): 3 = warp-per-row kernels, 2 = group kernels
     int gather_evict_last = 0;
-    int mirror_scatter = 0;         // tuning knob (env SMLP_MIRROR_SCATTER): fused update scatters into mval      // tuning knob (env SMLP_GATHER_EVICT_LAST): L2 policy of row gathers
+    int mirror_scatter = 0;
+    int l2hint = 0;                 // tuning knob (env SMLP_L2HINT): L2 eviction policies in the row kernels         // tuning knob (env SMLP_MIRROR_SCATTER): fused update scatters into mval      // tuning knob (env SMLP_GATHER_EVICT_LAST): L2 policy of row gathers
     int64_t launches = 0;
     std::string err;
 };

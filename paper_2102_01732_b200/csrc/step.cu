@@ -102,6 +102,25 @@ __device__ __forceinline__ void st_f32(float* p, float v, uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(p), "f"(v), "l"(pol) : "memory");
 }
 
+// L2-hinted variants used by the row kernels (hint = createpolicy register; "evict_normal" when the
+// knob is off, so the instruction count is the same either way)
+__device__ __forceinline__ float4 ldg4_hint(const float* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_hint(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t gather_policy(int hint) { return hint ? policy_evict_last() : policy_evict_normal(); }
+__device__ __forceinline__ uint64_t stream_policy(int hint) { return hint ? policy_evict_first() : policy_evict_normal(); }
+
 // ------------------------------------------------------------------------------------------
 // a1: input staging (transpose + optional row gather), zero padding of columns b >= B
 // ------------------------------------------------------------------------------------------
@@ -175,6 +194,7 @@ struct FwdArgs {
     const int32_t* skip_if_binary;   // layer 2 with the binary-input path: return if *flag == 0
     int gather_evict_last;           // L2 policy of the gathered rows: evict_last (1) or normal (0)
     int zero_row;                    // row index (relative to a_prev) of the zero row after the last chunk
+    int l2hint;                      // L2 policies: gathers evict_last, streamed operands evict_first
 };
 
 // Epilogue of one output row j per group: all 32 lanes call it (ballots); `own` marks the
@@ -326,10 +346,11 @@ struct RowCfg {
     // slower at every CB: profiles/spmm_bench_r01.txt, r01ae)
     static constexpr int UMAX = 8;
     static constexpr int U = (32 / P) < UMAX ? (32 / P) : UMAX;
-    static constexpr int MINB = U > 8 ? 2 : 4;             // resident 256-thread blocks per SM
+    static constexpr int MINB = U > 12 ? 2 : (U > 8 ? 3 : 4);   // resident 256-thread blocks per SM
     static constexpr int EB = U * P;                       // entries per batch
     static constexpr int NW = SEG_NNZ / 32;                // window registers per lane (a segment = one window)
-    static constexpr int NB = SEG_NNZ / EB;                // batches per window
+    static constexpr int NB = (SEG_NNZ + EB - 1) / EB;     // batches per window
+    static constexpr int WIN = (NB * EB + 31) / 32 * 32;   // window slots in shared memory (>= SEG_NNZ)
     static constexpr int QS = U < 4 ? U : 4;               // slots per "quad" (issue granularity)
     static constexpr int NQ = U / QS;                      // quads per batch
     static constexpr int NR = P >= 4 ? 1 : 4 / P;          // epilogue components per lane
@@ -456,7 +477,7 @@ __device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, c
 // NS gather slots of a batch, all issued before the first FMA (entry u P + g of the window in slot u)
 template <int CB, int NS>
 __device__ __forceinline__ void fwd_slots(const float* __restrict__ a_prev, const int2* win, int g, int q,
-                                          float4& acc) {
+                                          float4& acc, uint64_t pg) {
     constexpr int P = RowCfg<CB, true>::P;
     float4 x[NS];
     float wv[NS];
@@ -464,7 +485,7 @@ __device__ __forceinline__ void fwd_slots(const float* __restrict__ a_prev, cons
     for (int u = 0; u < NS; ++u) {
         const int2 e = win[u * P + g];
         wv[u] = __int_as_float(e.y);
-        x[u] = ldg4(a_prev + (int64_t)e.x * CB + q * 4);
+        x[u] = ldg4_hint(a_prev + (int64_t)e.x * CB + q * 4, pg);
     }
 #pragma unroll
     for (int u = 0; u < NS; ++u) fma4p(acc, wv[u], x[u]);
@@ -474,13 +495,13 @@ __device__ __forceinline__ void fwd_slots(const float* __restrict__ a_prev, cons
 // one fully unrolled body per length class; the padding slots gather the zero row)
 template <int CB>
 __device__ __forceinline__ void fwd_batch(const float* __restrict__ a_prev, const int2* win, int nb, int g, int q,
-                                          float4& acc) {
+                                          float4& acc, uint64_t pg) {
     using C = RowCfg<CB, true>;
     if constexpr (C::NQ == 1) {
-        fwd_slots<CB, C::QS>(a_prev, win, g, q, acc);
+        fwd_slots<CB, C::QS>(a_prev, win, g, q, acc, pg);
     } else {
-        if (nb > C::QS * C::P) fwd_slots<CB, C::U>(a_prev, win, g, q, acc);
-        else fwd_slots<CB, C::QS>(a_prev, win, g, q, acc);
+        if (nb > C::QS * C::P) fwd_slots<CB, C::U>(a_prev, win, g, q, acc, pg);
+        else fwd_slots<CB, C::QS>(a_prev, win, g, q, acc, pg);
     }
 }
 
@@ -509,10 +530,12 @@ template <int CB>
 __global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(FwdArgs A) {
     using C = RowCfg<CB, true>;
     constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB;
-    __shared__ int2 win_all[WARPS_PER_BLOCK][SEG_NNZ];
+    __shared__ int2 win_all[WARPS_PER_BLOCK][C::WIN];
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
     int2* win = win_all[threadIdx.x >> 5];
+    for (int e = SEG_NNZ + lane; e < C::WIN; e += 32) win[e] = make_int2(A.zero_row, 0);   // never-used tail
+    const uint64_t pg = gather_policy(A.l2hint);
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nseg = A.meta->n_fseg;
@@ -538,7 +561,7 @@ __global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(F
         float4 acc = f4zero();
 #pragma unroll
         for (int b = 0; b < NB; ++b)
-            if (b * EB < n) fwd_batch<CB>(A.a_prev, win + b * EB, n - b * EB, g, q, acc);
+            if (b * EB < n) fwd_batch<CB>(A.a_prev, win + b * EB, n - b * EB, g, q, acc, pg);
         acc = group_allreduce<G>(acc);
         if (cur.w < 0) {
             fwd_rows_epilogue<CB>(A, cur.x, acc, bj, lane, step_lo);
@@ -676,6 +699,7 @@ struct BwdArgs {
     const int32_t* skip_if_binary;   // layer 2 with the binary-input path: return if *flag == 0
     int gather_evict_last;           // L2 policy of the gathered rows: evict_last (1) or normal (0)
     int zero_row;                    // row index (relative to d_out) of the zero row after the last chunk
+    int l2hint;                      // L2 policies: gathers evict_last, streamed operands evict_first
 };
 
 // delta_{l-1} of input row i per group: f'(z) from the sign bits, dropout keep bits, store, and
@@ -921,7 +945,7 @@ __device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, c
 
 template <int CB, int NS, bool HAS_DPREV>
 __device__ __forceinline__ void bwd_slots(const float* __restrict__ d_out, const int2* win, float* red,
-                                          const float4& ai, int g, int q, float4& dacc) {
+                                          const float4& ai, int g, int q, float4& dacc, uint64_t pg) {
     using C = RowCfg<CB>;
     constexpr int P = C::P, S = C::S;
     float4 dx[NS];
@@ -930,7 +954,7 @@ __device__ __forceinline__ void bwd_slots(const float* __restrict__ d_out, const
     for (int u = 0; u < NS; ++u) {
         const int2 e = win[u * P + g];
         wv[u] = __int_as_float(e.y);
-        dx[u] = ldg4(d_out + (int64_t)e.x * CB + q * 4);
+        dx[u] = ldg4_hint(d_out + (int64_t)e.x * CB + q * 4, pg);
     }
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
@@ -941,13 +965,13 @@ __device__ __forceinline__ void bwd_slots(const float* __restrict__ d_out, const
 
 template <int CB, bool HAS_DPREV>
 __device__ __forceinline__ void bwd_batch(const float* __restrict__ d_out, const int2* win, float* red, int nb,
-                                          const float4& ai, int g, int q, float4& dacc) {
+                                          const float4& ai, int g, int q, float4& dacc, uint64_t pg) {
     using C = RowCfg<CB>;
     if constexpr (C::NQ == 1) {
-        bwd_slots<CB, C::QS, HAS_DPREV>(d_out, win, red, ai, g, q, dacc);
+        bwd_slots<CB, C::QS, HAS_DPREV>(d_out, win, red, ai, g, q, dacc, pg);
     } else {
-        if (nb > C::QS * C::P) bwd_slots<CB, C::U, HAS_DPREV>(d_out, win, red, ai, g, q, dacc);
-        else bwd_slots<CB, C::QS, HAS_DPREV>(d_out, win, red, ai, g, q, dacc);
+        if (nb > C::QS * C::P) bwd_slots<CB, C::U, HAS_DPREV>(d_out, win, red, ai, g, q, dacc, pg);
+        else bwd_slots<CB, C::QS, HAS_DPREV>(d_out, win, red, ai, g, q, dacc, pg);
     }
 }
 
@@ -973,6 +997,7 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     const int64_t s_lo = warp * nseg / nwarps, s_hi = (warp + 1) * nseg / nwarps;
     if (s_lo >= s_hi) return;
     const int4 none = make_int4(0, 0, 0, -2);
+    const uint64_t pg = gather_policy(A.l2hint), ps = stream_policy(A.l2hint);
     // window + a_{l-1}[i] of a segment into buffer b (cp.async, one segment ahead: no registers held)
     auto prefetch = [&](const int4& sg, int b) {
         window_async(win[b], A.col, A.val, sg.y, sg.z, lane);
@@ -995,9 +1020,9 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
         for (int r = 0; r < NW; ++r) {
             const int k = cur.y + lane + 32 * r;
             const bool ok = lane + 32 * r < n;
-            w[r] = UPD && ok ? __ldg(A.val + k) : 0.f;
-            gold[r] = GOLD && ok ? A.grad[k] : 0.f;
-            mold[r] = UPD && ok ? A.mom[k] : 0.f;
+            w[r] = UPD && ok ? ld_hint(A.val + k, ps) : 0.f;
+            gold[r] = GOLD && ok ? ld_hint(A.grad + k, ps) : 0.f;
+            mold[r] = UPD && ok ? ld_hint(A.mom + k, ps) : 0.f;
         }
         const BwdSide sd = bwd_side<DROP>(A, cur.x, HAS_DPREV && cur.w < 0, lane);
         cp_async_wait1();
@@ -1016,7 +1041,7 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
                 for (int b = b0; b < b0 + RB; ++b)
                     if (b * EB < n)
                         bwd_batch<CB, HAS_DPREV>(A.d_out, win[buf] + b * EB, red + (b - b0) * EB * S, n - b * EB, ai, g, q,
-                                                 dacc);
+                                                 dacc, pg);
                 __syncwarp();
                 // window entry e = lane + 32 r of this round: fixed-order sum of its G lane partials
 #pragma unroll
@@ -1052,11 +1077,11 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
                 const int k = cur.y + e;
                 const float gk = gsum[r] + gold[r];
                 if (!UPD) {
-                    A.grad[k] = gk;
+                    st_hint(A.grad + k, gk, ps);
                 } else {
                     const float v = A.mu * mold[r] - A.lr * (gk + A.wd * w[r]);
-                    A.mom[k] = v;
-                    A.val[k] = w[r] + v;
+                    st_hint(A.mom + k, v, ps);
+                    st_hint(A.val + k, w[r] + v, ps);
                     if (A.mval_scatter) A.mval[__ldg(A.minv + k)] = w[r] + v;   // the forward's mirror copy
                 }
             }
@@ -2123,6 +2148,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
             A.gather_evict_last = h->gather_evict_last;
             A.zero_row = (int)((int64_t)(h->max_chunks - c) * nin);
+            A.l2hint = h->l2hint;
             prof_start(h, K_FWD, l, 12.0 * nnz / nchunks + 4.0 * Bc * (double)(nin + nout), 2.0 * nnz * Bc);
             SMLP_TRY(dispatch_fwd(h, A, Ly));
             prof_stop(h);
@@ -2241,6 +2267,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
             A.gather_evict_last = h->gather_evict_last;
             A.zero_row = (int)((int64_t)(h->max_chunks - c) * nout);
+            A.l2hint = h->l2hint;
             A.mval_scatter = (h->mirror_scatter && h->kver >= 3 && !(l == 2 && h->xbits)) ? 1 : 0;
             prof_start(h, K_BWD, l, (is_fused ? 20.0 : 12.0) * nnz / nchunks + act_bytes,
                        (has_dprev ? 4.0 : 2.0) * nnz * Bc);

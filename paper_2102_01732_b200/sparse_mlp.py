@@ -29,7 +29,8 @@ PRUNE_OUTGOING = 1
 # the symbols include/sparse_mlp.h declares (checked by tests/test_abi.py)
 EXPORTED = [
     "sparse_mlp_create", "sparse_mlp_destroy", "sparse_mlp_set_stream", "sparse_mlp_forward",
-    "sparse_mlp_backward", "sparse_mlp_step", "sparse_mlp_train_step_host", "sparse_mlp_grad_view",
+    "sparse_mlp_backward", "sparse_mlp_step", "sparse_mlp_train_step_host", "sparse_mlp_train_step_host_async",
+    "sparse_mlp_sync", "sparse_mlp_grad_view",
     "sparse_mlp_param_view", "sparse_mlp_evolve_topology", "sparse_mlp_prune_neurons",
     "sparse_mlp_importance", "sparse_mlp_info", "sparse_mlp_export_layer", "sparse_mlp_import_layer",
     "sparse_mlp_export_bias", "sparse_mlp_import_bias", "sparse_mlp_export_alive",
@@ -103,6 +104,8 @@ def load_library(path: str = LIB_PATH):
         "sparse_mlp_backward": (I32, [VP, VP, VP, VP, P(smlp_sgd)]),
         "sparse_mlp_step": (I32, [VP, P(smlp_sgd)]),
         "sparse_mlp_train_step_host": (I32, [VP, VP, VP, I32, U64, P(smlp_sgd), VP]),
+        "sparse_mlp_train_step_host_async": (I32, [VP, VP, VP, I32, U64, P(smlp_sgd), VP]),
+        "sparse_mlp_sync": (I32, [VP]),
         "sparse_mlp_grad_view": (I32, [VP, P(VP), P(I64), P(U64)]),
         "sparse_mlp_param_view": (I32, [VP, P(VP), P(I64), P(U64)]),
         "sparse_mlp_evolve_topology": (I32, [VP, D, U64, VP]),
@@ -248,6 +251,15 @@ class SparseMLP:
                                                         C.byref(sgd.c()), C.byref(out)))
         return float(out.value)
 
+    def sparse_mlp_train_step_host_async(self, x_host, y_host, B: int, step: int, sgd: SGD, loss_host=None):
+        """Pipelined host-buffer step (pinned x_host / y_host / loss_host tensors); no sync."""
+        self._sync_stream()
+        self._check(self.lib.sparse_mlp_train_step_host_async(self.h, _ptr(x_host), _ptr(y_host), int(B), int(step),
+                                                              C.byref(sgd.c()), _ptr(loss_host)))
+
+    def sparse_mlp_sync(self):
+        self._check(self.lib.sparse_mlp_sync(self.h))
+
     def sparse_mlp_grad_view(self):
         p, n, v = C.c_void_p(), C.c_int64(), C.c_uint64()
         self._check(self.lib.sparse_mlp_grad_view(self.h, C.byref(p), C.byref(n), C.byref(v)))
@@ -380,6 +392,8 @@ class SparseMLP:
     grad_view = sparse_mlp_grad_view
     param_view = sparse_mlp_param_view
     train_step_host = sparse_mlp_train_step_host
+    train_step_host_async = sparse_mlp_train_step_host_async
+    sync = sparse_mlp_sync
 
 
 def from_config(cfg, seed: Optional[int] = None, rank: int = 0, max_batch: Optional[int] = None,

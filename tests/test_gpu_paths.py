@@ -247,3 +247,28 @@ def test_long_rows_and_chunk_widths_parity(chunk, B, dropout):
     torch.cuda.synchronize()
     assert_values_close(g, st, TOL * 3, "long rows fused")
     assert_topology_equal(g, st)
+
+
+def test_pipelined_host_step_matches_sync():
+    """sparse_mlp_train_step_host_async (double-buffered staging on a copy stream) computes the
+    same training trajectory as the synchronous host-buffer step and the device-buffer path,
+    bit for bit, and delivers every step's loss."""
+    from paper_2102_01732_b200 import SGD
+    torch = _torch()
+    cfg = _binary_cfg(batch=64, dropout=0.2)
+    g1, _ = pair(cfg, max_batch=64)
+    g2, _ = pair(cfg, max_batch=64)
+    X, Y = _binary_data(4 * 64, cfg.sizes[0], seed=21)
+    xp, yp = torch.from_numpy(X).pin_memory(), torch.from_numpy(Y).pin_memory()
+    losses = torch.zeros(4, dtype=torch.float32).pin_memory()
+    sgd = SGD(cfg.lr, cfg.momentum, cfg.weight_decay)
+    ref = []
+    for s in range(4):
+        ref.append(g1.train_step_host(xp[s * 64:(s + 1) * 64], yp[s * 64:(s + 1) * 64], 64, s, sgd))
+        g2.train_step_host_async(xp[s * 64:(s + 1) * 64], yp[s * 64:(s + 1) * 64], 64, s, sgd, losses[s:])
+    g2.sync()
+    torch.cuda.synchronize()
+    assert np.array_equal(losses.numpy(), np.array(ref, np.float32))
+    for l in range(2, cfg.n_layers + 1):
+        a, b = g1.export_layer(l), g2.export_layer(l)
+        assert np.array_equal(a["w"].view(np.uint32), b["w"].view(np.uint32))

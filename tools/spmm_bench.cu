@@ -239,6 +239,48 @@ __global__ void __launch_bounds__(256, MINB) k_row(Csr C) {
     }
 }
 
+// ---- split: row kernel over the entry sub-range [sb[j], se[j]) of every row (the entries whose
+// source lies in one slice of the slab), accumulating into z when ACC (source-range split passes
+// keep the gathered slab slice L2-resident)
+template <int CB, bool ACC>
+__global__ void __launch_bounds__(256, 4) k_split(Csr C, const int* __restrict__ sb, const int* __restrict__ se) {
+    constexpr int G = CB / 4, P = 32 / G, U = 8, QS = 4, EB = U * P;
+    __shared__ int2 win_all[8][MAXROW + 32];
+    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
+    int2* win = win_all[threadIdx.x >> 5];
+    const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * (long)blockDim.x) >> 5;
+    const long r_lo = warp * C.n_out / nw, r_hi = (warp + 1) * C.n_out / nw;
+    if (r_lo >= r_hi) return;
+    int beg = sb[r_lo], end = se[r_lo];
+    int s0 = beg + lane < end ? __ldg(C.src + beg + lane) : 0, s1 = beg + 32 + lane < end ? __ldg(C.src + beg + 32 + lane) : 0;
+    float w0 = beg + lane < end ? __ldg(C.w + beg + lane) : 0.f, w1 = beg + 32 + lane < end ? __ldg(C.w + beg + 32 + lane) : 0.f;
+    for (long r = r_lo; r < r_hi; ++r) {
+        int nbeg = 0, nend = 0;
+        if (r + 1 < r_hi) { nbeg = sb[r + 1]; nend = se[r + 1]; }
+        const int t0 = nbeg + lane < nend ? __ldg(C.src + nbeg + lane) : 0;
+        const int t1 = nbeg + 32 + lane < nend ? __ldg(C.src + nbeg + 32 + lane) : 0;
+        const float v0 = nbeg + lane < nend ? __ldg(C.w + nbeg + lane) : 0.f;
+        const float v1 = nbeg + 32 + lane < nend ? __ldg(C.w + nbeg + 32 + lane) : 0.f;
+        float4 prev = make_float4(0, 0, 0, 0);
+        if (ACC && g == 0) prev = *reinterpret_cast<const float4*>(C.z + r * CB + q * 4);
+        __syncwarp();
+        const int n = end - beg;
+        win[lane] = lane < n ? make_int2(s0, __float_as_int(w0)) : make_int2(C.zero_row, 0);
+        win[lane + 32] = lane + 32 < n ? make_int2(s1, __float_as_int(w1)) : make_int2(C.zero_row, 0);
+        win[lane + 64] = make_int2(C.zero_row, 0);
+        __syncwarp();
+        float4 acc = make_float4(0, 0, 0, 0);
+        for (int bo = 0; bo < n; bo += EB) {
+            const int nb = min(EB, n - bo);
+            if (nb > QS * P) row_slots<CB, U, false>(C, win + bo, g, q, acc, 0);
+            else row_slots<CB, QS, false>(C, win + bo, g, q, acc, 0);
+        }
+        acc = allred<G>(acc);
+        if (g == 0) *reinterpret_cast<float4*>(C.z + r * CB + q * 4) = f4add(acc, prev);
+        beg = nbeg; end = nend; s0 = t0; s1 = t1; w0 = v0; w1 = v1;
+    }
+}
+
 // ---- row2: one warp per row, (src, w) broadcast by shuffles from the prefetched registers
 template <int CB, int NS, int MODE>
 __device__ __forceinline__ void row2_slots(const Csr& C, int s0, int s1, float w0, float w1, int bo, int g, int q,
@@ -676,6 +718,32 @@ void run_cb(int n, double mean, int sms) {
     ROW(12, false, 3, "row U12 minb3");
     ROW(16, false, 2, "row U16 minb2");
     ROW(8, true, 4, "rowpol U8 minb4");
+    {   // source-range split passes: NS slices of the slab, one pass each (the last accumulates)
+        for (int NSL : {1, 2, 4}) {
+            std::vector<int> spl((size_t)(NSL + 1) * n);
+            for (int j = 0; j < n; ++j) {
+                int k = rp[j];
+                for (int sl = 0; sl <= NSL; ++sl) {
+                    const long lim = (long)n * sl / NSL;
+                    while (k < rp[j + 1] && src[k] < lim) ++k;
+                    spl[(size_t)sl * n + j] = sl == 0 ? rp[j] : (sl == NSL ? rp[j + 1] : k);
+                }
+            }
+            int* d_spl;
+            CK(cudaMalloc(&d_spl, spl.size() * 4));
+            CK(cudaMemcpy(d_spl, spl.data(), spl.size() * 4, cudaMemcpyHostToDevice));
+            int nb = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_split<CB, true>, 256, 0);
+            ms = timeit([&] {
+                k_split<CB, false><<<sms * nb, 256>>>(C, d_spl, d_spl + n);
+                for (int sl = 1; sl < NSL; ++sl) k_split<CB, true><<<sms * nb, 256>>>(C, d_spl + (size_t)sl * n, d_spl + (size_t)(sl + 1) * n);
+            });
+            char nm[64];
+            snprintf(nm, 64, "split x%d passes (nb %d)", NSL, nb);
+            report(nm, ms, true);
+            cudaFree(d_spl);
+        }
+    }
 #define CPA(WPB, NST)                                                                              \
     {                                                                                              \
         const size_t sm = (size_t)WPB * NST * (MAXROW * CB * 4 + MAXROW * 4);                      \
@@ -687,12 +755,9 @@ void run_cb(int n, double mean, int sms) {
         snprintf(nm, 64, "cpa wpb%d nst%d x%d", WPB, NST, nb);                                     \
         report(nm, ms, true);                                                                      \
     }
+    if (CB > 32) return;   // the shared-memory staging variants below do not fit wider rows
     CPA(4, 2);
-    CPA(4, 3);
     CPA(8, 2);
-    CPA(6, 2);
-    CPA(2, 4);
-    CPA(12, 2);
     // TMA gather4
     static EncodeFn enc = nullptr;
     if (!enc) {
@@ -734,6 +799,7 @@ int main(int argc, char** argv) {
     printf("# SMs %d, n %d, mean row %.1f\n", sms, n, mean);
     run_cb<32>(n, mean, sms);
     if (getenv("ONLY_ROW")) return 0;
-    run_cb<16>(n, mean, sms);
+    run_cb<64>(n, mean, sms);
+    run_cb<128>(n, mean, sms);
     return 0;
 }
