@@ -305,6 +305,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     if (const char* e = std::getenv("SMLP_KVER")) h->kver = std::atoi(e);
     if (const char* e = std::getenv("SMLP_MIRROR_SCATTER")) h->mirror_scatter = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_L2HINT")) h->l2hint = std::atoi(e);
+    if (const char* e = std::getenv("SMLP_L2PERSIST")) h->l2persist = std::atoi(e);
     const int rc = build_handle(h, cfg);
     if (rc != SMLP_OK) {
         g_create_error = h->err;

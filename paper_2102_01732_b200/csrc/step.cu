@@ -1253,8 +1253,19 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) fwd_narrow_kernel(NarrowArg
 template <int CB, int NOUT>
 __global__ void __launch_bounds__(32) fwd_narrow_finish_kernel(NarrowArgs A, int nparts) {
     const int e = blockIdx.x, lane = threadIdx.x;
+    // lane b sums parts b, b + 32, ... in order; the loads of 8 parts are issued together (one
+    // latency per 8 parts instead of one per part)
     float s = 0.f;
-    for (int b = lane; b < nparts; b += 32) s += A.ws[(int64_t)b * NOUT * CB + e];
+    for (int b0 = lane; b0 < nparts; b0 += 32 * 8) {
+        float p[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int b = b0 + 32 * u;
+            p[u] = b < nparts ? __ldg(A.ws + (int64_t)b * NOUT * CB + e) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += p[u];
+    }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
     if (lane == 0) A.a_out[e] = s + __ldg(A.bias + e / CB);
@@ -2081,6 +2092,27 @@ NarrowArgs narrow_args(smlp_handle* h, Layer& Ly, int c) {
     return A;
 }
 
+// Optional persisting-L2 access window over the slab a row kernel gathers from (knob
+// SMLP_L2PERSIST = hit ratio in percent; 0 = off).  Stream attribute, set around the launch.
+static void l2_window(smlp_handle* h, const void* base, size_t bytes) {
+    if (h->l2persist <= 0) return;
+    static bool limit_set = false;
+    if (!limit_set) {
+        int maxp = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
+        limit_set = true;
+    }
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    v.accessPolicyWindow.num_bytes = bytes;
+    v.accessPolicyWindow.hitRatio = bytes ? (float)h->l2persist / 100.f : 0.f;
+    v.accessPolicyWindow.hitProp = bytes ? cudaAccessPropertyPersisting : cudaAccessPropertyNormal;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    if (!bytes) cudaCtxResetPersistingL2Cache();
+}
+
 int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, bool train, uint64_t step,
                 float* probs) {
     const int CB = h->CB;
@@ -2150,7 +2182,9 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             A.zero_row = (int)((int64_t)(h->max_chunks - c) * nin);
             A.l2hint = h->l2hint;
             prof_start(h, K_FWD, l, 12.0 * nnz / nchunks + 4.0 * Bc * (double)(nin + nout), 2.0 * nnz * Bc);
+            l2_window(h, A.a_prev, (size_t)nin * CB * sizeof(float));
             SMLP_TRY(dispatch_fwd(h, A, Ly));
+            l2_window(h, nullptr, 0);
             prof_stop(h);
         }
     }
@@ -2271,7 +2305,9 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.mval_scatter = (h->mirror_scatter && h->kver >= 3 && !(l == 2 && h->xbits)) ? 1 : 0;
             prof_start(h, K_BWD, l, (is_fused ? 20.0 : 12.0) * nnz / nchunks + act_bytes,
                        (has_dprev ? 4.0 : 2.0) * nnz * Bc);
+            l2_window(h, A.d_out, (size_t)nout * CB * sizeof(float));
             SMLP_TRY(dispatch_bwd(h, A, Ly, has_dprev));
+            l2_window(h, nullptr, 0);
             prof_stop(h);
             // the forward reads the weights in mirror order: refresh that copy by a gather
             // right after the update, while the canonical values are still L2-resident
