@@ -180,7 +180,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2102_01732_b200 import SGD, SparseMLP
-    from paper_2102_01732_b200.dp import allreduce_sum_, init_process_group, replicas_identical, scaled_lr
+    from paper_2102_01732_b200.dp import OverlappedAllreduce, init_process_group, replicas_identical, scaled_lr
     from synth import get_config
 
     rank, world, local = init_process_group()
@@ -213,16 +213,23 @@ def main():
     nnz = info0["nnz"]
     warm_steps = max(1, (cfg.n_samples // (B * world)))    # one epoch of linear-scaling warmup
 
+    # N > 1 (or SMLP_BENCH_DP=1 to exercise the same path on one GPU): unfused backward, per-layer
+    # allreduce of the grad view overlapped on the backward (OverlappedAllreduce), Eq. 1 update
+    dp_path = world > 1 or os.environ.get("SMLP_BENCH_DP") == "1"
+    overlap = OverlappedAllreduce(model) if dp_path else None
+
     def one_step(s):
         idx = idx_all[s * B:(s + 1) * B]
         lr = scaled_lr(cfg.lr, world, s, warm_steps)
         model.forward(X, x_idx=idx, train=True, step=s)
-        if world == 1:
+        if not dp_path:
             model.backward(Y, y_idx=idx, loss=loss, fused=SGD(lr, cfg.momentum, cfg.weight_decay))
         else:
             model.backward(Y, y_idx=idx, loss=loss, fused=None)
-            g, _ = model.grad_view()
-            allreduce_sum_(g)
+            if world > 1:
+                overlap()
+            else:
+                overlap(reduce=lambda t: None)               # one rank: the identity, same streams / events
             model.step(SGD(lr, cfg.momentum, cfg.weight_decay, 1.0 / world))
 
     for s in range(args.warmup):
@@ -350,6 +357,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": cfg.name, "stand_in_for": cfg.stand_in_for, "global_batch": B * world,
+                           "step_path": "dp: unfused bwd + per-layer overlapped allreduce + Eq.1 kernel" if dp_path
+                           else "1 GPU: Eq.1 fused into the backward",
                            "batch_per_rank": B, "layer_sizes": list(cfg.sizes), "epsilon": cfg.epsilon,
                            "nnz": sum(nnz), "chunk_batch": info0["chunk_batch"],
                            "parallelism": f"dp{world}", "l2_flush": "inputs larger than L2 (resident shard "

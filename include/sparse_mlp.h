@@ -186,6 +186,18 @@ int sparse_mlp_sync(smlp_handle* h);
 int sparse_mlp_grad_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version);
 int sparse_mlp_param_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version);
 
+/* sparse_mlp_wait_layer — makes `stream` (a cudaStream_t) wait until the last backward's
+ * gradient of W^(l) (and of b_{l-1}) is final, so that layer's slice of the grad view can be
+ * allreduced while the backward of the layers below continues (SURVEY §8(e) overlap; the
+ * output layer finishes first).  ASYNC.  Errors: SMLP_E_ARG (l not in [2, L]), SMLP_E_STATE
+ * (no backward ran yet). */
+int sparse_mlp_wait_layer(smlp_handle* h, int32_t l, void* stream);
+
+/* sparse_mlp_view_layout — where each layer lives in the grad / param views: host int64
+ * arrays val_off[L-1], cap[L-1] (index l-2 = W^(l), floats) and *bias_base (start of
+ * b_2 || ... || b_L, through the end of the view).  Any pointer may be NULL. */
+int sparse_mlp_view_layout(smlp_handle* h, int64_t* val_off, int64_t* cap, int64_t* bias_base);
+
 /* Call after writing the param view directly (e.g. the Eq. 2 averaging allreduce): refreshes
  * the forward's mirror-ordered copy of the weights.  Asynchronous, graph-capturable. */
 int sparse_mlp_params_updated(smlp_handle* h);

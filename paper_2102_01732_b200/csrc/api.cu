@@ -306,6 +306,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     if (const char* e = std::getenv("SMLP_MIRROR_SCATTER")) h->mirror_scatter = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_L2HINT")) h->l2hint = std::atoi(e);
     if (const char* e = std::getenv("SMLP_L2PERSIST")) h->l2persist = std::atoi(e);
+    if (const char* e = std::getenv("SMLP_FUSED_UPDATE")) h->fused_update = std::atoi(e) != 0;
     const int rc = build_handle(h, cfg);
     if (rc != SMLP_OK) {
         g_create_error = h->err;
@@ -326,6 +327,8 @@ int sparse_mlp_destroy(smlp_handle* h) {
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     for (auto& a : h->allocs) tmp_free(h, a.ptr, a.bytes);
     h->allocs.clear();
+    for (auto e : h->layer_ev)
+        if (e) cudaEventDestroy(e);
     for (int k = 0; k < 2; ++k) {
         if (h->ev_copied[k]) cudaEventDestroy(h->ev_copied[k]);
         if (h->ev_consumed[k]) cudaEventDestroy(h->ev_consumed[k]);
@@ -410,7 +413,20 @@ int sparse_mlp_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_
     if (!labels) return set_err(h, SMLP_E_ARG, "labels is NULL");
     if (!h->trace_valid || !h->trace_train || h->trace_version != h->version)
         return set_err(h, SMLP_E_STALE, "backward needs a train-mode forward on the current topology version");
-    const int rc = run_backward(h, labels, y_idx, loss, fused);
+    int rc;
+    if (fused && !h->fused_update) {
+        // measured faster than applying Eq. 1 inside the last chunk's backward: the
+        // backward only accumulates the gradient, then one streaming Eq. 1 pass over the whole
+        // view (grad_scale 1) and the mirror refresh
+        rc = run_backward(h, labels, y_idx, loss, nullptr);
+        if (rc == SMLP_OK) {
+            smlp_sgd f = *fused;
+            f.grad_scale = 1.f;
+            rc = run_step(h, &f);
+        }
+    } else {
+        rc = run_backward(h, labels, y_idx, loss, fused);
+    }
     if (rc == SMLP_OK) {
         h->grads_pending = fused == nullptr;
         h->trace_valid = false;   // the trace is consumed (and fused updates changed the weights)
@@ -478,6 +494,24 @@ int sparse_mlp_sync(smlp_handle* h) {
     if (!h) return SMLP_E_ARG;
     SMLP_CK(h, cudaStreamSynchronize(h->stream));
     return check_data_flag(h);
+}
+
+int sparse_mlp_wait_layer(smlp_handle* h, int32_t l, void* stream) {
+    if (!h || l < 2 || l > h->L) return SMLP_E_ARG;
+    if (!h->layer_ev[l]) return set_err(h, SMLP_E_STATE, "no backward recorded for this layer");
+    SMLP_CK(h, cudaStreamWaitEvent((cudaStream_t)stream, h->layer_ev[l], 0));
+    return SMLP_OK;
+}
+
+int sparse_mlp_view_layout(smlp_handle* h, int64_t* val_off, int64_t* cap, int64_t* bias_base) {
+    if (!h) return SMLP_E_ARG;
+    for (int l = 2; l <= h->L; ++l) {
+        const smlp::Layer& Ly = h->layers[l - 2];
+        if (val_off) val_off[l - 2] = Ly.val_off;
+        if (cap) cap[l - 2] = Ly.cap;
+    }
+    if (bias_base) *bias_base = h->bias_base;
+    return SMLP_OK;
 }
 
 int sparse_mlp_grad_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version) {

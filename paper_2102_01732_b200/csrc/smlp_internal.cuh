@@ -144,6 +144,7 @@ struct smlp_handle {
     cudaEvent_t ev_copied[2] = {nullptr, nullptr};
     cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
     int stage_idx = 0;
+    cudaEvent_t layer_ev[SMLP_MAX_LAYERS + 1] = {nullptr};   // W^(l) gradient final (unfused backward)
 
     // trace of the last forward
     bool trace_valid = false;
@@ -163,7 +164,8 @@ struct smlp_handle {
     int gather_evict_last = 0;
     int mirror_scatter = 0;
     int l2hint = 0;
-    int l2persist = 0;              // tuning knob (env SMLP_L2PERSIST, percent): persisting-L2 window on gathered slabs                 // tuning knob (env SMLP_L2HINT): L2 eviction policies in the row kernels         // tuning knob (env SMLP_MIRROR_SCATTER): fused update scatters into mval      // tuning knob (env SMLP_GATHER_EVICT_LAST): L2 policy of row gathers
+    int l2persist = 0;
+    int fused_update = 0;           // tuning knob (env SMLP_FUSED_UPDATE): Eq. 1 inside the last chunk's backward              // tuning knob (env SMLP_L2PERSIST, percent): persisting-L2 window on gathered slabs                 // tuning knob (env SMLP_L2HINT): L2 eviction policies in the row kernels         // tuning knob (env SMLP_MIRROR_SCATTER): fused update scatters into mval      // tuning knob (env SMLP_GATHER_EVICT_LAST): L2 policy of row gathers
     int64_t launches = 0;
     std::string err;
 };

@@ -2197,6 +2197,14 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
     return SMLP_OK;
 }
 
+// W^(l)'s gradient (and b_{l-1}'s) is final: record the layer event (sparse_mlp_wait_layer lets a
+// communication stream start that layer's allreduce while the backward continues)
+static int layer_done(smlp_handle* h, int l) {
+    if (!h->layer_ev[l]) SMLP_CK(h, cudaEventCreateWithFlags(&h->layer_ev[l], cudaEventDisableTiming));
+    SMLP_CK(h, cudaEventRecord(h->layer_ev[l], h->stream));
+    return SMLP_OK;
+}
+
 int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, const smlp_sgd* fused) {
     const int CB = h->CB;
     const int B = h->trace_B;
@@ -2267,6 +2275,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
                            (has_dprev ? 4.0 : 2.0) * nnz * Bc);
                 SMLP_TRY(dispatch_narrow(h, A, Ly, false));
                 prof_stop(h);
+                if (last) SMLP_TRY(layer_done(h, l));
                 continue;
             }
             BwdArgs A{};
@@ -2316,6 +2325,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
                 SMLP_TRY(refresh_mirror_values(h, Ly));
                 prof_stop(h);
             }
+            if (last) SMLP_TRY(layer_done(h, l));
         }
     }
     if (h->xbits) {   // binary-input layer 2 (returns at once if not binary)
@@ -2335,6 +2345,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             SMLP_TRY(refresh_mirror_values(h, L2));
             prof_stop(h);
         }
+        SMLP_TRY(layer_done(h, 2));
     }
     return SMLP_OK;
 }
@@ -2348,7 +2359,12 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
                                                        sgd->momentum, sgd->weight_decay, sgd->grad_scale);
     SMLP_CK_LAUNCH(h, "sgd_update_kernel");
     prof_stop(h);
-    for (auto& Ly : h->layers) SMLP_TRY(refresh_mirror_values(h, Ly));
+    for (auto& Ly : h->layers) {
+        if (Ly.narrow) continue;                                   // narrow layers never read the mirror copy
+        prof_start(h, K_MIRROR, Ly.l, 12.0 * (double)Ly.nnz, 0.0);
+        SMLP_TRY(refresh_mirror_values(h, Ly));
+        prof_stop(h);
+    }
     return SMLP_OK;
 }
 

@@ -103,3 +103,51 @@ def dp_train_step(model, X, Y, idx, step: int, lr: float, momentum: float, weigh
     g, _ = model.grad_view()
     allreduce_sum_(g, group)
     model.step(SGD(lr, momentum, weight_decay, 1.0 / world))
+
+
+class OverlappedAllreduce:
+    """X1 with the communication overlapped on the backward: after an UNFUSED
+    backward is enqueued, each layer's slice of the grad view is SUM-allreduced on a side stream as
+    soon as the library's per-layer event says that gradient is final -- the output layer first,
+    while the backward of the layers below is still running -- then the bias block; the caller's
+    stream waits for all of them before the Eq. 1 update.  Every rank issues the same collectives
+    in the same order (same topology and layout), so the reduction is the plain value allreduce."""
+
+    def __init__(self, model, group=None):
+        import torch
+        self.m = model
+        self.group = group
+        self.stream = torch.cuda.Stream(device=model.device) if torch.cuda.is_available() else None
+        self.layout, self.bias_base = model.view_layout()
+
+    def __call__(self, reduce=None):
+        """reduce(tensor_slice) -> work handle (default: torch.distributed.all_reduce SUM, async)."""
+        import torch
+        import torch.distributed as dist
+        if reduce is None:
+            def reduce(t):
+                return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        g, _ = self.m.grad_view()
+        works = []
+        main = torch.cuda.current_stream()
+        self.stream.wait_stream(main)                       # the grad view is not reused before this
+        with torch.cuda.stream(self.stream):
+            for l in range(self.m.L, 1, -1):                 # W^(L) is final first
+                self.m.wait_layer(l, self.stream)
+                off, cap = self.layout[l - 2]
+                works.append(reduce(g[off:off + cap]))
+            works.append(reduce(g[self.bias_base:]))         # b_2..b_L: final once W^(2)'s backward ran
+        for w in works:
+            if w is not None:
+                w.wait()                                     # the current stream waits for the collective
+        main.wait_stream(self.stream)
+
+
+def dp_train_step_overlapped(model, X, Y, idx, step: int, lr: float, momentum: float, weight_decay: float,
+                             world: int, overlap: "OverlappedAllreduce", loss=None):
+    """dp_train_step with the per-layer allreduce overlapped on the backward."""
+    from .sparse_mlp import SGD
+    model.forward(X, x_idx=idx, train=True, step=step)
+    model.backward(Y, y_idx=idx, loss=loss, fused=None)
+    overlap()
+    model.step(SGD(lr, momentum, weight_decay, 1.0 / world))

@@ -30,7 +30,7 @@ PRUNE_OUTGOING = 1
 EXPORTED = [
     "sparse_mlp_create", "sparse_mlp_destroy", "sparse_mlp_set_stream", "sparse_mlp_forward",
     "sparse_mlp_backward", "sparse_mlp_step", "sparse_mlp_train_step_host", "sparse_mlp_train_step_host_async",
-    "sparse_mlp_sync", "sparse_mlp_grad_view",
+    "sparse_mlp_sync", "sparse_mlp_wait_layer", "sparse_mlp_view_layout", "sparse_mlp_grad_view",
     "sparse_mlp_param_view", "sparse_mlp_evolve_topology", "sparse_mlp_prune_neurons",
     "sparse_mlp_importance", "sparse_mlp_info", "sparse_mlp_export_layer", "sparse_mlp_import_layer",
     "sparse_mlp_export_bias", "sparse_mlp_import_bias", "sparse_mlp_export_alive",
@@ -106,6 +106,8 @@ def load_library(path: str = LIB_PATH):
         "sparse_mlp_train_step_host": (I32, [VP, VP, VP, I32, U64, P(smlp_sgd), VP]),
         "sparse_mlp_train_step_host_async": (I32, [VP, VP, VP, I32, U64, P(smlp_sgd), VP]),
         "sparse_mlp_sync": (I32, [VP]),
+        "sparse_mlp_wait_layer": (I32, [VP, I32, VP]),
+        "sparse_mlp_view_layout": (I32, [VP, VP, VP, VP]),
         "sparse_mlp_grad_view": (I32, [VP, P(VP), P(I64), P(U64)]),
         "sparse_mlp_param_view": (I32, [VP, P(VP), P(I64), P(U64)]),
         "sparse_mlp_evolve_topology": (I32, [VP, D, U64, VP]),
@@ -260,6 +262,17 @@ class SparseMLP:
     def sparse_mlp_sync(self):
         self._check(self.lib.sparse_mlp_sync(self.h))
 
+    def sparse_mlp_wait_layer(self, l: int, stream):
+        """`stream` (torch.cuda.Stream) waits until W^(l)'s gradient of the last backward is final."""
+        self._check(self.lib.sparse_mlp_wait_layer(self.h, int(l), C.c_void_p(stream.cuda_stream)))
+
+    def sparse_mlp_view_layout(self):
+        """([(val_off, cap) for W^(2)..W^(L)], bias_base) in floats of the grad / param views."""
+        n = self.L - 1
+        off, cap, bb = (C.c_int64 * n)(), (C.c_int64 * n)(), C.c_int64()
+        self._check(self.lib.sparse_mlp_view_layout(self.h, off, cap, C.byref(bb)))
+        return [(int(off[i]), int(cap[i])) for i in range(n)], int(bb.value)
+
     def sparse_mlp_grad_view(self):
         p, n, v = C.c_void_p(), C.c_int64(), C.c_uint64()
         self._check(self.lib.sparse_mlp_grad_view(self.h, C.byref(p), C.byref(n), C.byref(v)))
@@ -393,6 +406,8 @@ class SparseMLP:
     param_view = sparse_mlp_param_view
     train_step_host = sparse_mlp_train_step_host
     train_step_host_async = sparse_mlp_train_step_host_async
+    wait_layer = sparse_mlp_wait_layer
+    view_layout = sparse_mlp_view_layout
     sync = sparse_mlp_sync
 
 

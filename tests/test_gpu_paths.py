@@ -272,3 +272,38 @@ def test_pipelined_host_step_matches_sync():
     for l in range(2, cfg.n_layers + 1):
         a, b = g1.export_layer(l), g2.export_layer(l)
         assert np.array_equal(a["w"].view(np.uint32), b["w"].view(np.uint32))
+
+
+def test_overlapped_dp_path_matches_fused_on_one_rank():
+    """The K > 1 step structure on one GPU: unfused backward, per-layer grad slices released by the
+    library's layer events to a side stream (identity 'allreduce'), Eq. 1 update kernel + mirror
+    refresh -- the same trajectory as the fused 1-GPU step (up to the update's rounding)."""
+    from paper_2102_01732_b200 import SGD, SparseMLPError
+    from paper_2102_01732_b200.dp import OverlappedAllreduce
+    torch = _torch()
+    cfg = _binary_cfg(batch=64, dropout=0.1)
+    g1, _ = pair(cfg, max_batch=64)
+    g2, _ = pair(cfg, max_batch=64)
+    side = torch.cuda.Stream()
+    with pytest.raises(SparseMLPError, match="E_STATE"):
+        g2.wait_layer(2, side)                            # no backward recorded yet
+    X, Y = _binary_data(3 * 64, cfg.sizes[0], seed=5)
+    ov = OverlappedAllreduce(g2)
+    layout, bb = g2.view_layout()
+    assert layout[0][0] == 0 and all(o2 >= o1 + c1 for (o1, c1), (o2, _) in zip(layout, layout[1:]))
+    seen = []
+    sgd = SGD(cfg.lr, cfg.momentum, cfg.weight_decay)
+    for s in range(3):
+        x, y = to_dev(X[s * 64:(s + 1) * 64]), to_dev(Y[s * 64:(s + 1) * 64])
+        g1.forward(x, train=True, step=s)
+        g1.backward(y, fused=sgd)
+        g2.forward(x, train=True, step=s)
+        g2.backward(y, fused=None)
+        ov(reduce=lambda t: seen.append(t.numel()))
+        g2.step(sgd)
+    torch.cuda.synchronize()
+    assert seen[:cfg.n_layers - 1] == [c for _, c in reversed(layout)]   # output layer first
+    for l in range(2, cfg.n_layers + 1):
+        a, b = g1.export_layer(l), g2.export_layer(l)
+        assert np.array_equal(a["col"], b["col"])
+        assert rel_err(b["w"], a["w"]) <= 1e-6, l
