@@ -337,6 +337,12 @@ int sparse_mlp_destroy(smlp_handle* h) {
         cudaStreamSynchronize(h->copy_stream);
         cudaStreamDestroy(h->copy_stream);
     }
+    if (h->aux_stream) {
+        cudaStreamSynchronize(h->aux_stream);
+        cudaStreamDestroy(h->aux_stream);
+    }
+    for (auto e : h->aux_ev)
+        if (e) cudaEventDestroy(e);
     cudaStreamSynchronize(h->stream);
     delete h;
     return SMLP_OK;

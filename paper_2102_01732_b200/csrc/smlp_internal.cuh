@@ -141,6 +141,8 @@ struct smlp_handle {
     float* x_stage[2] = {nullptr, nullptr};   // [max_batch x n_1] x2 for train_step_host (double-buffered)
     int32_t* y_stage[2] = {nullptr, nullptr};
     cudaStream_t copy_stream = nullptr;        // H2D of the next host batch, overlapping the current step
+    cudaStream_t aux_stream = nullptr;         // mirror refreshes overlapping the Eq. 1 pass (run_step)
+    cudaEvent_t aux_ev[2] = {nullptr, nullptr};
     cudaEvent_t ev_copied[2] = {nullptr, nullptr};
     cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
     int stage_idx = 0;

@@ -2351,20 +2351,42 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
 }
 
 int run_step(smlp_handle* h, const smlp_sgd* sgd) {
+    // Eq. 1 per layer slice on the handle's stream; each layer's mirror refresh (a gather, bound by
+    // L2 requests rather than HBM bytes) runs on a side stream as soon as that slice is updated, so
+    // it overlaps the next slice's streaming update
     const int threads = 256;
     const int64_t n = h->param_count;
-    const int grid = (int)std::min<int64_t>((n + threads - 1) / threads, (int64_t)h->num_sms * 16);
-    prof_start(h, K_SGD, 0, 20.0 * (double)n, 0.0);
-    sgd_update_kernel<<<grid, threads, 0, h->stream>>>(h->param, h->mom, h->grad, n, h->bias_base, sgd->lr,
-                                                       sgd->momentum, sgd->weight_decay, sgd->grad_scale);
-    SMLP_CK_LAUNCH(h, "sgd_update_kernel");
-    prof_stop(h);
-    for (auto& Ly : h->layers) {
-        if (Ly.narrow) continue;                                   // narrow layers never read the mirror copy
-        prof_start(h, K_MIRROR, Ly.l, 12.0 * (double)Ly.nnz, 0.0);
-        SMLP_TRY(refresh_mirror_values(h, Ly));
-        prof_stop(h);
+    if (!h->aux_stream) {
+        SMLP_CK(h, cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking));
+        for (auto& e : h->aux_ev) SMLP_CK(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
+    auto update = [&](int64_t lo, int64_t hi, bool decay) -> int {
+        if (hi <= lo) return SMLP_OK;
+        const int grid = (int)std::min<int64_t>((hi - lo + threads - 1) / threads, (int64_t)h->num_sms * 16);
+        sgd_update_kernel<<<grid, threads, 0, h->stream>>>(h->param + lo, h->mom + lo, h->grad + lo, hi - lo,
+                                                           decay ? hi - lo : 0, sgd->lr, sgd->momentum,
+                                                           sgd->weight_decay, sgd->grad_scale);
+        SMLP_CK_LAUNCH(h, "sgd_update_kernel");
+        return SMLP_OK;
+    };
+    prof_start(h, K_SGD, 0, 20.0 * (double)n, 0.0);
+    bool side = false;
+    for (auto& Ly : h->layers) {
+        SMLP_TRY(update(Ly.val_off, Ly.val_off + Ly.cap, true));
+        if (Ly.narrow) continue;                                   // narrow layers never read the mirror copy
+        SMLP_CK(h, cudaEventRecord(h->aux_ev[0], h->stream));
+        SMLP_CK(h, cudaStreamWaitEvent(h->aux_stream, h->aux_ev[0], 0));
+        mirror_values_kernel<<<launch_grid(h, Ly.cap, 256), 256, 0, h->aux_stream>>>(Ly.val, Ly.mperm, Ly.meta,
+                                                                                     Ly.mval);
+        SMLP_CK_LAUNCH(h, "mirror_values_kernel");
+        side = true;
+    }
+    SMLP_TRY(update(h->bias_base, n, false));                      // biases: no weight decay
+    if (side) {
+        SMLP_CK(h, cudaEventRecord(h->aux_ev[1], h->aux_stream));
+        SMLP_CK(h, cudaStreamWaitEvent(h->stream, h->aux_ev[1], 0));
+    }
+    prof_stop(h);
     return SMLP_OK;
 }
 
