@@ -301,8 +301,6 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
         h->has_allocator = true;
     }
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
-    if (const char* e = std::getenv("SMLP_GATHER_EVICT_LAST")) h->gather_evict_last = std::atoi(e) != 0;
-    if (const char* e = std::getenv("SMLP_KVER")) h->kver = std::atoi(e);
     if (const char* e = std::getenv("SMLP_MIRROR_SCATTER")) h->mirror_scatter = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_L2HINT")) h->l2hint = std::atoi(e);
     if (const char* e = std::getenv("SMLP_L2PERSIST")) h->l2persist = std::atoi(e);

@@ -162,10 +162,8 @@ struct smlp_handle {
     std::vector<smlp::ProfRec> prof_recs;
     std::vector<cudaEvent_t> ev_pool;
     int num_sms = 148;
-    int kver = 3;                   // tuning knob (env SMLP_KVER): 3 = warp-per-row kernels, 2 = group kernels
-    int gather_evict_last = 0;
     int mirror_scatter = 0;
-    int l2hint = 0;
+    int l2hint = 1;                 // tuning knob (env SMLP_L2HINT): L2 eviction policies in the row kernels (on: +0.4%)
     int l2persist = 0;
     int fused_update = 0;           // tuning knob (env SMLP_FUSED_UPDATE): Eq. 1 inside the last chunk's backward              // tuning knob (env SMLP_L2PERSIST, percent): persisting-L2 window on gathered slabs                 // tuning knob (env SMLP_L2HINT): L2 eviction policies in the row kernels         // tuning knob (env SMLP_MIRROR_SCATTER): fused update scatters into mval      // tuning knob (env SMLP_GATHER_EVICT_LAST): L2 policy of row gathers
     int64_t launches = 0;

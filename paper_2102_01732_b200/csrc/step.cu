@@ -1,24 +1,25 @@
 // step.cu — the per-minibatch hot path on sm_100a CUDA cores.
 //
 //   stage_input    a1  x[B x n_1] (optionally row-gathered by x_idx) -> act[1] chunked transposed
-//   fwd_kernel     a2/a3  z_l = a_{l-1} W^(l) + b_l over the output-major mirror.  A "group" of
-//                  G = CB/4 lanes owns one <= SEG_NNZ-entry segment of an output row (P = 32/G groups
-//                  per warp run in lock-step, predicated to the longest segment); each lane holds one
-//                  float4 of the CB batch columns; per block of G entries the group loads (src, w)
-//                  coalesced, broadcasts them by shuffle, and keeps G row gathers in flight (the next
-//                  block's indices are prefetched).  Epilogue: bias, All-ReLU (Eq. 3),
+//   fwd_rows_kernel a2/a3  z_l = a_{l-1} W^(l) + b_l over the output-major mirror: one warp per
+//                  <= SEG_NNZ-entry segment of an output row; G = CB/4 lanes hold one float4 of a
+//                  gathered activation row, the P = 32/G groups take interleaved entries of the same
+//                  row; the segment's (src, w) window is prefetched one segment ahead and staged in
+//                  shared memory, 8 gather slots per lane are in flight before the first FMA (padding
+//                  slots gather a zero row).  Epilogue: bias, All-ReLU (Eq. 3),
 //                  inverted dropout (Philox), sign / keep bit masks.
 //   fwd_finish     rows split into several segments: fixed-order sum of the partials + epilogue
 //   softmax_ce     a3  p = softmax(z_L), loss, delta_L = (p - onehot)/B, output-bias gradient
-//   bwd_kernel     a4/a5/a6  a group owns a segment of an input row i of the canonical CSR: per
-//                  entry it gathers delta_l[j] once, accumulates delta_{l-1}[i] += w_ij delta_l[j]
-//                  (SpMM against W^T) and the partial dot <a_{l-1}[i], delta_l[j]> (SDDMM); a
-//                  transpose reduction over the G lanes leaves lane q with the batch sum of entry q,
-//                  which it applies as the Eq. 1 update of (w, v) in place (1-GPU fused path) or
-//                  writes to the grad view; mirror_values then refreshes the forward's
-//                  mirror-ordered copy of w by a gather (a scatter would cost a sector read-fill)
+//   bwd_rows_kernel a4/a5  one warp per segment of an input row i of the canonical CSR: per
+//                  gathered delta_l[j] it accumulates delta_{l-1}[i] += w_ij delta_l[j] (SpMM against
+//                  W^T) and the lane's partial of <a_{l-1}[i], delta_l[j]> (SDDMM), reduced per entry
+//                  in a fixed order through shared memory; the gradient accumulates over chunks in the
+//                  grad view (or, with SMLP_FUSED_UPDATE, Eq. 1 is applied on the last chunk)
+//   bits kernels   W^(2) when every input is 0 or 1: bit-packed input, exact sums of w / of delta
+//   narrow kernels output layers with n_L <= 32: streamed canonical rows instead of gathers
 //   bwd_finish     multi-segment rows: fixed-order sum of the delta partials + epilogue
-//   sgd_update     a6 on the grad view after the caller's allreduce (K > 1), then mirror refresh
+//   sgd_update     a6 on the grad view (1 GPU: right after the backward; K > 1: after the allreduce),
+//                  per layer slice, with each layer's mirror refresh on a side stream
 //
 // Batch chunks: with CB < B the batch is processed in ceil(B/CB) chunk launches so the gathered
 // activation slab (n x CB fp32) stays L2-resident; gradients accumulate over chunks in order.
@@ -38,12 +39,6 @@ constexpr unsigned FULL = 0xffffffffu;
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 __device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
-__device__ __forceinline__ void fma4(float4& acc, float w, const float4& x) {
-    acc.x = fmaf(w, x.x, acc.x);
-    acc.y = fmaf(w, x.y, acc.y);
-    acc.z = fmaf(w, x.z, acc.z);
-    acc.w = fmaf(w, x.w, acc.w);
-}
 __device__ __forceinline__ float comp(const float4& v, int c) {
     return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
@@ -74,24 +69,12 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     return p;
 }
 // read-only for the whole kernel
-__device__ __forceinline__ int32_t ldro_i32(const int32_t* p, uint64_t pol) {
-    int32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ float ldro_f32(const float* p, uint64_t pol) {
-    float v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
-    return v;
-}
 __device__ __forceinline__ float4 ldro_f4(const float* p, uint64_t pol) {
     float4 v;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
     return v;
 }
-// gathered rows: read-only, L1 not allocated (no reuse within the SM), policy chosen by the caller
-__device__ __forceinline__ float4 ldg_row4(const float* p, uint64_t pol) { return ldro_f4(p, pol); }
 // read-write by the same thread within the kernel (coherent path)
 __device__ __forceinline__ float ldrw_f32(const float* p, uint64_t pol) {
     float v;
@@ -192,7 +175,6 @@ struct FwdArgs {
     const uint64_t* step_ptr; // device dropout-step source (graph replay) or null
     int b0;                   // global batch index of column 0 of this chunk
     const int32_t* skip_if_binary;   // layer 2 with the binary-input path: return if *flag == 0
-    int gather_evict_last;           // L2 policy of the gathered rows: evict_last (1) or normal (0)
     int zero_row;                    // row index (relative to a_prev) of the zero row after the last chunk
     int l2hint;                      // L2 policies: gathers evict_last, streamed operands evict_first
 };
@@ -238,72 +220,7 @@ __device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4
     }
 }
 
-// Gather-accumulate of one segment [beg, end) per group (groups in lock-step up to maxblk).
-template <int CB>
-__device__ __forceinline__ float4 fwd_segment(const FwdArgs& A, int beg, int end, int maxblk, int lane,
-                                              uint64_t pol_s, uint64_t pol_g) {
-    constexpr int G = CB / 4;
-    constexpr int U = G < 8 ? G : 8;
-    const int g = lane / G, q = lane % G, gbase = g * G;
-    float4 acc = f4zero();
-    int k = beg + q;
-    int src = 0;
-    float w = 0.f;
-    if (k < end) {
-        src = ldro_i32(A.msrc + k, pol_s);
-        w = ldro_f32(A.mval + k, pol_s);
-    }
-    for (int b = 0; b < maxblk; ++b) {
-        const int kn = k + G;                          // prefetch the next block's entries
-        int src_n = 0;
-        float w_n = 0.f;
-        if (kn < end) {
-            src_n = ldro_i32(A.msrc + kn, pol_s);
-            w_n = ldro_f32(A.mval + kn, pol_s);
-        }
-        const int base = beg + b * G;
-#pragma unroll
-        for (int u0 = 0; u0 < G; u0 += U) {
-            float4 x[U];
-            float wv[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int s = __shfl_sync(FULL, src, gbase + u0 + u);
-                wv[u] = __shfl_sync(FULL, w, gbase + u0 + u);
-                x[u] = (base + u0 + u < end) ? ldg_row4(A.a_prev + (int64_t)s * CB + q * 4, pol_g) : f4zero();
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) fma4(acc, wv[u], x[u]);
-        }
-        k = kn;
-        src = src_n;
-        w = w_n;
-    }
-    return acc;
-}
 
-template <int CB>
-__global__ void __launch_bounds__(256) fwd_kernel(FwdArgs A) {
-    constexpr int G = CB / 4, P = 32 / G;
-    if (A.skip_if_binary && *A.skip_if_binary == 0) return;
-    const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int nseg = A.meta->n_fseg;
-    const uint32_t step_lo = A.step_ptr ? (uint32_t)(*A.step_ptr) : A.step_lo;
-    const uint64_t pol_s = policy_evict_first();
-    const uint64_t pol_g = A.gather_evict_last ? policy_evict_last() : policy_evict_normal();
-    for (int s0 = warp * P; s0 < nseg; s0 += nwarps * P) {
-        const int s = s0 + g;
-        const bool active = s < nseg;
-        const int4 sg = active ? A.seg[s] : make_int4(0, 0, 0, -2);
-        const int nblk = (sg.z - sg.y + G - 1) / G;
-        const int maxblk = __reduce_max_sync(FULL, nblk);
-        const float4 acc = fwd_segment<CB>(A, sg.y, sg.z, maxblk, lane, pol_s, pol_g);
-        fwd_epilogue<CB>(A, sg.x, acc, active && sg.w < 0, lane, step_lo);
-        if (active && sg.w >= 0) st4(A.ws + (int64_t)sg.w * CB + q * 4, acc);
-    }
-}
 
 template <int CB>
 __global__ void __launch_bounds__(256) fwd_finish_kernel(FwdArgs A) {
@@ -396,11 +313,13 @@ __device__ __forceinline__ float4 group_allreduce(float4 v) {
 
 // cp.async (LDGSTS): global -> shared without a register destination, zero-filled when !valid
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, bool valid) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0) : "memory");
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, bool valid, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;" ::"r"(dst), "l"(src),
+                 "r"(valid ? 4 : 0), "l"(pol) : "memory");
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
+                 "r"(valid ? 16 : 0), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
@@ -411,13 +330,13 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // zero-filled and then pointed at the zero row after the last chunk (weight 0), so every gather
 // slot of a quad is unconditional.
 __device__ __forceinline__ void window_async(int2* win, const int32_t* __restrict__ idx, const float* __restrict__ wv,
-                                             int beg, int end, int lane) {
+                                             int beg, int end, int lane, uint64_t pol) {
 #pragma unroll
     for (int r = 0; r < SEG_NNZ / 32; ++r) {
         const int e = lane + 32 * r, k = beg + e;
         const bool ok = k < end;
-        cp_async4(smem_u32(&win[e].x), idx + (ok ? k : beg), ok);
-        cp_async4(smem_u32(&win[e].y), wv + (ok ? k : beg), ok);
+        cp_async4(smem_u32(&win[e].x), idx + (ok ? k : beg), ok, pol);
+        cp_async4(smem_u32(&win[e].y), wv + (ok ? k : beg), ok, pol);
     }
 }
 __device__ __forceinline__ void window_pad(int2* win, int n, int lane, int zero_row) {
@@ -697,7 +616,6 @@ struct BwdArgs {
     int fused;
     float lr, mu, wd;
     const int32_t* skip_if_binary;   // layer 2 with the binary-input path: return if *flag == 0
-    int gather_evict_last;           // L2 policy of the gathered rows: evict_last (1) or normal (0)
     int zero_row;                    // row index (relative to d_out) of the zero row after the last chunk
     int l2hint;                      // L2 policies: gathers evict_last, streamed operands evict_first
 };
@@ -741,94 +659,6 @@ __device__ __forceinline__ void bwd_epilogue(const BwdArgs& A, int64_t i, float4
     }
 }
 
-template <int CB, bool HAS_DPREV>
-__global__ void __launch_bounds__(256) bwd_kernel(BwdArgs A) {
-    constexpr int G = CB / 4, P = 32 / G;
-    if (A.skip_if_binary && *A.skip_if_binary == 0) return;
-    constexpr int U = G < 8 ? G : 8;
-    const int lane = threadIdx.x & 31;
-    const int g = lane / G, q = lane % G, gbase = g * G;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int nseg = A.meta->n_bseg;
-    const bool first_chunk = A.first != 0, last_chunk = A.last != 0;
-    const uint64_t pol_s = policy_evict_first();
-    const uint64_t pol_g = A.gather_evict_last ? policy_evict_last() : policy_evict_normal();
-    for (int s0 = warp * P; s0 < nseg; s0 += nwarps * P) {
-        const int s = s0 + g;
-        const bool active = s < nseg;
-        const int4 sg = active ? A.seg[s] : make_int4(0, 0, 0, -2);
-        const int64_t i = sg.x;
-        const int beg = sg.y, end = sg.z;
-        const int maxblk = __reduce_max_sync(FULL, (end - beg + G - 1) / G);
-        const float4 ai = active ? ldro_f4(A.a_prev + i * CB + q * 4, pol_s) : f4zero();
-        float4 dacc = f4zero();
-        int k = beg + q;
-        int jcol = 0;
-        float w = 0.f;
-        if (k < end) {
-            jcol = ldro_i32(A.col + k, pol_s);
-            w = ldrw_f32(A.val + k, pol_s);
-        }
-        for (int b = 0; b < maxblk; ++b) {
-            const int kn = k + G;                      // prefetch the next block's entries
-            int jcol_n = 0;
-            float w_n = 0.f;
-            if (kn < end) {
-                jcol_n = ldro_i32(A.col + kn, pol_s);
-                w_n = ldrw_f32(A.val + kn, pol_s);
-            }
-            const int base = beg + b * G;
-            float p[G];
-#pragma unroll
-            for (int u0 = 0; u0 < G; u0 += U) {
-                float4 dx[U];
-                float wv[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int jj = __shfl_sync(FULL, jcol, gbase + u0 + u);
-                    wv[u] = __shfl_sync(FULL, w, gbase + u0 + u);
-                    dx[u] = (base + u0 + u < end) ? ldg_row4(A.d_out + (int64_t)jj * CB + q * 4, pol_g) : f4zero();
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (HAS_DPREV) fma4(dacc, wv[u], dx[u]);
-                    p[u0 + u] = fmaf(ai.x, dx[u].x, fmaf(ai.y, dx[u].y, fmaf(ai.z, dx[u].z, ai.w * dx[u].w)));
-                }
-            }
-            // transpose reduction over the G lanes of the group: lane q ends with the batch sum
-            // of entry q of this block (= its own entry k)
-#pragma unroll
-            for (int h = G / 2; h >= 1; h >>= 1) {
-                const bool upper = (q & h) != 0;
-#pragma unroll
-                for (int u = 0; u < h; ++u) {
-                    const float send = upper ? p[u] : p[u + h];
-                    const float keep = upper ? p[u + h] : p[u];
-                    p[u] = keep + __shfl_xor_sync(FULL, send, h);
-                }
-            }
-            if (k < end) {
-                float gk = p[0];
-                if (!first_chunk) gk += ldrw_f32(A.grad + k, pol_s);
-                if (!last_chunk || !A.fused) {
-                    st_f32(A.grad + k, gk, pol_s);
-                } else {
-                    const float v = A.mu * ldrw_f32(A.mom + k, pol_s) - A.lr * (gk + A.wd * w);
-                    st_f32(A.mom + k, v, pol_s);
-                    st_f32(A.val + k, w + v, pol_s);
-                }
-            }
-            k = kn;
-            jcol = jcol_n;
-            w = w_n;
-        }
-        if (HAS_DPREV) {
-            bwd_epilogue<CB>(A, i, dacc, active && sg.w < 0, lane);
-            if (active && sg.w >= 0) st4(A.ws + (int64_t)sg.w * CB + q * 4, dacc);
-        }
-    }
-}
 
 template <int CB>
 __global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
@@ -1000,9 +830,9 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     const uint64_t pg = gather_policy(A.l2hint), ps = stream_policy(A.l2hint);
     // window + a_{l-1}[i] of a segment into buffer b (cp.async, one segment ahead: no registers held)
     auto prefetch = [&](const int4& sg, int b) {
-        window_async(win[b], A.col, A.val, sg.y, sg.z, lane);
+        window_async(win[b], A.col, A.val, sg.y, sg.z, lane, ps);
         if (lane < G) cp_async16(smem_u32(&ais[b][lane]), A.a_prev + (int64_t)(sg.w != -2 ? sg.x : 0) * CB + lane * 4,
-                                 sg.w != -2);
+                                 sg.w != -2, ps);
         cp_async_commit();
     };
     int4 cur = A.seg[s_lo];
@@ -1661,81 +1491,6 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
     }
 }
 
-template <int CB>
-__global__ void __launch_bounds__(256) bwd_bits_kernel(BitsArgs A) {
-    constexpr int G = CB / 4;
-    __shared__ float2 rec[WARPS_PER_BLOCK][32][XBITS_WORDS];
-    if (*A.nonbinary) return;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int g = lane / G, q = lane % G;
-    const bool colok = g < A.nchunks;
-    const int wsel = lane >> 3, sh = (lane * 4) & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t nunits = (A.n_out + BITS_ROWS - 1) / BITS_ROWS;
-    const uint4* xb4 = reinterpret_cast<const uint4*>(A.xbits);
-    auto dcol = [&](int64_t j) {
-        return (colok && j < A.n_out) ? ldg4(A.d_out + ((int64_t)g * A.n_out + j) * CB + q * 4) : f4zero();
-    };
-    for (int64_t u0 = warp; u0 < nunits; u0 += nwarps) {
-        const int64_t j0 = u0 * BITS_ROWS;
-        const int nrows = (int)(A.n_out - j0 < BITS_ROWS ? A.n_out - j0 : BITS_ROWS);
-        const int rp_l = __ldg(A.mrow_ptr + j0 + min(lane, nrows));       // lane t: start of local row t
-        const int E0 = __shfl_sync(FULL, rp_l, 0), E1 = __ldg(A.mrow_ptr + j0 + nrows);
-        int row = 0;
-        int row_end = nrows > 1 ? __shfl_sync(FULL, rp_l, 1) : E1;
-        float4 d = dcol(j0), d_next = dcol(j0 + 1);      // delta_2 of the current / next row
-        int k = E0 + lane;
-        int src = k < E1 ? __ldg(A.msrc + k) : 0;
-        for (int blk = E0; blk < E1; blk += 32) {
-            const int kn = k + 32;
-            const int src_n = kn < E1 ? __ldg(A.msrc + kn) : 0;
-            if (k < E1) {
-                const uint4 xb = __ldg(xb4 + src);
-                rec[wib][lane][0] = make_float2(0.f, __uint_as_float(xb.x));
-                rec[wib][lane][1] = make_float2(0.f, __uint_as_float(xb.y));
-                rec[wib][lane][2] = make_float2(0.f, __uint_as_float(xb.z));
-                rec[wib][lane][3] = make_float2(0.f, __uint_as_float(xb.w));
-            }
-            __syncwarp();
-            float p[32];
-#pragma unroll
-            for (int u = 0; u < 32; ++u) {
-                p[u] = 0.f;
-                if (blk + u < E1) {
-                    while (blk + u == row_end) {           // next row: its delta was prefetched
-                        ++row;
-                        d = d_next;
-                        d_next = dcol(j0 + row + 1);
-                        row_end = row + 1 <= 31 ? __shfl_sync(FULL, rp_l, row + 1) : E1;
-                    }
-                    const uint32_t bits = __float_as_uint(rec[wib][u][wsel].y) >> sh;
-                    float t = 0.f;
-                    if (bits & 1u) t += d.x;
-                    if (bits & 2u) t += d.y;
-                    if (bits & 4u) t += d.z;
-                    if (bits & 8u) t += d.w;
-                    p[u] = t;
-                }
-            }
-            __syncwarp();
-            // transpose reduction over the 32 lanes: lane u ends with the batch sum of entry u
-#pragma unroll
-            for (int hh = 16; hh >= 1; hh >>= 1) {
-                const bool upper = (lane & hh) != 0;
-#pragma unroll
-                for (int u = 0; u < hh; ++u) {
-                    const float send = upper ? p[u] : p[u + hh];
-                    const float keep = upper ? p[u + hh] : p[u];
-                    p[u] = keep + __shfl_xor_sync(FULL, send, hh);
-                }
-            }
-            if (k < E1) A.gmirror[k] = p[0];
-            k = kn;
-            src = src_n;
-        }
-    }
-}
 
 // Backward of the binary-input layer, one lane per mirror entry (i -> j): since x[b, i] is 0 or 1,
 // g_ij = sum_b x[b, i] delta_2[b, j] is the sum of delta_2[b, j] over the SET bits b of input
@@ -1869,14 +1624,8 @@ int rows_grid(const smlp_handle* h, K kernel, int64_t segs) {
 template <int CB>
 int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
     constexpr int P = 32 / (CB / 4);
-    if (h->kver >= 3) {
-        fwd_rows_kernel<CB><<<rows_grid(h, fwd_rows_kernel<CB>, L.fseg_cap), WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
-        SMLP_CK_LAUNCH(h, "fwd_rows_kernel");
-    } else {
-        const int grid = persistent_grid(h, L.fseg_cap, P);
-        fwd_kernel<CB><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
-        SMLP_CK_LAUNCH(h, "fwd_kernel");
-    }
+    fwd_rows_kernel<CB><<<rows_grid(h, fwd_rows_kernel<CB>, L.fseg_cap), WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+    SMLP_CK_LAUNCH(h, "fwd_rows_kernel");
     if (L.fslot_cap > 0) {
         const int g2 = persistent_grid(h, std::max<int64_t>(1, L.fslot_cap / 2), P);
         fwd_finish_kernel<CB><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
@@ -1888,40 +1637,30 @@ int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
 template <int CB>
 int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev) {
     constexpr int P = 32 / (CB / 4);
-    if (h->kver >= 3) {
-        const bool gold = !A.first, upd = A.last && A.fused, drop = A.dropout_prev != 0;
-        const int mode = (has_dprev ? 8 : 0) | (gold ? 4 : 0) | (upd ? 2 : 0) | (drop ? 1 : 0);
+    const bool gold = !A.first, upd = A.last && A.fused, drop = A.dropout_prev != 0;
+    const int mode = (has_dprev ? 8 : 0) | (gold ? 4 : 0) | (upd ? 2 : 0) | (drop ? 1 : 0);
 #define SMLP_BWD_ROWS(HD, GO, UP, DR)                                                                          \
-    case (HD ? 8 : 0) | (GO ? 4 : 0) | (UP ? 2 : 0) | (DR ? 1 : 0):                                         \
-        bwd_rows_kernel<CB, HD, GO, UP, DR><<<rows_grid(h, bwd_rows_kernel<CB, HD, GO, UP, DR>, L.bseg_cap),      \
-                                              WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);                      \
-        break;
-        switch (mode) {
-            SMLP_BWD_ROWS(true, false, false, false)
-            SMLP_BWD_ROWS(true, false, false, true)
-            SMLP_BWD_ROWS(true, false, true, false)
-            SMLP_BWD_ROWS(true, false, true, true)
-            SMLP_BWD_ROWS(true, true, false, false)
-            SMLP_BWD_ROWS(true, true, false, true)
-            SMLP_BWD_ROWS(true, true, true, false)
-            SMLP_BWD_ROWS(true, true, true, true)
-            SMLP_BWD_ROWS(false, false, false, false)
-            SMLP_BWD_ROWS(false, false, true, false)
-            SMLP_BWD_ROWS(false, true, false, false)
-            SMLP_BWD_ROWS(false, true, true, false)
-            default: return set_err(h, SMLP_E_ARG, "bwd_rows_kernel: bad mode");
-        }
-#undef SMLP_BWD_ROWS
-        SMLP_CK_LAUNCH(h, "bwd_rows_kernel");
-    } else {
-        const int grid = persistent_grid(h, L.bseg_cap, P);
-        if (has_dprev) {
-            bwd_kernel<CB, true><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
-        } else {
-            bwd_kernel<CB, false><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
-        }
-        SMLP_CK_LAUNCH(h, "bwd_kernel");
+case (HD ? 8 : 0) | (GO ? 4 : 0) | (UP ? 2 : 0) | (DR ? 1 : 0):                                         \
+    bwd_rows_kernel<CB, HD, GO, UP, DR><<<rows_grid(h, bwd_rows_kernel<CB, HD, GO, UP, DR>, L.bseg_cap),      \
+                                          WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);                      \
+    break;
+    switch (mode) {
+        SMLP_BWD_ROWS(true, false, false, false)
+        SMLP_BWD_ROWS(true, false, false, true)
+        SMLP_BWD_ROWS(true, false, true, false)
+        SMLP_BWD_ROWS(true, false, true, true)
+        SMLP_BWD_ROWS(true, true, false, false)
+        SMLP_BWD_ROWS(true, true, false, true)
+        SMLP_BWD_ROWS(true, true, true, false)
+        SMLP_BWD_ROWS(true, true, true, true)
+        SMLP_BWD_ROWS(false, false, false, false)
+        SMLP_BWD_ROWS(false, false, true, false)
+        SMLP_BWD_ROWS(false, true, false, false)
+        SMLP_BWD_ROWS(false, true, true, false)
+        default: return set_err(h, SMLP_E_ARG, "bwd_rows_kernel: bad mode");
     }
+#undef SMLP_BWD_ROWS
+    SMLP_CK_LAUNCH(h, "bwd_rows_kernel");
     if (has_dprev && L.bslot_cap > 0) {
         const int g2 = persistent_grid(h, std::max<int64_t>(1, L.bslot_cap / 2), P);
         bwd_finish_kernel<CB><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
@@ -2056,15 +1795,12 @@ int launch_bits(smlp_handle* h, const BitsArgs& A, const Layer& L2, bool fwd) {
             fwd_bits_kernel<CB, false><<<rows_grid(h, fwd_bits_kernel<CB, false>, units), WARPS_PER_BLOCK * 32, 0,
                                          h->stream>>>(A);
         SMLP_CK_LAUNCH(h, "fwd_bits_kernel");
-    } else if (h->kver >= 3) {
+    } else {
         const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((L2.n_out + 8 * WARPS_PER_BLOCK - 1) /
                                                                      (8 * WARPS_PER_BLOCK),
                                                                  (int64_t)h->num_sms * 8));
         bwd_bits_rows_kernel<CB><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
         SMLP_CK_LAUNCH(h, "bwd_bits_rows_kernel");
-    } else {
-        bwd_bits_kernel<CB><<<grid, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
-        SMLP_CK_LAUNCH(h, "bwd_bits_kernel");
     }
     return SMLP_OK;
 }
@@ -2178,7 +1914,6 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             A.step_ptr = h->step_counter;
             A.b0 = c * CB;
             A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
-            A.gather_evict_last = h->gather_evict_last;
             A.zero_row = (int)((int64_t)(h->max_chunks - c) * nin);
             A.l2hint = h->l2hint;
             prof_start(h, K_FWD, l, 12.0 * nnz / nchunks + 4.0 * Bc * (double)(nin + nout), 2.0 * nnz * Bc);
@@ -2308,10 +2043,9 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.mu = mu;
             A.wd = wd;
             A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
-            A.gather_evict_last = h->gather_evict_last;
             A.zero_row = (int)((int64_t)(h->max_chunks - c) * nout);
             A.l2hint = h->l2hint;
-            A.mval_scatter = (h->mirror_scatter && h->kver >= 3 && !(l == 2 && h->xbits)) ? 1 : 0;
+            A.mval_scatter = (h->mirror_scatter && !(l == 2 && h->xbits)) ? 1 : 0;
             prof_start(h, K_BWD, l, (is_fused ? 20.0 : 12.0) * nnz / nchunks + act_bytes,
                        (has_dprev ? 4.0 : 2.0) * nnz * Bc);
             l2_window(h, A.d_out, (size_t)nout * CB * sizeof(float));
