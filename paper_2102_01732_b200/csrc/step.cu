@@ -1472,14 +1472,18 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
                 while (blk + u == row_end && row < nrows) finish_row();
                 if (u >= n) break;
                 const int stop = min(n, row_end - blk);
+                float2 alo = make_float2(acc.x, acc.y), ahi = make_float2(acc.z, acc.w);
+                const char* rp = reinterpret_cast<const char*>(myrec);
+                const char* lp = reinterpret_cast<const char*>(lut);
+#pragma unroll 4
                 for (; u < stop; ++u) {
-                    const float2 r = myrec[u * XBITS_WORDS];
+                    const float2 r = *reinterpret_cast<const float2*>(rp + u * (XBITS_WORDS * 8));
                     // x in {0, 1}: fmaf(w, x, acc) is acc + w for x = 1 and acc for x = 0, bit for bit
-                    const float4 m = lut[(__float_as_uint(r.y) >> sh) & 15u];
-                    const float2 lo = ffma2(make_float2(r.x, r.x), make_float2(m.x, m.y), make_float2(acc.x, acc.y));
-                    const float2 hi = ffma2(make_float2(r.x, r.x), make_float2(m.z, m.w), make_float2(acc.z, acc.w));
-                    acc = make_float4(lo.x, lo.y, hi.x, hi.y);
+                    const float4 m = *reinterpret_cast<const float4*>(lp + (((__float_as_uint(r.y) >> sh) & 15u) << 4));
+                    alo = ffma2(make_float2(r.x, r.x), make_float2(m.x, m.y), alo);
+                    ahi = ffma2(make_float2(r.x, r.x), make_float2(m.z, m.w), ahi);
                 }
+                acc = make_float4(alo.x, alo.y, ahi.x, ahi.y);
             }
             __syncwarp();
             w = w_n;
