@@ -186,6 +186,14 @@ int sparse_mlp_sync(smlp_handle* h);
 int sparse_mlp_grad_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version);
 int sparse_mlp_param_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version);
 
+/* sparse_mlp_gradient_flow — PAPER.md:315 ("the first-order approximation of the decrease in
+ * the loss expected after a gradient step"): the squared L2 norm of the
+ * pending gradient of an unfused backward, sum over W^(2..L) of sum g^2 over the existing
+ * connections plus sum gb^2 over the biases, accumulated in fp64 in a fixed order
+ * (deterministic).  *out_host: host double.  SYNC.  Errors: SMLP_E_STATE if no unfused
+ * backward's gradient is pending. */
+int sparse_mlp_gradient_flow(smlp_handle* h, double* out_host);
+
 /* sparse_mlp_wait_layer — makes `stream` (a cudaStream_t) wait until the last backward's
  * gradient of W^(l) (and of b_{l-1}) is final, so that layer's slice of the grad view can be
  * allreduced while the backward of the layers below continues (SURVEY §8(e) overlap; the

@@ -385,3 +385,17 @@ def train_step(st: State, x, y, lr, momentum, weight_decay, step_idx: int = 0):
     gr = backward(st, tr, y)
     step(st, gr, lr, momentum, weight_decay)
     return gr.loss, tr, gr
+
+
+def gradient_flow(grads: Grads) -> float:
+    """Gradient flow ("the first-order approximation of the decrease in the loss
+    expected after a gradient step"): the squared L2 norm of the whole
+    gradient, sum over layers of sum g_ij^2 over the existing connections plus sum gb^2 over the
+    biases.  Each fp32 gradient value is squared and summed in float64 (a plain definition: the
+    order of the float64 sum is the only freedom)."""
+    tot = 0.0
+    for g in grads.g:
+        tot += float(np.sum(np.square(g.astype(F64))))
+    for gb in grads.gb:
+        tot += float(np.sum(np.square(gb.astype(F64))))
+    return tot

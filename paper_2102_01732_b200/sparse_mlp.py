@@ -30,7 +30,7 @@ PRUNE_OUTGOING = 1
 EXPORTED = [
     "sparse_mlp_create", "sparse_mlp_destroy", "sparse_mlp_set_stream", "sparse_mlp_forward",
     "sparse_mlp_backward", "sparse_mlp_step", "sparse_mlp_train_step_host", "sparse_mlp_train_step_host_async",
-    "sparse_mlp_sync", "sparse_mlp_wait_layer", "sparse_mlp_view_layout", "sparse_mlp_grad_view",
+    "sparse_mlp_sync", "sparse_mlp_gradient_flow", "sparse_mlp_wait_layer", "sparse_mlp_view_layout", "sparse_mlp_grad_view",
     "sparse_mlp_param_view", "sparse_mlp_evolve_topology", "sparse_mlp_prune_neurons",
     "sparse_mlp_importance", "sparse_mlp_info", "sparse_mlp_export_layer", "sparse_mlp_import_layer",
     "sparse_mlp_export_bias", "sparse_mlp_import_bias", "sparse_mlp_export_alive",
@@ -106,6 +106,7 @@ def load_library(path: str = LIB_PATH):
         "sparse_mlp_train_step_host": (I32, [VP, VP, VP, I32, U64, P(smlp_sgd), VP]),
         "sparse_mlp_train_step_host_async": (I32, [VP, VP, VP, I32, U64, P(smlp_sgd), VP]),
         "sparse_mlp_sync": (I32, [VP]),
+        "sparse_mlp_gradient_flow": (I32, [VP, VP]),
         "sparse_mlp_wait_layer": (I32, [VP, I32, VP]),
         "sparse_mlp_view_layout": (I32, [VP, VP, VP, VP]),
         "sparse_mlp_grad_view": (I32, [VP, P(VP), P(I64), P(U64)]),
@@ -262,6 +263,13 @@ class SparseMLP:
     def sparse_mlp_sync(self):
         self._check(self.lib.sparse_mlp_sync(self.h))
 
+    def sparse_mlp_gradient_flow(self) -> float:
+        """Squared L2 norm of the pending (unfused) gradient."""
+        self._sync_stream()
+        out = C.c_double(0.0)
+        self._check(self.lib.sparse_mlp_gradient_flow(self.h, C.byref(out)))
+        return float(out.value)
+
     def sparse_mlp_wait_layer(self, l: int, stream):
         """`stream` (torch.cuda.Stream) waits until W^(l)'s gradient of the last backward is final."""
         self._check(self.lib.sparse_mlp_wait_layer(self.h, int(l), C.c_void_p(stream.cuda_stream)))
@@ -407,6 +415,7 @@ class SparseMLP:
     train_step_host = sparse_mlp_train_step_host
     train_step_host_async = sparse_mlp_train_step_host_async
     wait_layer = sparse_mlp_wait_layer
+    gradient_flow = sparse_mlp_gradient_flow
     view_layout = sparse_mlp_view_layout
     sync = sparse_mlp_sync
 

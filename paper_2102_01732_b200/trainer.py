@@ -158,3 +158,40 @@ class Trainer:
 
     def fit(self, epochs: int) -> List[EpochRecord]:
         return [self.train_epoch(e, last=(e == epochs - 1)) for e in range(epochs)]
+
+
+# ---------------------------------------------------------------------------------- post-training
+def evaluate(model: SparseMLP, X, Y, batch: int) -> float:
+    """Test accuracy: inference forward (no dropout) in batches of <= batch rows, argmax of p."""
+    import torch
+    n = X.shape[0]
+    correct = 0
+    probs = torch.empty((batch, model.sizes[-1]), dtype=torch.float32, device=X.device)
+    for s in range(0, n, batch):
+        b = min(batch, n - s)
+        model.forward(X[s:s + b], train=False, probs=probs)
+        correct += int((probs[:b].argmax(1) == Y[s:s + b].long()).sum().item())
+    return correct / n
+
+
+def prune_sweep(model: SparseMLP, X, Y, batch: int, percentiles=(5.0, 10.0, 15.0, 20.0, 25.0)):
+    """Importance Pruning applied ONCE after training (Supp. C, Table of
+    post-training pruning): for every threshold percentile rho, prune the
+    trained model's hidden neurons with sparse_mlp_prune_neurons, record the test accuracy and the
+    number of remaining connections, then restore the trained model.  Each rho starts from the
+    same trained model (one-shot, not cumulative).  Returns [(rho, accuracy, connections)] plus
+    the unpruned (None, accuracy, connections) first."""
+    L = model.L
+    snap = {l: (model.export_layer(l), model.sparse_mlp_export_bias(l)) for l in range(2, L + 1)}
+    alive = {l: model.sparse_mlp_export_alive(l) for l in range(1, L + 1)}
+    out = [(None, evaluate(model, X, Y, batch), int(sum(model.info()["nnz"])))]
+    for rho in percentiles:
+        model.prune_neurons(float(rho))
+        out.append((float(rho), evaluate(model, X, Y, batch), int(sum(model.info()["nnz"]))))
+        for l in range(2, L + 1):                      # restore the trained model
+            e, (b, vb) = snap[l]
+            model.import_layer(l, e["row_ptr"], e["col"], e["w"], e["v"])
+            model.sparse_mlp_import_bias(l, b, vb)
+        for l in range(1, L + 1):
+            model.sparse_mlp_import_alive(l, alive[l])
+    return out

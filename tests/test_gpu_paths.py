@@ -14,7 +14,7 @@ import pytest
 
 from oracle import model as M
 from oracle.compare import rel_err
-from synth import get_config
+from synth import get_config, make_dataset
 from tests.gpu_helpers import TOL, assert_topology_equal, assert_values_close, pair, to_dev
 
 pytestmark = pytest.mark.gpu
@@ -307,3 +307,66 @@ def test_overlapped_dp_path_matches_fused_on_one_rank():
         a, b = g1.export_layer(l), g2.export_layer(l)
         assert np.array_equal(a["col"], b["col"])
         assert rel_err(b["w"], a["w"]) <= 1e-6, l
+
+
+@pytest.mark.parametrize("cfg_name", ["C1", "C2"])
+def test_gradient_flow_parity(cfg_name):
+    """sparse_mlp_gradient_flow against oracle.model.gradient_flow on the same
+    unfused backward; deterministic (two calls give the same bits); E_STATE without pending
+    gradients."""
+    from paper_2102_01732_b200 import SparseMLPError
+    torch = _torch()
+    cfg = get_config(cfg_name, dropout=0.0)
+    g, st = pair(cfg)
+    rng = np.random.default_rng(17)
+    X = rng.standard_normal((cfg.batch, cfg.sizes[0])).astype(np.float32)
+    Y = rng.integers(0, cfg.sizes[-1], cfg.batch).astype(np.int32)
+    with pytest.raises(SparseMLPError, match="E_STATE"):
+        g.gradient_flow()
+    g.forward(to_dev(X), train=True, step=0)
+    g.backward(to_dev(Y), fused=None)
+    f1, f2 = g.gradient_flow(), g.gradient_flow()
+    torch.cuda.synchronize()
+    tr = M.forward(st, X, True, 0)
+    gr = M.backward(st, tr, Y)
+    ref = M.gradient_flow(gr)
+    assert f1 == f2
+    assert abs(f1 - ref) <= 3e-4 * ref, (f1, ref)
+
+
+def test_post_training_prune_sweep_parity():
+    """Supp. C: one-shot Importance Pruning of a trained model at rho =
+    5..25.  Every sweep point equals the oracle's prune of the same trained state: identical
+    remaining connection counts (bit-exact topology decision) and the same test accuracy up to
+    arg-max ties; the trained model is restored after each point."""
+    from oracle import topology as T
+    from paper_2102_01732_b200 import SGD
+    from paper_2102_01732_b200.trainer import prune_sweep
+    torch = _torch()
+    cfg = get_config("C1", dropout=0.0)
+    g, st = pair(cfg)
+    X, Y = make_dataset(cfg, n=6 * cfg.batch)
+    sgd = SGD(cfg.lr * 10, cfg.momentum, cfg.weight_decay)
+    for s in range(4):                                   # a short training run, oracle in lockstep
+        x, y = X[s * cfg.batch:(s + 1) * cfg.batch], Y[s * cfg.batch:(s + 1) * cfg.batch]
+        g.forward(to_dev(x), train=True, step=s)
+        g.backward(to_dev(y.astype(np.int32)), fused=sgd)
+        M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, s)
+    torch.cuda.synchronize()
+    for Ly in st.layers:                                 # identical trained state on both sides
+        g.import_layer(Ly.l, Ly.row_ptr.astype(np.int32), Ly.col, Ly.w, Ly.v)
+        g.sparse_mlp_import_bias(Ly.l, st.b[Ly.l - 2], st.vb[Ly.l - 2])
+    Xt, Yt = to_dev(X[4 * cfg.batch:]), to_dev(Y[4 * cfg.batch:].astype(np.int32))
+    sweep = prune_sweep(g, Xt, Yt, cfg.batch)
+    assert sweep[0][0] is None and sweep[0][2] == sum(len(L.w) for L in st.layers)
+    xt, yt = X[4 * cfg.batch:], Y[4 * cfg.batch:]
+    import copy
+    for rho, acc, conns in sweep[1:]:
+        so = copy.deepcopy(st)
+        T.prune(so, rho)
+        assert conns == sum(len(L.w) for L in so.layers), rho
+        p = M.forward(so, xt, False, 0).p
+        acc_o = float(np.mean(np.argmax(p, 1) == yt))
+        assert abs(acc - acc_o) <= 2.0 / len(yt), (rho, acc, acc_o)
+    e = g.export_layer(3)                                # restored after the sweep
+    assert np.array_equal(e["col"], st.layers[1].col) and np.array_equal(e["w"], st.layers[1].w)

@@ -364,3 +364,28 @@ def test_kink_guard_ignores_exact_zero_preactivations():
     x = np.zeros((8, 40), np.float32)
     tr = M.forward(st, x, True, 0)
     assert np.all(tr.z[1] == 0) and sum(tr.ambiguous) == 0
+
+
+# ---------------------------------------------------------------- gradient flow (§8(f) item 2)
+def test_gradient_flow_pins():
+    """PAPER.md:315 / SPEC S:187-195: the squared L2 norm of all existing-weight and bias
+    gradients.  Pins: zero gradients -> 0; a single entry 3 -> 9; equals the dense-masked
+    reference's squared gradient norm (independent fp64 backprop) on a small network."""
+    st = M.create((7, 6, 5, 3), 3.0, "all_relu", 0.4, 0.0, "he_uniform", 13)
+    z = M.Grads([np.zeros_like(L.w) for L in st.layers], [np.zeros_like(b) for b in st.b], 0.0, [])
+    assert M.gradient_flow(z) == 0.0
+    one = M.Grads([np.zeros_like(L.w) for L in st.layers], [np.zeros_like(b) for b in st.b], 0.0, [])
+    one.g[1][2] = 3.0
+    assert M.gradient_flow(one) == 9.0
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((9, 7)).astype(np.float32)
+    y = rng.integers(0, 3, 9)
+    tr = M.forward(st, x, True, 0)
+    gr = M.backward(st, tr, y)
+    Ws = [Ly.dense(np.float64) for Ly in st.layers]
+    bs = [b.astype(np.float64) for b in st.b]
+    _, _, dWs, dbs = dense_ref.forward_backward(Ws, bs, x.astype(np.float64), y, 0.4, "all_relu")
+    # the masked dense gradient restricted to the support (off-support entries are not parameters)
+    ref = sum(float(np.sum(np.square(dWs[k][Ly.rows(), Ly.col]))) for k, Ly in enumerate(st.layers))
+    ref += sum(float(np.sum(np.square(b))) for b in dbs)
+    assert abs(M.gradient_flow(gr) - ref) <= 1e-4 * ref
