@@ -194,6 +194,23 @@ int sparse_mlp_param_view(smlp_handle* h, float** dev, int64_t* count, uint64_t*
  * backward's gradient is pending. */
 int sparse_mlp_gradient_flow(smlp_handle* h, double* out_host);
 
+/* sparse_mlp_export_positions — the entries of W^(l) in canonical order as device arrays:
+ * pos_dev[k] = i * n_l + j (uint64), val_dev[k] = w_ij; both caller-owned device buffers of at
+ * least nnz(W^(l)) elements (sparse_mlp_info).  ASYNC.  Used to all-gather replicas' supports. */
+int sparse_mlp_export_positions(smlp_handle* h, int32_t l, uint64_t* pos_dev, float* val_dev);
+
+/* sparse_mlp_union_average_layer — WASAP phase-2 averaging (Alg. 1, Eq. 2
+ * PAPER.md:94-96, re-sparsification PAPER.md:97-98) of W^(l) over the
+ * UNION of K replicas' supports.  pos_all / val_all: device arrays of `total` entries, the K
+ * replicas' sparse_mlp_export_positions lists concatenated in rank order.  Per distinct position:
+ * fp32 sum of the present values in rank order, / K in fp32 (absent = 0; DESIGN R31); then the
+ * union entries closest to zero are removed (key |w| bits, ties by position) down to `target`
+ * connections; the rest become W^(l) with momentum 0.  Deterministic, so replicas that pass the
+ * same inputs end bit-identical.  *kept (host, may be NULL) = min(target, union size).
+ * version += 1.  SYNC.  Errors: SMLP_E_ARG (l, K < 1, target > capacity), SMLP_E_NOMEM. */
+int sparse_mlp_union_average_layer(smlp_handle* h, int32_t l, int32_t K, const uint64_t* pos_all,
+                                   const float* val_all, int64_t total, int64_t target, int64_t* kept);
+
 /* sparse_mlp_wait_layer — makes `stream` (a cudaStream_t) wait until the last backward's
  * gradient of W^(l) (and of b_{l-1}) is final, so that layer's slice of the grad view can be
  * allreduced while the backward of the layers below continues (SURVEY §8(e) overlap; the

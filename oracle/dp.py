@@ -62,3 +62,59 @@ def average(states: List[State]) -> None:
         for s in states:
             s.layers[idx].w = w.copy()
             s.b[idx] = b.copy()
+
+
+def average_union(states: List[State], targets: Sequence[int]) -> List[int]:
+    """WASAP phase-2 averaging (Alg. 1 PAPER.md:616-629; Eq. 2 PAPER.md:94-96; SPEC S:282-290;
+    SURVEY.md §8(f) item 1) of K replicas whose topologies evolved independently, written out per
+    layer exactly as the paper states it: the averaged support is the union of the K supports,
+    each union entry's value is (sum over replicas of its value, absent = 0) / K, and then the
+    connections closest to zero are pruned ("unimportant connections ... the largest negative
+    weights and the smallest positive weights") down to targets[l-2] (the
+    pre-phase-2 count).
+    Arithmetic (DESIGN reading R31, shared with the CUDA path because it decides which entries
+    survive): the sum is taken in float32 over the PRESENT values in rank order, then divided by
+    K in float32; removal order is (|w| bit pattern, position) ascending.  Momentum of the
+    averaged model is 0; biases are averaged (sum in rank order in float64, / K, rounded once).
+    Every state is replaced by the averaged model.  Returns the kept count per layer."""
+    K = len(states)
+    L = states[0].L
+    kept = []
+    new_layers = []
+    for idx in range(L - 1):
+        lays = [s.layers[idx] for s in states]
+        n_in, n_out = lays[0].n_in, lays[0].n_out
+        vals = {}
+        for Ly in lays:                                   # rank order
+            pos = Ly.rows().astype(np.uint64) * np.uint64(n_out) + Ly.col.astype(np.uint64)
+            for p, w in zip(pos.tolist(), Ly.w.tolist()):
+                w32 = np.float32(w)
+                vals[p] = w32 if p not in vals else np.float32(vals[p] + w32)
+        upos = np.array(sorted(vals), dtype=np.uint64)
+        uval = np.array([np.float32(vals[int(p)]) / np.float32(K) for p in upos], dtype=F32)
+        U = len(upos)
+        keep_n = min(U, int(targets[idx]))
+        keys = (uval.view(np.uint32).astype(np.uint64) & np.uint64(0x7fffffff)) << np.uint64(32)
+        keys |= np.arange(U, dtype=np.uint64)
+        order = np.argsort(keys, kind="stable")
+        keep = np.ones(U, bool)
+        keep[order[:U - keep_n]] = False
+        kp, kv = upos[keep], uval[keep]
+        rows = (kp // np.uint64(n_out)).astype(np.int64)
+        cols = (kp % np.uint64(n_out)).astype(np.int32)
+        row_ptr = np.zeros(n_in + 1, np.int64)
+        np.add.at(row_ptr, rows + 1, 1)
+        new_layers.append((np.cumsum(row_ptr), cols, kv.astype(F32)))
+        kept.append(keep_n)
+    b_avg = [(np.sum([s.b[i].astype(F64) for s in states], axis=0) / K).astype(F32) for i in range(L - 1)]
+    for s in states:
+        for idx, (rp, cols, w) in enumerate(new_layers):
+            Ly = s.layers[idx]
+            Ly.row_ptr = rp.copy()
+            Ly.col = cols.copy()
+            Ly.w = w.copy()
+            Ly.v = np.zeros_like(w)
+            s.b[idx] = b_avg[idx].copy()
+            s.vb[idx] = np.zeros_like(s.vb[idx])
+        s.version += 1
+    return kept

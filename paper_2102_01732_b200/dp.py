@@ -151,3 +151,41 @@ def dp_train_step_overlapped(model, X, Y, idx, step: int, lr: float, momentum: f
     model.backward(Y, y_idx=idx, loss=loss, fused=None)
     overlap()
     model.step(SGD(lr, momentum, weight_decay, 1.0 / world))
+
+
+def union_average_(model, targets, group=None) -> list:
+    """WASAP phase 2 end (Alg. 1): average K replicas
+    whose topologies evolved independently over the UNION of their supports and re-sparsify each
+    layer to targets[l-2] connections (the phase-1 count), then average the biases (Eq. 2).
+    Collectives: per layer an all-gather of the nnz counts and of the (position, value) lists
+    (padded to the largest), concatenated in rank order; the merge / selection / rebuild runs in
+    the library identically on every rank, so the replicas end bit-identical.  Returns the kept
+    count per weight layer."""
+    import torch
+    import torch.distributed as dist
+    K = dist.get_world_size(group) if dist.is_initialized() else 1
+    kept = []
+    for l in range(2, model.L + 1):
+        pos, val = model.export_positions(l)
+        if K > 1:
+            n = torch.tensor([pos.numel()], dtype=torch.int64, device=pos.device)
+            ns = [torch.zeros_like(n) for _ in range(K)]
+            dist.all_gather(ns, n, group=group)
+            counts = [int(x.item()) for x in ns]
+            m = max(counts)
+            pp = torch.zeros(m, dtype=torch.int64, device=pos.device)
+            vp = torch.zeros(m, dtype=torch.float32, device=pos.device)
+            pp[:pos.numel()] = pos
+            vp[:val.numel()] = val
+            P = [torch.empty_like(pp) for _ in range(K)]
+            V = [torch.empty_like(vp) for _ in range(K)]
+            dist.all_gather(P, pp, group=group)
+            dist.all_gather(V, vp, group=group)
+            pos = torch.cat([P[k][:counts[k]] for k in range(K)])
+            val = torch.cat([V[k][:counts[k]] for k in range(K)])
+        kept.append(model.union_average_layer(l, K, pos, val, int(targets[l - 2])))
+    p, _ = model.param_view()
+    _, bias_base = model.view_layout()
+    average_(p[bias_base:], group)
+    model.params_updated()
+    return kept

@@ -30,7 +30,7 @@ PRUNE_OUTGOING = 1
 EXPORTED = [
     "sparse_mlp_create", "sparse_mlp_destroy", "sparse_mlp_set_stream", "sparse_mlp_forward",
     "sparse_mlp_backward", "sparse_mlp_step", "sparse_mlp_train_step_host", "sparse_mlp_train_step_host_async",
-    "sparse_mlp_sync", "sparse_mlp_gradient_flow", "sparse_mlp_wait_layer", "sparse_mlp_view_layout", "sparse_mlp_grad_view",
+    "sparse_mlp_sync", "sparse_mlp_gradient_flow", "sparse_mlp_export_positions", "sparse_mlp_union_average_layer", "sparse_mlp_wait_layer", "sparse_mlp_view_layout", "sparse_mlp_grad_view",
     "sparse_mlp_param_view", "sparse_mlp_evolve_topology", "sparse_mlp_prune_neurons",
     "sparse_mlp_importance", "sparse_mlp_info", "sparse_mlp_export_layer", "sparse_mlp_import_layer",
     "sparse_mlp_export_bias", "sparse_mlp_import_bias", "sparse_mlp_export_alive",
@@ -107,6 +107,8 @@ def load_library(path: str = LIB_PATH):
         "sparse_mlp_train_step_host_async": (I32, [VP, VP, VP, I32, U64, P(smlp_sgd), VP]),
         "sparse_mlp_sync": (I32, [VP]),
         "sparse_mlp_gradient_flow": (I32, [VP, VP]),
+        "sparse_mlp_export_positions": (I32, [VP, I32, VP, VP]),
+        "sparse_mlp_union_average_layer": (I32, [VP, I32, I32, VP, VP, I64, I64, VP]),
         "sparse_mlp_wait_layer": (I32, [VP, I32, VP]),
         "sparse_mlp_view_layout": (I32, [VP, VP, VP, VP]),
         "sparse_mlp_grad_view": (I32, [VP, P(VP), P(I64), P(U64)]),
@@ -270,6 +272,24 @@ class SparseMLP:
         self._check(self.lib.sparse_mlp_gradient_flow(self.h, C.byref(out)))
         return float(out.value)
 
+    def sparse_mlp_export_positions(self, l: int):
+        """(pos uint64 as int64 tensor, val float32 tensor) of W^(l) on the device, canonical order."""
+        torch = self._torch
+        nnz = self.sparse_mlp_info()["nnz"][l - 1]
+        pos = torch.empty(max(nnz, 1), dtype=torch.int64, device=f"cuda:{self.device}")
+        val = torch.empty(max(nnz, 1), dtype=torch.float32, device=f"cuda:{self.device}")
+        self._sync_stream()
+        self._check(self.lib.sparse_mlp_export_positions(self.h, int(l), _ptr(pos), _ptr(val)))
+        return pos[:nnz], val[:nnz]
+
+    def sparse_mlp_union_average_layer(self, l: int, K: int, pos_all, val_all, target: int) -> int:
+        """WASAP phase-2 union averaging of W^(l) (see include/sparse_mlp.h); returns the kept count."""
+        kept = C.c_int64(0)
+        self._sync_stream()
+        self._check(self.lib.sparse_mlp_union_average_layer(self.h, int(l), int(K), _ptr(pos_all), _ptr(val_all),
+                                                            int(pos_all.numel()), int(target), C.byref(kept)))
+        return int(kept.value)
+
     def sparse_mlp_wait_layer(self, l: int, stream):
         """`stream` (torch.cuda.Stream) waits until W^(l)'s gradient of the last backward is final."""
         self._check(self.lib.sparse_mlp_wait_layer(self.h, int(l), C.c_void_p(stream.cuda_stream)))
@@ -416,6 +436,9 @@ class SparseMLP:
     train_step_host_async = sparse_mlp_train_step_host_async
     wait_layer = sparse_mlp_wait_layer
     gradient_flow = sparse_mlp_gradient_flow
+    params_updated = sparse_mlp_params_updated
+    export_positions = sparse_mlp_export_positions
+    union_average_layer = sparse_mlp_union_average_layer
     view_layout = sparse_mlp_view_layout
     sync = sparse_mlp_sync
 

@@ -20,7 +20,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from .dp import allreduce_sum_, average_, scaled_lr, shard_bounds
+from .dp import allreduce_sum_, average_, scaled_lr, shard_bounds, union_average_
 from .sparse_mlp import SGD, SparseMLP
 
 
@@ -158,6 +158,31 @@ class Trainer:
 
     def fit(self, epochs: int) -> List[EpochRecord]:
         return [self.train_epoch(e, last=(e == epochs - 1)) for e in range(epochs)]
+
+    def fit_wasap(self, phase1_epochs: int, phase2_epochs: int) -> List[EpochRecord]:
+        """WASAP with the paper's phase 2 (Alg. 1):
+        phase 1 = synchronous DP (one gradient allreduce per step, replicated evolution); phase 2 =
+        every replica trains its own shard with NO per-step collective and evolves its topology
+        with its own counter (rank-specific evolve index, DESIGN R21), so the K topologies diverge;
+        at the end the K models are averaged over the union of their supports and re-sparsified
+        to the phase-1 per-layer connection counts (dp.union_average_)."""
+        recs = [self.train_epoch(e, last=False) for e in range(phase1_epochs)]
+        targets = self.m.info()["nnz"][1:]
+        world, use_graph = self.world, self.use_graph
+        self.world, self.use_graph = 1, False            # local steps: no collective in phase 2
+        try:
+            for e in range(phase1_epochs, phase1_epochs + phase2_epochs):
+                rec = self.train_epoch(e, last=True)       # local training, no replicated evolve
+                t1 = time.perf_counter()
+                # independent evolution: counter distinct per (epoch, rank)
+                rec.removed = self.m.evolve_topology(self.cfg.zeta, (1 << 20) + e * max(1, world) + self.rank)
+                self.torch.cuda.synchronize()
+                rec.evolve_s = time.perf_counter() - t1
+                recs.append(rec)
+        finally:
+            self.world, self.use_graph = world, use_graph
+        union_average_(self.m, targets, self.group)
+        return recs
 
 
 # ---------------------------------------------------------------------------------- post-training

@@ -1,0 +1,76 @@
+"""Loss-curve parity over 5 epochs (BASELINE.json north_star: "loss curves must agree within 1e-3
+over 5 epochs"; SURVEY.md §8(d) parity coverage: C1, C2, C3).
+
+The GPU run goes through the epoch driver (paper_2102_01732_b200/trainer.py: CUDA-graph replay of
+full batches, eager tail batch, Importance Pruning and SET evolution at the epoch boundary); the
+oracle replays exactly the same schedule on the CPU (same per-epoch permutation, same global step
+counter for dropout, same prune / evolve calls).  Per-epoch mean training losses must agree to
+1e-3 relative.  Topology decisions are taken independently on each side (a near-tie at a selection
+threshold may flip one connection; the curve criterion tolerates that).  C2 and C3 keep their
+shapes, batch, dropout and pruning schedule but train on a seeded subset of their samples so the
+oracle finishes in about a minute.
+"""
+import numpy as np
+import pytest
+
+from oracle import model as M
+from oracle import topology as T
+from synth import get_config, make_dataset
+from tests.gpu_helpers import pair
+
+pytestmark = pytest.mark.gpu
+
+EPOCHS = 5
+
+
+def _oracle_curve(cfg, st, X, Y, epochs):
+    n, B = X.shape[0], cfg.batch
+    losses, step = [], 0
+    for e in range(epochs):
+        order = np.random.default_rng([cfg.data_seed, e, 0]).permutation(n).astype(np.int32)
+        tot = 0.0
+        for s in range(0, n, B):
+            idx = order[s:s + B]
+            loss, _, _ = M.train_step(st, X[idx], Y[idx], cfg.lr, cfg.momentum, cfg.weight_decay, step)
+            tot += loss * len(idx)
+            step += 1
+        losses.append(tot / n)
+        if cfg.prune and e % cfg.prune_every == 0 and e >= cfg.prune_start:
+            T.prune(st, cfg.prune_percentile)
+        if e < epochs - 1:
+            T.evolve(st, cfg.zeta, e)
+    return losses
+
+
+@pytest.mark.parametrize("name,n", [("C1", None), ("C2", 2_560), ("C3", 160)])
+def test_loss_curves_5_epochs(name, n):
+    import torch
+    from paper_2102_01732_b200.trainer import Trainer
+    cfg = get_config(name) if n is None else get_config(name, n_samples=n)
+    X, Y = make_dataset(cfg, n=cfg.n_samples)
+    Y = Y.astype(np.int32)
+    g, st = pair(cfg)
+    tr = Trainer(g, cfg, torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda(), use_graph=True, graph_steps=4)
+    recs = tr.fit(EPOCHS)
+    gpu = [r.loss for r in recs]
+    ora = _oracle_curve(cfg, st, X, Y, EPOCHS)
+    for e, (a, b) in enumerate(zip(gpu, ora)):
+        assert abs(a - b) <= 1e-3 * abs(b), (name, e, gpu, ora)
+    assert gpu[-1] < gpu[0]                                   # it trains
+    if cfg.prune:
+        assert recs[-1].alive[1] < cfg.sizes[1]               # pruning fired
+
+
+def test_wasap_phase2_single_rank():
+    """fit_wasap on one rank: phase 2 (local steps, rank-specific evolution) then the union
+    averaging with K = 1, which re-sparsifies to the phase-1 counts (a no-op on the counts)."""
+    import torch
+    from paper_2102_01732_b200.trainer import Trainer
+    cfg = get_config("C1")
+    X, Y = make_dataset(cfg, n=cfg.n_samples)
+    g, _ = pair(cfg)
+    tr = Trainer(g, cfg, torch.from_numpy(X).cuda(), torch.from_numpy(Y.astype(np.int32)).cuda())
+    before = g.info()["nnz"]
+    recs = tr.fit_wasap(1, 1)
+    assert len(recs) == 2 and g.info()["nnz"] == before
+    assert all(np.isfinite(r.loss) for r in recs)

@@ -370,3 +370,46 @@ def test_post_training_prune_sweep_parity():
         assert abs(acc - acc_o) <= 2.0 / len(yt), (rho, acc, acc_o)
     e = g.export_layer(3)                                # restored after the sweep
     assert np.array_equal(e["col"], st.layers[1].col) and np.array_equal(e["w"], st.layers[1].w)
+
+
+def test_union_average_parity():
+    """WASAP phase 2 end: K = 3 replicas evolved independently, averaged over
+    the union of their supports and re-sparsified to the phase-1 counts.  Every replica runs the
+    library merge on the same gathered (position, value) lists and ends bit-identical; topology
+    and values are bit-exact to oracle.dp.average_union (the arithmetic that decides the
+    selection is shared, DESIGN R31)."""
+    from oracle import dp as ODP
+    from oracle import topology as T
+    torch = _torch()
+    cfg = get_config("C1", dropout=0.0)
+    K = 3
+    gs, sts = [], []
+    for k in range(K):
+        g, st = pair(cfg)
+        g.evolve_topology(cfg.zeta, 50 + k)
+        T.evolve(st, cfg.zeta, 50 + k)
+        gs.append(g)
+        sts.append(st)
+    targets = [L.nnz for L in sts[0].layers]
+    for l in range(2, cfg.n_layers + 1):
+        lists = [g.export_positions(l) for g in gs]
+        pos = torch.cat([p for p, _ in lists])
+        val = torch.cat([v for _, v in lists])
+        for g in gs:
+            assert g.union_average_layer(l, K, pos, val, targets[l - 2]) == min(targets[l - 2], len(set(pos.tolist())))
+    torch.cuda.synchronize()
+    kept = ODP.average_union(sts, targets)
+    for g in gs:
+        for Ly in sts[0].layers:
+            e = g.export_layer(Ly.l)
+            assert np.array_equal(e["row_ptr"], Ly.row_ptr.astype(np.int32)), Ly.l
+            assert np.array_equal(e["col"], Ly.col), Ly.l
+            assert np.array_equal(e["w"].view(np.uint32), Ly.w.view(np.uint32)), Ly.l
+            assert not np.any(e["v"])
+    assert kept == [g.info()["nnz"][l - 1] for l in range(2, cfg.n_layers + 1) for g in gs[:1]]
+    # the averaged model still trains (mirror and work lists rebuilt)
+    from paper_2102_01732_b200 import SGD
+    X, Y = make_dataset(cfg, n=cfg.batch)
+    gs[0].forward(to_dev(X), train=True, step=0)
+    gs[0].backward(to_dev(Y.astype(np.int32)), fused=SGD(cfg.lr, cfg.momentum, cfg.weight_decay))
+    torch.cuda.synchronize()

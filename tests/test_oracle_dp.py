@@ -1,9 +1,12 @@
 """Pins for oracle/dp.py (CPU): K-rank synchronous DP (WASSP phase 1) and Eq. 2 averaging."""
+import copy
+
 import numpy as np
 import pytest
 
 from oracle import dp
 from oracle import model as M
+from oracle import topology as T
 from oracle.compare import rel_err
 
 
@@ -81,3 +84,85 @@ def test_average_identity_and_mean():
             assert np.max(np.abs(Ly.w - ref[i])) <= 1e-6 * np.max(np.abs(ref[i]))
     with pytest.raises(ValueError):
         dp.average([_st(seed=4), _st(seed=5)])
+
+
+# ---------------------------------------------------------------- union averaging (WASAP phase 2)
+def _tiny_pair_disjoint():
+    """Two replicas of a 2 x 2 layer with one connection each at different positions."""
+    sts = []
+    for pos, w in (((0, 1), 4.0), ((1, 0), 2.0)):
+        st = M.create((2, 2, 2), 0.5, "all_relu", 0.5, 0.0, "he_uniform", 1)
+        Ly = st.layers[0]
+        Ly.row_ptr = np.array([0, 1 if pos[0] == 0 else 0, 1], np.int64)
+        Ly.col = np.array([pos[1]], np.int32)
+        Ly.w = np.array([w], np.float32)
+        Ly.v = np.zeros(1, np.float32)
+        sts.append(st)
+    return sts
+
+
+def test_union_average_spec_example():
+    """Disjoint single entries 4 and 2 -> union values {2, 1} after / K = 2; prune to 1 keeps 2."""
+    a, b = _tiny_pair_disjoint()
+    kept = dp.average_union([a, b], [1, a.layers[1].nnz])
+    assert kept[0] == 1
+    for s in (a, b):
+        Ly = s.layers[0]
+        assert Ly.w.tolist() == [2.0] and Ly.col.tolist() == [1] and Ly.row_ptr.tolist() == [0, 1, 1]
+    a, b = _tiny_pair_disjoint()
+    dp.average_union([a, b], [2, a.layers[1].nnz])   # no pruning: the union, position order
+    assert a.layers[0].w.tolist() == [2.0, 1.0] and a.layers[0].keys().tolist() == [1, 2]
+
+
+def test_union_average_k1_identity_and_identical_supports():
+    st = _st()
+    ref = copy.deepcopy(st)
+    dp.average_union([st], [L.nnz for L in st.layers])          # K = 1, own counts: identity
+    for p, q in zip(st.layers, ref.layers):
+        assert np.array_equal(p.col, q.col) and np.array_equal(p.w.view(np.uint32), q.w.view(np.uint32))
+        assert not np.any(p.v)
+    # identical supports, target = nnz: the plain Eq. 2 mean (average()) up to the float32 sum
+    a, b = _st(seed=4), _st(seed=4)
+    rng = np.random.default_rng(2)
+    for L in b.layers:
+        L.w = (L.w + rng.standard_normal(L.w.shape).astype(np.float32) * 0.01).astype(np.float32)
+    a2, b2 = copy.deepcopy(a), copy.deepcopy(b)
+    dp.average_union([a, b], [L.nnz for L in a.layers])
+    dp.average([a2, b2])
+    for p, q in zip(a.layers, a2.layers):
+        assert np.array_equal(p.col, q.col)
+        assert np.max(np.abs(p.w - q.w)) <= 1e-7
+
+
+def test_union_average_evolved_replicas_invariants_and_brute_force():
+    """K = 4 replicas evolved independently: union >= every support, exactly `target` kept, and
+    the kept set is the brute-force top-target |mean| (ties by position)."""
+    base = _st(seed=11)
+    sts = []
+    for k in range(4):
+        s = copy.deepcopy(base)
+        T.evolve(s, 0.3, 100 + k)                              # independent topologies
+        sts.append(s)
+    targets = [L.nnz for L in base.layers]
+    supports = [[set(L.keys().tolist()) for L in s.layers] for s in sts]
+    vals = [[dict(zip(L.keys().tolist(), L.w.tolist())) for L in s.layers] for s in sts]
+    kept = dp.average_union(sts, targets)
+    for idx, target in enumerate(targets):
+        union = set().union(*[supports[k][idx] for k in range(4)])
+        assert len(union) >= max(len(supports[k][idx]) for k in range(4))
+        assert kept[idx] == min(target, len(union)) and sts[0].layers[idx].nnz == kept[idx]
+        mean = {}
+        for p in sorted(union):
+            sv = None
+            for k in range(4):
+                if p in vals[k][idx]:
+                    w = np.float32(vals[k][idx][p])
+                    sv = w if sv is None else np.float32(sv + w)
+            mean[p] = np.float32(sv) / np.float32(4)
+        ranked = sorted(union, key=lambda p: (int(np.float32(mean[p]).view(np.uint32)) & 0x7fffffff, p))
+        expect = sorted(ranked[len(union) - kept[idx]:])
+        assert sts[0].layers[idx].keys().tolist() == expect
+        assert sts[0].layers[idx].w.tolist() == [float(mean[p]) for p in expect]
+    for s in sts[1:]:                                          # every replica holds the same model
+        for p, q in zip(s.layers, sts[0].layers):
+            assert np.array_equal(p.keys(), q.keys()) and np.array_equal(p.w, q.w)
