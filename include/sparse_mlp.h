@@ -211,6 +211,18 @@ int sparse_mlp_export_positions(smlp_handle* h, int32_t l, uint64_t* pos_dev, fl
 int sparse_mlp_union_average_layer(smlp_handle* h, int32_t l, int32_t K, const uint64_t* pos_all,
                                    const float* val_all, int64_t total, int64_t target, int64_t* kept);
 
+/* sparse_mlp_retain_valid_updates — RetainValidUpdates of Alg. 1 (Fig. 4
+ * PAPER.md:81-89): a gradient of W^(l) computed on an
+ * older topology (stale_pos: its sorted canonical positions i * n_l + j, stale_g: the gradient
+ * values, both device arrays of n_stale entries, e.g. sparse_mlp_export_positions + the grad view
+ * slice at that version) is mapped onto the CURRENT support: each current connection takes the
+ * stale gradient at its position, or 0 if the connection did not exist then (the intersection of
+ * the two supports).  Written into W^(l)'s slice of the grad view; the bias slices are left to the
+ * caller; then sparse_mlp_step applies Eq. 1.  *retained (host, may be NULL) = size of the
+ * intersection.  Pure data movement (bit-exact).  SYNC. */
+int sparse_mlp_retain_valid_updates(smlp_handle* h, int32_t l, const uint64_t* stale_pos,
+                                    const float* stale_g, int64_t n_stale, int64_t* retained);
+
 /* sparse_mlp_wait_layer — makes `stream` (a cudaStream_t) wait until the last backward's
  * gradient of W^(l) (and of b_{l-1}) is final, so that layer's slice of the grad view can be
  * allreduced while the backward of the layers below continues (SURVEY §8(e) overlap; the

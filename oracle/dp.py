@@ -118,3 +118,17 @@ def average_union(states: List[State], targets: Sequence[int]) -> List[int]:
             s.vb[idx] = np.zeros_like(s.vb[idx])
         s.version += 1
     return kept
+
+
+def retain_valid_updates(stale_keys: Sequence[np.ndarray], stale_g: Sequence[np.ndarray], st_now: State) -> List[np.ndarray]:
+    """RetainValidUpdates of Alg. 1 (Fig. 4):
+    a worker's gradient computed on the topology at time t (per layer: canonical positions
+    i * n_out + j and values) restricted to the server's CURRENT topology: each current connection
+    takes the stale gradient at its position if that position existed at t, else 0 -- the
+    intersection of the two supports.  Returns per-layer gradients aligned to st_now's canonical
+    order."""
+    out = []
+    for Ly, keys, g in zip(st_now.layers, stale_keys, stale_g):
+        table = dict(zip(np.asarray(keys).tolist(), np.asarray(g, dtype=F32).tolist()))
+        out.append(np.array([table.get(p, 0.0) for p in Ly.keys().tolist()], dtype=F32))
+    return out

@@ -181,3 +181,52 @@ int sparse_mlp_export_positions(smlp_handle* h, int32_t l, uint64_t* pos_dev, fl
     SMLP_CK(h, cudaMemcpyAsync(val_dev, Ly.val, sizeof(float) * (size_t)Ly.nnz, cudaMemcpyDeviceToDevice, h->stream));
     return SMLP_OK;
 }
+
+namespace smlp {
+namespace {
+
+// g_now[k] = stale gradient at the position of current entry k, 0 if that position was not in the
+// stale support (binary search in the sorted stale positions)
+__global__ void retain_kernel(const int32_t* __restrict__ rowid, const int32_t* __restrict__ col, int64_t nnz,
+                              int64_t n_out, const uint64_t* __restrict__ spos, const float* __restrict__ sg,
+                              int64_t ns, float* __restrict__ g_now, unsigned long long* __restrict__ hits) {
+    unsigned long long h = 0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = (uint64_t)rowid[k] * (uint64_t)n_out + (uint64_t)col[k];
+        int64_t lo = 0, hi = ns;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (spos[mid] < p) lo = mid + 1;
+            else hi = mid;
+        }
+        const bool found = lo < ns && spos[lo] == p;
+        g_now[k] = found ? sg[lo] : 0.f;
+        h += found ? 1ull : 0ull;
+    }
+    if (h) atomicAdd(hits, h);   // integer: exact and order-independent
+}
+
+}  // namespace
+}  // namespace smlp
+
+int sparse_mlp_retain_valid_updates(smlp_handle* h, int32_t l, const uint64_t* stale_pos, const float* stale_g,
+                                    int64_t n_stale, int64_t* retained) {
+    using namespace smlp;
+    if (!h || l < 2 || l > h->L || n_stale < 0 || (n_stale > 0 && (!stale_pos || !stale_g))) return SMLP_E_ARG;
+    Layer& Ly = h->layers[l - 2];
+    unsigned long long* cnt = (unsigned long long*)tmp_alloc(h, sizeof(unsigned long long));
+    if (!cnt) return set_err(h, SMLP_E_NOMEM, "retain counter");
+    SMLP_CK(h, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), h->stream));
+    if (Ly.nnz > 0) {
+        retain_kernel<<<launch_grid(h, Ly.nnz, TPB), TPB, 0, h->stream>>>(Ly.rowid, Ly.col, Ly.nnz, Ly.n_out, stale_pos,
+                                                                          stale_g, n_stale, Ly.grad, cnt);
+        SMLP_CK_LAUNCH(h, "retain_kernel");
+    }
+    unsigned long long c = 0;
+    SMLP_CK(h, cudaMemcpyAsync(&c, cnt, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
+    SMLP_CK(h, cudaStreamSynchronize(h->stream));
+    tmp_free(h, cnt, sizeof(unsigned long long));
+    if (retained) *retained = (int64_t)c;
+    h->grads_pending = true;    // the caller applies it with sparse_mlp_step (biases: its grad view slice)
+    return SMLP_OK;
+}

@@ -189,3 +189,34 @@ def union_average_(model, targets, group=None) -> list:
     average_(p[bias_base:], group)
     model.params_updated()
     return kept
+
+
+class StaleGradient:
+    """A gradient together with the topology it was computed on (version-tagged), for the
+    asynchronous phase-1 analogue (Alg. 1): taken after an
+    unfused backward, applied later -- possibly after the model's topology evolved -- through
+    RetainValidUpdates."""
+
+    def __init__(self, model):
+        g, version = model.grad_view()
+        layout, bias_base = model.view_layout()
+        nnz = model.info()["nnz"]
+        self.version = version
+        self.layers = []
+        for l in range(2, model.L + 1):
+            pos, _ = model.export_positions(l)
+            off = layout[l - 2][0]
+            self.layers.append((pos.clone(), g[off:off + nnz[l - 1]].clone()))
+        self.bias = g[bias_base:].clone()
+
+
+def apply_stale_gradient(model, stale: "StaleGradient", sgd) -> list:
+    """Server side of Alg. 1 phase 1: g = RetainValidUpdates(stale gradient, current model) per
+    layer (intersection of supports), the biases unchanged (dense), then the Eq. 1 update.
+    Returns the retained connection count per layer."""
+    kept = [model.retain_valid_updates(l, pos, gv) for l, (pos, gv) in zip(range(2, model.L + 1), stale.layers)]
+    g, _ = model.grad_view()
+    _, bias_base = model.view_layout()
+    g[bias_base:].copy_(stale.bias)
+    model.step(sgd)
+    return kept

@@ -30,7 +30,8 @@ PRUNE_OUTGOING = 1
 EXPORTED = [
     "sparse_mlp_create", "sparse_mlp_destroy", "sparse_mlp_set_stream", "sparse_mlp_forward",
     "sparse_mlp_backward", "sparse_mlp_step", "sparse_mlp_train_step_host", "sparse_mlp_train_step_host_async",
-    "sparse_mlp_sync", "sparse_mlp_gradient_flow", "sparse_mlp_export_positions", "sparse_mlp_union_average_layer", "sparse_mlp_wait_layer", "sparse_mlp_view_layout", "sparse_mlp_grad_view",
+    "sparse_mlp_sync", "sparse_mlp_gradient_flow", "sparse_mlp_export_positions", "sparse_mlp_union_average_layer",
+    "sparse_mlp_retain_valid_updates", "sparse_mlp_wait_layer", "sparse_mlp_view_layout", "sparse_mlp_grad_view",
     "sparse_mlp_param_view", "sparse_mlp_evolve_topology", "sparse_mlp_prune_neurons",
     "sparse_mlp_importance", "sparse_mlp_info", "sparse_mlp_export_layer", "sparse_mlp_import_layer",
     "sparse_mlp_export_bias", "sparse_mlp_import_bias", "sparse_mlp_export_alive",
@@ -109,6 +110,7 @@ def load_library(path: str = LIB_PATH):
         "sparse_mlp_gradient_flow": (I32, [VP, VP]),
         "sparse_mlp_export_positions": (I32, [VP, I32, VP, VP]),
         "sparse_mlp_union_average_layer": (I32, [VP, I32, I32, VP, VP, I64, I64, VP]),
+        "sparse_mlp_retain_valid_updates": (I32, [VP, I32, VP, VP, I64, VP]),
         "sparse_mlp_wait_layer": (I32, [VP, I32, VP]),
         "sparse_mlp_view_layout": (I32, [VP, VP, VP, VP]),
         "sparse_mlp_grad_view": (I32, [VP, P(VP), P(I64), P(U64)]),
@@ -290,6 +292,15 @@ class SparseMLP:
                                                             int(pos_all.numel()), int(target), C.byref(kept)))
         return int(kept.value)
 
+    def sparse_mlp_retain_valid_updates(self, l: int, stale_pos, stale_g) -> int:
+        """Map a stale gradient of W^(l) (device tensors: sorted positions, values) onto the current
+        support, into the grad view (RetainValidUpdates); returns the intersection size."""
+        out = C.c_int64(0)
+        self._sync_stream()
+        self._check(self.lib.sparse_mlp_retain_valid_updates(self.h, int(l), _ptr(stale_pos), _ptr(stale_g),
+                                                             int(stale_pos.numel()), C.byref(out)))
+        return int(out.value)
+
     def sparse_mlp_wait_layer(self, l: int, stream):
         """`stream` (torch.cuda.Stream) waits until W^(l)'s gradient of the last backward is final."""
         self._check(self.lib.sparse_mlp_wait_layer(self.h, int(l), C.c_void_p(stream.cuda_stream)))
@@ -439,6 +450,7 @@ class SparseMLP:
     params_updated = sparse_mlp_params_updated
     export_positions = sparse_mlp_export_positions
     union_average_layer = sparse_mlp_union_average_layer
+    retain_valid_updates = sparse_mlp_retain_valid_updates
     view_layout = sparse_mlp_view_layout
     sync = sparse_mlp_sync
 

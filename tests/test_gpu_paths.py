@@ -413,3 +413,45 @@ def test_union_average_parity():
     gs[0].forward(to_dev(X), train=True, step=0)
     gs[0].backward(to_dev(Y.astype(np.int32)), fused=SGD(cfg.lr, cfg.momentum, cfg.weight_decay))
     torch.cuda.synchronize()
+
+
+def test_retain_valid_updates_parity():
+    """Async phase-1 analogue: a gradient taken on topology version t is
+    applied after a SET evolution (version t') through RetainValidUpdates -- the retained
+    gradient is bit-exact to oracle.dp.retain_valid_updates (intersection of supports), and the
+    resulting Eq. 1 update matches the oracle's."""
+    from oracle import dp as ODP
+    from oracle import topology as T
+    from paper_2102_01732_b200 import SGD
+    from paper_2102_01732_b200.dp import StaleGradient, apply_stale_gradient
+    torch = _torch()
+    cfg = get_config("C1", dropout=0.0)
+    g, st = pair(cfg)
+    X, Y = make_dataset(cfg, n=cfg.batch)
+    g.forward(to_dev(X), train=True, step=0)
+    g.backward(to_dev(Y.astype(np.int32)), fused=None)
+    stale = StaleGradient(g)                                   # gradient at version t
+    torch.cuda.synchronize()
+    tr = M.forward(st, X, True, 0)
+    gr = M.backward(st, tr, Y)
+    keys_t = [L.keys() for L in st.layers]
+    g.step(SGD(0.0))                                          # consume (no update) before evolving
+    g.evolve_topology(cfg.zeta, 7)                             # topology moves on (version t')
+    T.evolve(st, cfg.zeta, 7)
+    assert_topology_equal(g, st)
+    sgd = SGD(cfg.lr, cfg.momentum, cfg.weight_decay)
+    ref = ODP.retain_valid_updates(keys_t, gr.g, st)
+    for (pos, gv), Ly, r in zip(stale.layers, st.layers, ref):
+        k = g.retain_valid_updates(Ly.l, pos, gv)
+        assert k == len(set(keys_t[Ly.l - 2].tolist()) & set(Ly.keys().tolist()))
+        # pure data movement: bit-exact against the same mapping of the GPU's own stale values
+        table = dict(zip(pos.cpu().numpy().tolist(), gv.cpu().numpy().tolist()))
+        mapped = np.array([table.get(p, 0.0) for p in Ly.keys().tolist()], np.float32)
+        got = g.sparse_mlp_export_trace(2, Ly.l)[:len(mapped)]
+        assert np.array_equal(got.view(np.uint32), mapped.view(np.uint32)), Ly.l
+        assert rel_err(mapped, r) <= TOL                      # and the oracle's retained gradient
+    kept = apply_stale_gradient(g, stale, sgd)                 # the full server step
+    torch.cuda.synchronize()
+    assert kept == [len(set(keys_t[L.l - 2].tolist()) & set(L.keys().tolist())) for L in st.layers]
+    M.step(st, M.Grads(ref, gr.gb, gr.loss, gr.deltas), sgd.lr, sgd.momentum, sgd.weight_decay)
+    assert_values_close(g, st, TOL)

@@ -166,3 +166,40 @@ def test_union_average_evolved_replicas_invariants_and_brute_force():
     for s in sts[1:]:                                          # every replica holds the same model
         for p, q in zip(s.layers, sts[0].layers):
             assert np.array_equal(p.keys(), q.keys()) and np.array_equal(p.w, q.w)
+
+
+# ---------------------------------------------------------------- RetainValidUpdates (async phase 1)
+def test_retain_valid_updates_pins():
+    """identity when the topology did not change; worker {(0,0),(0,1)} vs server
+    {(0,1),(1,1)} keeps only (0,1); after a random evolution the applied support is a subset of
+    the server support and equals the set intersection (brute force)."""
+    st = _st(seed=8)
+    keys = [L.keys() for L in st.layers]
+    gs = [np.arange(1, L.nnz + 1, dtype=np.float32) for L in st.layers]
+    same = dp.retain_valid_updates(keys, gs, st)
+    assert all(np.array_equal(a, b) for a, b in zip(same, gs))
+    # the 2 x 2 example
+    srv = M.create((2, 2, 2), 0.5, "all_relu", 0.5, 0.0, "he_uniform", 1)
+    Ly = srv.layers[0]
+    Ly.row_ptr = np.array([0, 1, 2], np.int64)
+    Ly.col = np.array([1, 1], np.int32)                # server: (0,1), (1,1)
+    Ly.w = np.ones(2, np.float32)
+    Ly.v = np.zeros(2, np.float32)
+    worker_keys = [np.array([0, 1], np.int64)] + [L.keys() for L in srv.layers[1:]]   # (0,0), (0,1)
+    worker_g = [np.array([5.0, 7.0], np.float32)] + [np.zeros(L.nnz, np.float32) for L in srv.layers[1:]]
+    g = dp.retain_valid_updates(worker_keys, worker_g, srv)
+    assert g[0].tolist() == [7.0, 0.0]
+    # randomized: evolve between push and apply
+    rng = np.random.default_rng(0)
+    for trial in range(5):
+        s = _st(seed=20 + trial)
+        k0 = [L.keys() for L in s.layers]
+        g0 = [rng.standard_normal(L.nnz).astype(np.float32) for L in s.layers]
+        T.evolve(s, 0.3, trial)
+        g1 = dp.retain_valid_updates(k0, g0, s)
+        for L, kk, gg, out in zip(s.layers, k0, g0, g1):
+            inter = set(kk.tolist()) & set(L.keys().tolist())
+            nz = {p for p, v in zip(L.keys().tolist(), out.tolist()) if v != 0.0}
+            assert nz <= inter
+            table = dict(zip(kk.tolist(), gg.tolist()))
+            assert out.tolist() == [np.float32(table.get(p, 0.0)) for p in L.keys().tolist()]
