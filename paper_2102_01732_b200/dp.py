@@ -130,7 +130,8 @@ class OverlappedAllreduce:
         g, _ = self.m.grad_view()
         works = []
         main = torch.cuda.current_stream()
-        self.stream.wait_stream(main)                       # the grad view is not reused before this
+        # no blanket wait on the main stream: each slice waits only for its own layer's event, so
+        # the collectives overlap the rest of the backward
         with torch.cuda.stream(self.stream):
             for l in range(self.m.L, 1, -1):                 # W^(L) is final first
                 self.m.wait_layer(l, self.stream)
