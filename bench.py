@@ -352,20 +352,40 @@ def main():
         k2 = max(3, min(args.steps, 10))
         lossp = torch.zeros(k2 + 2, dtype=torch.float32).pin_memory()
         sgd = SGD(cfg.lr, cfg.momentum, cfg.weight_decay)
+        if dp_path:
+            # N > 1: the synchronous DP step from host buffers -- H2D of x / y (pinned, on the
+            # stream), forward, unfused backward, overlapped per-layer allreduce, Eq. 1, loss D2H
+            xd = torch.empty((B, cfg.sizes[0]), dtype=torch.float32, device=device)
+            yd = torch.empty(B, dtype=torch.int32, device=device)
+            ld = torch.zeros(1, dtype=torch.float32, device=device)
+
+            def host_step(j, step_idx, slot):
+                xd.copy_(xp[j * B:(j + 1) * B], non_blocking=True)
+                yd.copy_(yp[j * B:(j + 1) * B], non_blocking=True)
+                model.forward(xd, train=True, step=step_idx)
+                model.backward(yd, loss=ld, fused=None)
+                if world > 1:
+                    overlap()
+                else:
+                    overlap(reduce=lambda t: None)
+                model.step(SGD(cfg.lr, cfg.momentum, cfg.weight_decay, 1.0 / world))
+                lossp[slot:slot + 1].copy_(ld, non_blocking=True)
+        else:
+            def host_step(j, step_idx, slot):
+                model.train_step_host_async(xp[j * B:(j + 1) * B], yp[j * B:(j + 1) * B], B, step_idx, sgd,
+                                            lossp[slot:])
         for s in range(2):
-            model.train_step_host_async(xp[s * B:(s + 1) * B], yp[s * B:(s + 1) * B], B, 10_000 + s, sgd, lossp[s:])
+            host_step(s, 10_000 + s, s)
         model.sync()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        # every step: H2D of its x / y from pinned host memory (copy stream, overlapping the previous
-        # step's compute), forward, fused backward, D2H of its loss; all inside the timed region
+        # every step: H2D of its x / y from pinned host memory (1 GPU: on a copy stream, overlapping
+        # the previous step's compute), forward, backward + update, D2H of its loss; all timed
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for s in range(k2):
-            j = s % nb
-            model.train_step_host_async(xp[j * B:(j + 1) * B], yp[j * B:(j + 1) * B], B, 20_000 + s, sgd,
-                                        lossp[2 + s:])
+            host_step(s % nb, 20_000 + s, 2 + s)
         e1.record(stream)
         model.sync()
         torch.cuda.synchronize()
@@ -375,8 +395,10 @@ def main():
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": B * world * k2 / (float(et.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": B * cfg.sizes[0] * 4 + B * 4, "d2h_bytes_per_step": 4,
-               "api": "sparse_mlp_train_step_host_async (pinned host x, y -> device on a copy stream "
-                      "overlapping the previous step, fwd, fused bwd, loss -> pinned host)"}
+               "api": ("pinned host x, y -> device, forward, unfused backward, overlapped per-layer allreduce, "
+                       "Eq. 1 step, loss -> pinned host" if dp_path else
+                       "sparse_mlp_train_step_host_async (pinned host x, y -> device on a copy stream "
+                       "overlapping the previous step, fwd, fused bwd, loss -> pinned host)")}
 
     # ---------------------------------------------------------------- epoch-boundary ops (evolve / prune)
     epoch = None
