@@ -239,7 +239,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    use_graph = (args.graph == "on" or (args.graph == "auto" and cfg.name != "C5")) and world == 1 and not dp_path
+    use_graph = args.graph in ("on", "auto") and world == 1 and not dp_path
     graph_note = None
     if use_graph:
         # C1-C4 steps last ~0.1-0.3 ms: replay G captured steps per CUDA graph; the
@@ -268,8 +268,6 @@ def main():
     clocks.start()
     time.sleep(0.3)
     launches0 = model.info()["launches"]
-    if not use_graph:
-        model.sparse_mlp_profile(True)
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -293,19 +291,24 @@ def main():
     if use_graph:
         launches = int(round(launches_per_step * args.steps))
         model.sparse_mlp_set_step_counter(None)
-        # per-kernel table: eager profiled steps after the timed graph replays (same kernels)
-        model.sparse_mlp_profile(True)
-        for s in range(total_steps, total_steps + min(args.steps, 8)):
-            one_step(s % total_steps)
-        torch.cuda.synchronize()
-        prof = model.sparse_mlp_profile_read()
-        model.sparse_mlp_profile(False)
-        graph_note = (f"timed region: {args.steps // G} CUDA-graph replays of {G} steps; kernel table and "
-                      "roofline from eager profiled steps right after it")
     else:
-        prof = model.sparse_mlp_profile_read()
-        model.sparse_mlp_profile(False)
         launches = model.info()["launches"] - launches0
+    # per-kernel times: the same number of steps again, eager, with the library's event pair around
+    # every launch (the events cost ~3% of a C5 step, so they stay out of the headline region)
+    torch.cuda.synchronize()
+    model.sparse_mlp_profile(True)
+    evp0, evp1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evp0.record(stream)
+    for s in range(args.steps):
+        one_step(args.warmup + s)
+    evp1.record(stream)
+    torch.cuda.synchronize()
+    ms_prof = evp0.elapsed_time(evp1) / args.steps
+    prof = model.sparse_mlp_profile_read()
+    model.sparse_mlp_profile(False)
+    profiled_steps = args.steps
+    if use_graph:
+        graph_note = f"timed region: {args.steps // G} CUDA-graph replays of {G} steps (no per-kernel events)"
     clk = clocks.stop()
     t_ms = torch.tensor([ms], dtype=torch.float64, device=device)
     if world > 1:
@@ -435,7 +438,8 @@ def main():
                            f"{X.numel() * 4 / 1e9:.1f} GB; per-step traffic {step_bytes / 1e9:.2f} GB)",
                            "create_s": round(t_create, 2), "cuda_graph": graph_note},
                 "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": int(launches), "clocks": clk, "epoch": epoch,
+                "gpu_launches": int(launches), "clocks": clk, "epoch": epoch, "profiled_steps": profiled_steps,
+                "ms_per_step_profiled": round(ms_prof, 4),
                 "kernels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in prof]}
         print(json.dumps(line), flush=True)
         if args.profile_json:

@@ -63,6 +63,16 @@ void dev_free(smlp_handle* h, void* p) {
     }
 }
 
+// inside a CUDA-graph capture the profiling events become external event-record nodes, so every
+// replay re-stamps them and the kernel times of the last replay can be read back
+static void prof_record(smlp_handle* h, cudaEvent_t e) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(h->stream, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags(e, h->stream, cudaEventRecordExternal);
+    else
+        cudaEventRecord(e, h->stream);
+}
+
 void prof_start(smlp_handle* h, int kind, int layer, double bytes, double flops) {
     if (!h->prof) return;
     ProfRec r{kind, layer, nullptr, nullptr, bytes, flops};
@@ -74,13 +84,13 @@ void prof_start(smlp_handle* h, int kind, int layer, double bytes, double flops)
             cudaEventCreate(e);
         }
     }
-    cudaEventRecord(r.a, h->stream);
+    prof_record(h, r.a);
     h->prof_recs.push_back(r);
 }
 
 void prof_stop(smlp_handle* h) {
     if (!h->prof || h->prof_recs.empty()) return;
-    cudaEventRecord(h->prof_recs.back().b, h->stream);
+    prof_record(h, h->prof_recs.back().b);
 }
 
 }  // namespace smlp
