@@ -340,6 +340,21 @@ def main():
     step_roof = {"bytes_per_step_F1": step_bytes, "achieved_GBps": round(step_bytes / (ms_per_step * 1e-3) / 1e9, 1),
                  "frac": round(step_bytes / (ms_per_step * 1e-3) / 1e9 / peak, 4)}
 
+    # ---------------------------------------------------------------- epoch-boundary ops (evolve / prune)
+    epoch = None
+    if not args.no_epoch:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if cfg.prune:
+            model.prune_neurons(cfg.prune_percentile)
+        model.evolve_topology(cfg.zeta, 0)
+        torch.cuda.synchronize()
+        t_ev = time.perf_counter() - t0
+        steps_per_epoch = math.ceil(cfg.n_samples / (B * world))
+        epoch = {"evolve_s": round(t_ev, 4), "steps_per_epoch": steps_per_epoch,
+                 "epoch_samples_per_s_incl_evolve": cfg.n_samples / (steps_per_epoch * ms_per_step / 1e3 + t_ev),
+                 "replicas_identical": bool(replicas_identical(model.param_view()[0])) if world > 1 else True}
+
     # ---------------------------------------------------------------- end to end through the host-buffer API
     e2e = None
     if not args.no_e2e:
@@ -402,21 +417,6 @@ def main():
                        "Eq. 1 step, loss -> pinned host" if dp_path else
                        "sparse_mlp_train_step_host_async (pinned host x, y -> device on a copy stream "
                        "overlapping the previous step, fwd, fused bwd, loss -> pinned host)")}
-
-    # ---------------------------------------------------------------- epoch-boundary ops (evolve / prune)
-    epoch = None
-    if not args.no_epoch:
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        if cfg.prune:
-            model.prune_neurons(cfg.prune_percentile)
-        model.evolve_topology(cfg.zeta, 0)
-        torch.cuda.synchronize()
-        t_ev = time.perf_counter() - t0
-        steps_per_epoch = math.ceil(cfg.n_samples / (B * world))
-        epoch = {"evolve_s": round(t_ev, 4), "steps_per_epoch": steps_per_epoch,
-                 "epoch_samples_per_s_incl_evolve": cfg.n_samples / (steps_per_epoch * ms_per_step / 1e3 + t_ev),
-                 "replicas_identical": bool(replicas_identical(model.param_view()[0])) if world > 1 else True}
 
     cpu = None
     if cpu_fut is not None:
