@@ -455,3 +455,31 @@ def test_retain_valid_updates_parity():
     assert kept == [len(set(keys_t[L.l - 2].tolist()) & set(L.keys().tolist())) for L in st.layers]
     M.step(st, M.Grads(ref, gr.gb, gr.loss, gr.deltas), sgd.lr, sgd.momentum, sgd.weight_decay)
     assert_values_close(g, st, TOL)
+
+
+def test_c5_full_size_evolve_and_prune_bitexact():
+    """SET evolution and Importance Pruning at full C5 size (52.3M connections; op-by-op parity on all five
+    configs, C5 included): from the identical ER init (bit-exact, checked), one evolution on each
+    side gives the identical topology and identical values -- survivors keep theirs, the ~6M
+    regrown connections per hidden layer take the same Philox positions and init values."""
+    from oracle import topology as T
+    torch = _torch()
+    cfg = get_config("C5")
+    g, st = pair(cfg)
+    assert_topology_equal(g, st, "C5 init")
+    removed_g = g.evolve_topology(cfg.zeta, 3)
+    removed_o = T.evolve(st, cfg.zeta, 3)
+    torch.cuda.synchronize()
+    assert list(removed_g[1:]) == list(removed_o)
+    assert_topology_equal(g, st, "C5 evolve")
+    for Ly in st.layers:
+        e = g.export_layer(Ly.l)
+        assert np.array_equal(e["w"].view(np.uint32), Ly.w.view(np.uint32)), f"C5 W^({Ly.l}) values"
+        assert np.array_equal(e["v"].view(np.uint32), Ly.v.view(np.uint32)), f"C5 W^({Ly.l}) momentum"
+    # Importance Pruning at full size (rho = 5, the paper's best post-training threshold): the fp64
+    # importance sums and percentile decisions are reproduced exactly, so the same neurons die
+    pruned_g, removed_g = g.prune_neurons(5.0)
+    pruned_o, removed_o = T.prune(st, 5.0)
+    torch.cuda.synchronize()
+    assert list(pruned_g) == list(pruned_o) and list(removed_g) == list(removed_o)
+    assert_topology_equal(g, st, "C5 prune")
