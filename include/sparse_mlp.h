@@ -83,7 +83,13 @@ typedef struct {
     int32_t        rank;         /* data-parallel rank: enters the dropout stream only        */
     int32_t        max_batch;    /* largest B passed to forward, >= 1                         */
     int32_t        chunk_batch;  /* batch columns per activation chunk (4..128, power of 2);
-                                    0 = auto (min(128, next_pow2(max(4, max_batch))))        */
+                                    0 = auto: min(128, next_pow2(max(4, max_batch))), halved
+                                    while the widest layer's slab n_l x CB x 4 B exceeds the
+                                    L2; the forward tensors (a_l, masks) then use their own
+                                    width CBf <= CB, halved (not below 32) while the slab
+                                    exceeds half the L2.  Explicit: CBf = CB.  Env
+                                    SMLP_FWD_CB overrides CBf (power of 2, <= CB, >= 32 if
+                                    narrower; else SMLP_E_ARG)                               */
     int32_t        device;       /* CUDA device ordinal                                       */
     void*          stream;       /* cudaStream_t the handle enqueues on (NULL = legacy)       */
     const smlp_allocator* allocator; /* NULL = cudaMallocAsync on `stream`                   */
@@ -111,6 +117,7 @@ typedef struct {
     int64_t  bias_offset[SMLP_MAX_LAYERS];   /* offset of b_l in the param view           */
     int64_t  param_count;                    /* floats in the param / grad views          */
     int64_t  launches;                       /* kernels launched by this handle so far    */
+    int32_t  fwd_chunk_batch;                /* CBf: chunk width of a_l and the masks     */
 } smlp_info;
 
 /* sparse_mlp_create — PAPER.md:51-52 ("Initially each W^(l) is a Erdos-Renyi random graph"),

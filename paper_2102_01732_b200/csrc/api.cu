@@ -200,7 +200,9 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
         Ly.narrow = Ly.l == L && Ly.n_out <= NARROW_MAX && (int64_t)Ly.nout_pad * CB <= NARROW_MAX_ELEMS;
         if (Ly.narrow) {
             Ly.ngrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->num_sms * 4, (Ly.n_in + 63) / 64));
-            Ly.nws = zalloc<float>(h, (size_t)Ly.ngrid * Ly.nout_pad * CB, &rc);
+            // CTA partials of a forward pass of up to 128 columns (several forward chunks)
+            const int64_t wmax = std::max<int64_t>(CB, std::min<int64_t>(128, NARROW_MAX_ELEMS / Ly.nout_pad));
+            Ly.nws = zalloc<float>(h, (size_t)Ly.ngrid * Ly.nout_pad * wmax, &rc);
         }
     }
     if (rc) return rc;
@@ -208,11 +210,11 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
     for (int l = 1; l <= L; ++l) {
         const size_t n = (size_t)h->sizes[l - 1];
         // + one zero row after the last chunk: the padding target of the row kernels' gather slots
-        h->act[l] = zalloc<float>(h, ((size_t)h->max_chunks * n + 1) * CB, &rc);
+        h->act[l] = zalloc<float>(h, ((size_t)h->max_chunks_f * n + 1) * h->CBf, &rc);
         if (l >= 2) h->delta[l] = zalloc<float>(h, ((size_t)h->max_chunks * n + 1) * CB, &rc);
         if (l >= 2 && l < L) {
-            h->zmask[l] = zalloc<uint4>(h, (size_t)h->max_chunks * n, &rc);
-            h->kmask[l] = zalloc<uint4>(h, (size_t)h->max_chunks * n, &rc);
+            h->zmask[l] = zalloc<uint4>(h, (size_t)h->max_chunks_f * n, &rc);
+            h->kmask[l] = zalloc<uint4>(h, (size_t)h->max_chunks_f * n, &rc);
         }
         h->alive[l] = zalloc<uint8_t>(h, n, &rc);
         if (rc) return rc;
@@ -221,7 +223,7 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
     }
     h->d_err = zalloc<int32_t>(h, 1, &rc);
     // binary-input path of W^(2): bit-packed input, usable when the padded batch fits 128 columns
-    if ((int64_t)h->max_chunks * CB <= 32 * XBITS_WORDS) {
+    if ((int64_t)h->max_chunks * CB <= 32 * XBITS_WORDS && (int64_t)h->max_chunks_f * h->CBf <= 32 * XBITS_WORDS) {
         h->xbits = zalloc<uint32_t>(h, (size_t)h->sizes[0] * XBITS_WORDS, &rc);
         h->d_nonbinary = zalloc<int32_t>(h, 1, &rc);
         h->gmirror2 = zalloc<float>(h, (size_t)std::max<int64_t>(h->layers[0].cap, 1), &rc);
@@ -275,6 +277,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
         return set_err(nullptr, SMLP_E_ARG, "unknown activation");
     if (cfg->init < SMLP_INIT_NORMAL || cfg->init > SMLP_INIT_HE_U) return set_err(nullptr, SMLP_E_ARG, "unknown init");
     int CB = cfg->chunk_batch;
+    int CBf = CB;
     if (CB != 0 && (CB < 4 || CB > 128 || (CB & (CB - 1))))
         return set_err(nullptr, SMLP_E_ARG, "chunk_batch must be a power of two in [4, 128]");
     if (cudaSetDevice(cfg->device) != cudaSuccess) return set_err(nullptr, SMLP_E_CUDA, "cudaSetDevice failed");
@@ -289,7 +292,15 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
         for (int l = 0; l < cfg->n_layers; ++l) nmax = std::max<int64_t>(nmax, cfg->sizes[l]);
         CB = std::min(128, next_pow2(std::max(4, cfg->max_batch)));
         while (CB > 4 && (double)nmax * CB * 4.0 > 1.0 * (double)l2) CB >>= 1;
+        // forward width: the forward gathers a_{l-1} only (no second operand in flight), so a
+        // narrower slab that stays L2-resident pays more than the wider chunk's fewer passes
+        // (C5: 32 columns / 64 MB forward, 64 columns / 128 MB backward)
+        CBf = CB;
+        while (CBf > 32 && (double)nmax * CBf * 4.0 > 0.5 * (double)l2) CBf >>= 1;
     }
+    if (const char* e = std::getenv("SMLP_FWD_CB")) CBf = std::atoi(e);
+    if (CBf > CB || CBf < 4 || (CBf & (CBf - 1)) || (CBf < CB && CBf < 32))
+        return set_err(nullptr, SMLP_E_ARG, "forward chunk width must be a power of two, <= chunk_batch and >= 32 when narrower");
 
     smlp_handle* h = new smlp_handle();
     h->L = cfg->n_layers;
@@ -304,6 +315,8 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     h->max_batch = cfg->max_batch;
     h->CB = CB;
     h->max_chunks = (cfg->max_batch + CB - 1) / CB;
+    h->CBf = CBf;
+    h->max_chunks_f = (cfg->max_batch + CBf - 1) / CBf;
     h->device = cfg->device;
     h->stream = (cudaStream_t)cfg->stream;
     if (cfg->allocator && cfg->allocator->alloc && cfg->allocator->free) {
@@ -584,6 +597,7 @@ int sparse_mlp_info(smlp_handle* h, smlp_info* info) {
     std::memset(info, 0, sizeof(*info));
     info->n_layers = h->L;
     info->chunk_batch = h->CB;
+    info->fwd_chunk_batch = h->CBf;
     info->version = h->version;
     for (int l = 1; l <= h->L; ++l) {
         info->sizes[l - 1] = h->sizes[l - 1];
@@ -701,8 +715,8 @@ int sparse_mlp_import_alive(smlp_handle* h, int32_t l, const uint8_t* alive) {
 
 int sparse_mlp_export_trace(smlp_handle* h, int32_t kind, int32_t l, float* out) {
     if (!h || !out) return SMLP_E_ARG;
-    const int CB = h->CB;
     if (kind == 0 || kind == 1) {
+        const int CB = kind == 0 ? h->CBf : h->CB;   // act: forward layout, delta: backward layout
         if (!valid_layer(h, l, kind == 0 ? 1 : 2)) return set_err(h, SMLP_E_SHAPE, "export_trace: bad layer");
         const int B = h->trace_B;
         if (B < 1) return set_err(h, SMLP_E_STATE, "export_trace: no forward yet");

@@ -11,7 +11,9 @@
 //                        mperm [cap] (canonical index of the entry).
 //   activations        : "chunked transposed": act[l] = [n_chunks][n_l][CB] fp32, CB = chunk_batch
 //                        batch columns per chunk, so one neuron's CB values are one contiguous
-//                        row (CB = 128 -> 512 B, one float4 per lane of a warp).
+//                        row (CB = 128 -> 512 B, one float4 per lane of a warp).  The forward
+//                        tensors (act, zmask, kmask) use their own width CBf <= CB (CB / CBf
+//                        forward chunks per backward chunk); delta uses CB.
 //   masks              : per hidden neuron row and chunk, uint4 = 4 x 32 bits; word c, bit q
 //                        is batch column 4q + c of the chunk (one ballot per float4 lane).
 //   work lists         : per layer, forward segments over mirror rows and backward segments
@@ -111,8 +113,10 @@ struct smlp_handle {
     uint64_t seed = 0;
     int rank = 0;
     int max_batch = 0;
-    int CB = 128;
+    int CB = 128;           // backward chunk width (delta layout)
     int max_chunks = 1;
+    int CBf = 128;          // forward chunk width (act / zmask / kmask layout), CB % CBf == 0
+    int max_chunks_f = 1;
     int device = 0;
     cudaStream_t stream = nullptr;
     smlp_allocator allocator{};

@@ -501,8 +501,8 @@ __global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(F
 // softmax cross-entropy (single block, fixed-order reductions)
 // ------------------------------------------------------------------------------------------
 struct SoftmaxArgs {
-    const float* logits;      // act[L] [nchunks][n_L][CB]
-    float* delta;             // delta[L] same layout
+    const float* logits;      // act[L] [nchunks_f][n_L][CBf]
+    float* delta;             // delta[L] [nchunks][n_L][CB]
     const int32_t* labels;
     const int32_t* y_idx;
     float* loss;              // scalar or null
@@ -511,7 +511,7 @@ struct SoftmaxArgs {
     float* bias_mom;
     float* bias_grad;         // grad view slice (unfused)
     int64_t nL;
-    int B, nchunks, CB;
+    int B, nchunks, CB, CBf;
     int fused;
     float lr, mu;
 };
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(512) softmax_ce_kernel(SoftmaxArgs A) {
     const float invB = 1.0f / (float)A.B;
     for (int b = tid; b < total; b += blockDim.x) {
         const int c = b / A.CB, lb = b % A.CB;
-        const float* zc = A.logits + (int64_t)c * A.nL * A.CB + lb;
+        const float* zc = A.logits + (int64_t)(b / A.CBf) * A.nL * A.CBf + b % A.CBf;
         float* dc = A.delta + (int64_t)c * A.nL * A.CB + lb;
         if (b >= A.B) {
             for (int64_t j = 0; j < A.nL; ++j) dc[j * A.CB] = 0.f;
@@ -536,14 +536,14 @@ __global__ void __launch_bounds__(512) softmax_ce_kernel(SoftmaxArgs A) {
             y = 0;
         }
         float mx = -INFINITY;
-        for (int64_t j = 0; j < A.nL; ++j) mx = fmaxf(mx, zc[j * A.CB]);
+        for (int64_t j = 0; j < A.nL; ++j) mx = fmaxf(mx, zc[j * A.CBf]);
         float s = 0.f;
-        for (int64_t j = 0; j < A.nL; ++j) s += expf(zc[j * A.CB] - mx);
+        for (int64_t j = 0; j < A.nL; ++j) s += expf(zc[j * A.CBf] - mx);
         const float lse = logf(s);
-        lsum += (double)(lse - (zc[(int64_t)y * A.CB] - mx));
+        lsum += (double)(lse - (zc[(int64_t)y * A.CBf] - mx));
         const float inv = 1.0f / s;
         for (int64_t j = 0; j < A.nL; ++j) {
-            const float p = expf(zc[j * A.CB] - mx) * inv;
+            const float p = expf(zc[j * A.CBf] - mx) * inv;
             dc[j * A.CB] = (p - (j == y ? 1.f : 0.f)) * invB;
         }
     }
@@ -589,11 +589,12 @@ __global__ void softmax_probs_kernel(const float* __restrict__ logits, float* __
 // backward (delta SpMM against W^T + SDDMM + fused update)
 // ------------------------------------------------------------------------------------------
 struct BwdArgs {
-    const float* a_prev;      // chunk base [n_in][CB]   (activations of layer l-1)
+    const float* a_prev;      // a_{l-1}, forward layout: base of forward chunk c CB / CBF ([n_in][CBF] each)
     const float* d_out;       // chunk base [n_out][CB]  (delta_l)
     float* d_prev;            // chunk base [n_in][CB]   (delta_{l-1}) or null for l = 2
-    const uint4* zmask_prev;  // chunk base [n_in]
+    const uint4* zmask_prev;  // forward layout: base of forward chunk c CB / CBF ([n_in] each)
     const uint4* kmask_prev;
+    int64_t n_prev;           // n_{l-1}
     const int4* seg;
     const int4* multi;
     const LayerMeta* meta;
@@ -620,21 +621,43 @@ struct BwdArgs {
     int l2hint;                      // L2 policies: gathers evict_last, streamed operands evict_first
 };
 
+// Forward-layout position of a backward chunk's local column lc (CB = R CBF, R in {1, 2, 4}; the
+// chunk base passed is that of forward chunk c R): column lc lives in forward chunk c R + lc / CBF
+// at column off = lc % CBF, so a_{l-1}[i] of it is a_prev[i CBF + aoff] and its mask bits are word
+// off & 3, bit off >> 2 of zmask_prev[i + moff].  With CBF = CB: aoff = lc, moff = 0, the plain
+// layout (compile-time).
+template <int CB, int CBF>
+struct FwdPos {
+    int64_t aoff, moff;
+    int off;
+    __device__ __forceinline__ FwdPos(int lc, int64_t n) {
+        if constexpr (CBF == CB) {
+            aoff = lc; moff = 0; off = lc;
+        } else {
+            off = lc % CBF;
+            moff = (int64_t)(lc / CBF) * n;
+            aoff = moff * CBF + off;
+        }
+    }
+};
+
 // delta_{l-1} of input row i per group: f'(z) from the sign bits, dropout keep bits, store, and
 // the bias gradient of layer l-1 (accumulated across chunks in order).
-template <int CB>
+template <int CB, int CBF>
 __device__ __forceinline__ void bwd_epilogue(const BwdArgs& A, int64_t i, float4 d, bool own, int lane) {
     constexpr int G = CB / 4;
     const int q = lane % G;
     float o[4] = {0.f, 0.f, 0.f, 0.f};
     if (own) {
-        const uint4 zb = A.zmask_prev[i];
+        const FwdPos<CB, CBF> fp(4 * q, A.n_prev);
+        const int qb = fp.off >> 2;
+        const uint4 zb = A.zmask_prev[fp.moff + i];
         uint4 kb = make_uint4(FULL, FULL, FULL, FULL);
-        if (A.dropout_prev) kb = A.kmask_prev[i];
+        if (A.dropout_prev) kb = A.kmask_prev[fp.moff + i];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const bool pos = (word(zb, c) >> q) & 1u;
-            const bool keep = (word(kb, c) >> q) & 1u;
+            const bool pos = (word(zb, c) >> qb) & 1u;
+            const bool keep = (word(kb, c) >> qb) & 1u;
             const float fp = pos ? 1.f : A.neg_slope_prev;
             const float v = comp(d, c) * fp;
             o[c] = A.dropout_prev ? (keep ? v * A.keep_scale_prev : 0.f) : v;
@@ -660,7 +683,7 @@ __device__ __forceinline__ void bwd_epilogue(const BwdArgs& A, int64_t i, float4
 }
 
 
-template <int CB>
+template <int CB, int CBF>
 __global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
     constexpr int G = CB / 4, P = 32 / G;
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;
@@ -677,7 +700,7 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
             const float4 p = ldg4(A.ws + (int64_t)(m.y + t) * CB + q * 4);
             acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
         }
-        bwd_epilogue<CB>(A, m.x, acc, active, lane);
+        bwd_epilogue<CB, CBF>(A, m.x, acc, active, lane);
     }
 }
 
@@ -689,14 +712,14 @@ struct BwdSide {            // per-row operands of the backward epilogue (loaded
     float bgs, bmom, bval;  // lane 0: bias-grad accumulator, bias momentum and bias of neuron i
 };
 template <bool DROP>
-__device__ __forceinline__ BwdSide bwd_side(const BwdArgs& A, int64_t i, bool valid, int lane) {
+__device__ __forceinline__ BwdSide bwd_side(const BwdArgs& A, int64_t i, int64_t moff, bool valid, int lane) {
     BwdSide t;
     t.zb = make_uint4(0, 0, 0, 0);
     t.kb = make_uint4(FULL, FULL, FULL, FULL);
     t.bgs = t.bmom = t.bval = 0.f;
     if (!valid) return t;
-    t.zb = A.zmask_prev[i];
-    if (DROP) t.kb = A.kmask_prev[i];
+    t.zb = A.zmask_prev[moff + i];
+    if (DROP) t.kb = A.kmask_prev[moff + i];
     if (lane == 0) {
         if (!A.first) t.bgs = A.bgs[i];
         if (A.last && A.fused) {
@@ -738,7 +761,7 @@ __device__ __forceinline__ void group_reduce_scatter(float4 v, int g, float (&ou
 // accumulated over chunks in order).  d[r] = component r P + g of the row's sum.
 template <int CB>
 __device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, const float (&d)[RowCfg<CB>::NR],
-                                                  const BwdSide& sd, int lane) {
+                                                  const BwdSide& sd, int qb, int lane) {
     using C = RowCfg<CB>;
     constexpr int G = C::G, P = C::P, NR = C::NR;
     const int g = lane / G, q = lane % G;
@@ -748,8 +771,8 @@ __device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, c
     for (int r = 0; r < NR; ++r) {
         const int c = r * P + g;
         if (c < 4) {
-            const bool pos = (word(zb, c) >> q) & 1u;
-            const bool keep = (word(kb, c) >> q) & 1u;
+            const bool pos = (word(zb, c) >> qb) & 1u;
+            const bool keep = (word(kb, c) >> qb) & 1u;
             const float v = d[r] * (pos ? 1.f : A.neg_slope_prev);
             const float o = A.dropout_prev ? (keep ? v * A.keep_scale_prev : 0.f) : v;
             A.d_prev[i * CB + q * 4 + c] = o;
@@ -807,7 +830,7 @@ __device__ __forceinline__ void bwd_batch(const float* __restrict__ d_out, const
 
 // GOLD: add the gradient accumulated by earlier chunks; UPD: last chunk of the fused path (Eq. 1
 // on (w, v) in place); DROP: dropout on layer l-1
-template <int CB, bool HAS_DPREV, bool GOLD, bool UPD, bool DROP>
+template <int CB, int CBF, bool HAS_DPREV, bool GOLD, bool UPD, bool DROP>
 __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     using C = RowCfg<CB>;
     constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB, S = C::S, NR = C::NR;
@@ -828,11 +851,13 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     if (s_lo >= s_hi) return;
     const int4 none = make_int4(0, 0, 0, -2);
     const uint64_t pg = gather_policy(A.l2hint), ps = stream_policy(A.l2hint);
+    const FwdPos<CB, CBF> fp(4 * q, A.n_prev);   // the lane's 4 columns in the forward layout
     // window + a_{l-1}[i] of a segment into buffer b (cp.async, one segment ahead: no registers held)
     auto prefetch = [&](const int4& sg, int b) {
         window_async(win[b], A.col, A.val, sg.y, sg.z, lane, ps);
-        if (lane < G) cp_async16(smem_u32(&ais[b][lane]), A.a_prev + (int64_t)(sg.w != -2 ? sg.x : 0) * CB + lane * 4,
-                                 sg.w != -2, ps);
+        if (lane < G)
+            cp_async16(smem_u32(&ais[b][lane]), A.a_prev + (int64_t)(sg.w != -2 ? sg.x : 0) * CBF + fp.aoff, sg.w != -2,
+                       ps);
         cp_async_commit();
     };
     int4 cur = A.seg[s_lo];
@@ -854,7 +879,7 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
             gold[r] = GOLD && ok ? ld_hint(A.grad + k, ps) : 0.f;
             mold[r] = UPD && ok ? ld_hint(A.mom + k, ps) : 0.f;
         }
-        const BwdSide sd = bwd_side<DROP>(A, cur.x, HAS_DPREV && cur.w < 0, lane);
+        const BwdSide sd = bwd_side<DROP>(A, cur.x, fp.moff, HAS_DPREV && cur.w < 0, lane);
         cp_async_wait1();
         __syncwarp();
         window_pad(win[buf], n, lane, A.zero_row);
@@ -920,7 +945,7 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
             if (cur.w < 0) {
                 float d[NR];
                 group_reduce_scatter<CB>(dacc, g, d);
-                bwd_rows_epilogue<CB>(A, cur.x, d, sd, lane);
+                bwd_rows_epilogue<CB>(A, cur.x, d, sd, fp.off >> 2, lane);
             } else {
                 dacc = group_allreduce<G>(dacc);
                 if (g == 0) st4(A.ws + (int64_t)cur.w * CB + q * 4, dacc);
@@ -952,13 +977,13 @@ struct NarrowArgs {
     float* val;
     float* mom;
     float* grad;
-    const float* a_prev;      // chunk base [n_in][CB]
-    float* a_out;             // fwd: chunk base [n_out][CB] (logits)
+    const float* a_prev;      // fwd: chunk base [n_in][CBf]; bwd: base of forward chunk c CB / CBf
+    float* a_out;             // fwd: chunk base [n_out][CBf] (logits)
     const float* bias;        // fwd: b_L
     float* ws;                // fwd: [gridDim][NOUT][CB] CTA partials
     const float* d_out;       // bwd: delta_L chunk base [n_out][CB]
     float* d_prev;            // bwd: delta_{L-1} chunk base [n_in][CB]
-    const uint4* zmask_prev;
+    const uint4* zmask_prev;  // bwd: base of forward chunk c CB / CBf
     const uint4* kmask_prev;
     float* bgs;
     float* bias_prev;
@@ -966,6 +991,7 @@ struct NarrowArgs {
     float* bias_grad_prev;
     int64_t n_in;
     int n_out;
+    int ncols;                // fwd: columns present in this launch (<= its width)
     const LayerMeta* meta;    // device nnz: complete layer (nnz = n_in n_out) -> row i = [i n_out, (i+1) n_out)
     float neg_slope_prev;
     float keep_scale_prev;
@@ -1012,13 +1038,18 @@ __device__ __forceinline__ void narrow_row(const NarrowArgs& A, bool dense, int6
     }
 }
 
-template <int CB, int NOUT>
+// The forward covers CB / CBF consecutive forward chunks per launch (CB columns, A.ncols of them
+// present): one pass over the rows and weights for all of them; column b of the launch is column
+// b % CBF of chunk b / CBF (FwdPos).  Each column's sum runs over the same rows in the same order
+// whatever CB, so the logits do not depend on it.
+template <int CB, int CBF, int NOUT>
 __global__ void __launch_bounds__(NARROW_WARPS * 32) fwd_narrow_kernel(NarrowArgs A) {
     constexpr int VEC = CB >= 32 ? CB / 32 : 1;
     constexpr int RU = VEC == 4 ? 4 : 8;
     __shared__ float red[NOUT * CB];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool colok = lane * VEC < CB;
+    const bool colok = lane * VEC < A.ncols;
+    const FwdPos<CB, CBF> fp(colok ? lane * VEC : 0, A.n_in);
     const int64_t r0 = (A.n_in * blockIdx.x) / gridDim.x, r1 = (A.n_in * (blockIdx.x + 1)) / gridDim.x;
     const bool dense = (int64_t)A.meta->nnz == A.n_in * (int64_t)A.n_out;   // graph-stable (device count)
     float acc[NOUT][VEC];
@@ -1044,7 +1075,7 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) fwd_narrow_kernel(NarrowArg
                     cj[r] = __ldg(A.col + beg + lane);
                     w[r] = A.val[beg + lane];
                 }
-                if (colok) ldvec<VEC>(a[r], A.a_prev + i * CB + lane * VEC);
+                if (colok) ldvec<VEC>(a[r], A.a_prev + i * CBF + fp.aoff);
             }
         }
 #pragma unroll
@@ -1079,10 +1110,11 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) fwd_narrow_kernel(NarrowArg
 }
 
 // one warp per logit element e = jj * CB + b: fixed-order sum of the CTA partials (lane-strided,
-// then an xor tree) + b_L
-template <int CB, int NOUT>
+// then an xor tree) + b_L, stored at column b % CBF of forward chunk b / CBF
+template <int CB, int CBF, int NOUT>
 __global__ void __launch_bounds__(32) fwd_narrow_finish_kernel(NarrowArgs A, int nparts) {
     const int e = blockIdx.x, lane = threadIdx.x;
+    if (e % CB >= A.ncols) return;
     // lane b sums parts b, b + 32, ... in order; the loads of 8 parts are issued together (one
     // latency per 8 parts instead of one per part)
     float s = 0.f;
@@ -1098,15 +1130,19 @@ __global__ void __launch_bounds__(32) fwd_narrow_finish_kernel(NarrowArgs A, int
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    if (lane == 0) A.a_out[e] = s + __ldg(A.bias + e / CB);
+    if (lane == 0) {
+        const int jj = e / CB, b = e % CB;
+        A.a_out[((int64_t)(b / CBF) * A.n_out + jj) * CBF + b % CBF] = s + __ldg(A.bias + jj);
+    }
 }
 
-template <int CB, int NOUT>
+template <int CB, int CBF, int NOUT>
 __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_kernel(NarrowArgs A) {
     constexpr int VEC = CB >= 32 ? CB / 32 : 1;
     constexpr int RU = VEC == 4 ? 2 : (VEC == 2 ? 4 : 8);
     const int lane = threadIdx.x & 31;
     const bool colok = lane * VEC < CB;
+    const FwdPos<CB, CBF> fp(colok ? lane * VEC : 0, A.n_in);   // the lane's columns, forward layout
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const bool dense = (int64_t)A.meta->nnz == A.n_in * (int64_t)A.n_out;   // graph-stable (device count)
@@ -1141,10 +1177,10 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_kernel(NarrowArg
                     w[r] = A.val[beg[r] + lane];
                     if (!A.first) gacc[r] = A.grad[beg[r] + lane];
                 }
-                if (colok) ldvec<VEC>(a[r], A.a_prev + i * CB + lane * VEC);
-                if (A.d_prev) {
-                    zb[r] = __ldg(A.zmask_prev + i);
-                    if (A.dropout_prev) kb[r] = __ldg(A.kmask_prev + i);
+                if (colok) ldvec<VEC>(a[r], A.a_prev + i * CBF + fp.aoff);
+                if (A.d_prev && colok) {
+                    zb[r] = __ldg(A.zmask_prev + fp.moff + i);
+                    if (A.dropout_prev) kb[r] = __ldg(A.kmask_prev + fp.moff + i);
                 }
             }
         }
@@ -1190,7 +1226,7 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_kernel(NarrowArg
                 float bsum = 0.f;
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) {
-                    const int b = lane * VEC + v;
+                    const int b = fp.off + v;           // column within its forward chunk
                     const bool pos = (word(zb[r], b & 3) >> (b >> 2)) & 1u;
                     const bool keep = (word(kb[r], b & 3) >> (b >> 2)) & 1u;
                     const float x = dp[v] * (pos ? 1.f : A.neg_slope_prev);
@@ -1225,10 +1261,11 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_kernel(NarrowArg
 // delta_L (n_L x CB) is broadcast from shared memory.  Rows of a dense-capped layer are either
 // complete (j = 0..n_L-1 in order) or empty (outgoing row of a pruned neuron), so entry jj of a
 // row is output jj.  ~10 warp instructions per row instead of ~200 with one row per warp.
-template <int CB, int NOUT>
+template <int CB, int CBF, int NOUT>
 __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_rows_kernel(NarrowArgs A) {
     constexpr int CS = CB < 32 ? CB : 32;     // columns per slice
     constexpr int NS = CB / CS;
+    static_assert(CBF % CS == 0, "a slice lies inside one forward chunk");
     constexpr int TS = CS + 1;                // odd smem row stride: lane-per-row access is conflict-free
     constexpr int C4 = CS / 4;                // float4 per row slice
     __shared__ float dLs[NOUT][CB];
@@ -1255,17 +1292,21 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_rows_kernel(Narr
             g[jj] = 0.f;
         }
         uint4 zb = make_uint4(0, 0, 0, 0), kb = make_uint4(FULL, FULL, FULL, FULL);
-        if (A.d_prev && valid) {
-            zb = __ldg(A.zmask_prev + i);
-            if (A.dropout_prev) kb = __ldg(A.kmask_prev + i);
-        }
         float bsum = 0.f;
         for (int sl = 0; sl < NS; ++sl) {
+            // a slice lies inside one forward chunk (CBF >= min(CB, 32) = CS): its rows and masks
+            const FwdPos<CB, CBF> fp(sl * CS, A.n_in);
+            if (A.d_prev && valid && fp.off == 0) {   // first slice of a forward chunk
+                zb = __ldg(A.zmask_prev + fp.moff + i);
+                if (A.dropout_prev) kb = __ldg(A.kmask_prev + fp.moff + i);
+            }
 #pragma unroll
             for (int m = 0; m < C4; ++m) {        // coalesced: 32 rows x CS columns of a_{L-1}
                 const int e = lane + 32 * m, rr = e / C4, cc = e % C4;
                 const int64_t row = r0 + rr;
-                const float4 v = row < A.n_in ? ldro_f4(A.a_prev + row * CB + sl * CS + 4 * cc, pol_s) : f4zero();
+                const float4 v = row < A.n_in
+                                     ? ldro_f4(A.a_prev + row * CBF + fp.aoff + 4 * cc, pol_s)
+                                     : f4zero();
                 float* d = tl + rr * TS + 4 * cc;
                 d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
             }
@@ -1282,8 +1323,9 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_rows_kernel(Narr
                     g[jj] = fmaf(av, d, g[jj]);           // SDDMM over the chunk's columns
                 }
                 if (A.d_prev) {
-                    const bool pos = (word(zb, b & 3) >> (b >> 2)) & 1u;
-                    const bool keep = (word(kb, b & 3) >> (b >> 2)) & 1u;
+                    const int bf = fp.off + c;            // column within its forward chunk
+                    const bool pos = (word(zb, bf & 3) >> (bf >> 2)) & 1u;
+                    const bool keep = (word(kb, bf & 3) >> (bf >> 2)) & 1u;
                     const float x = dp * (pos ? 1.f : A.neg_slope_prev);
                     const float o = A.dropout_prev ? (keep ? x * A.keep_scale_prev : 0.f) : x;
                     bsum += o;
@@ -1638,14 +1680,14 @@ int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
     return SMLP_OK;
 }
 
-template <int CB>
+template <int CB, int CBF>
 int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev) {
     constexpr int P = 32 / (CB / 4);
     const bool gold = !A.first, upd = A.last && A.fused, drop = A.dropout_prev != 0;
     const int mode = (has_dprev ? 8 : 0) | (gold ? 4 : 0) | (upd ? 2 : 0) | (drop ? 1 : 0);
 #define SMLP_BWD_ROWS(HD, GO, UP, DR)                                                                          \
 case (HD ? 8 : 0) | (GO ? 4 : 0) | (UP ? 2 : 0) | (DR ? 1 : 0):                                         \
-    bwd_rows_kernel<CB, HD, GO, UP, DR><<<rows_grid(h, bwd_rows_kernel<CB, HD, GO, UP, DR>, L.bseg_cap),      \
+    bwd_rows_kernel<CB, CBF, HD, GO, UP, DR><<<rows_grid(h, bwd_rows_kernel<CB, CBF, HD, GO, UP, DR>, L.bseg_cap), \
                                           WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);                      \
     break;
     switch (mode) {
@@ -1667,14 +1709,14 @@ case (HD ? 8 : 0) | (GO ? 4 : 0) | (UP ? 2 : 0) | (DR ? 1 : 0):                 
     SMLP_CK_LAUNCH(h, "bwd_rows_kernel");
     if (has_dprev && L.bslot_cap > 0) {
         const int g2 = persistent_grid(h, std::max<int64_t>(1, L.bslot_cap / 2), P);
-        bwd_finish_kernel<CB><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        bwd_finish_kernel<CB, CBF><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
         SMLP_CK_LAUNCH(h, "bwd_finish_kernel");
     }
     return SMLP_OK;
 }
 
-#define SMLP_DISPATCH_CB(h, fn, ...)                                   \
-    switch ((h)->CB) {                                                 \
+#define SMLP_DISPATCH_CB(h, width, fn, ...)                            \
+    switch (width) {                                                   \
         case 4: return fn<4>(__VA_ARGS__);                             \
         case 8: return fn<8>(__VA_ARGS__);                             \
         case 16: return fn<16>(__VA_ARGS__);                           \
@@ -1684,25 +1726,44 @@ case (HD ? 8 : 0) | (GO ? 4 : 0) | (UP ? 2 : 0) | (DR ? 1 : 0):                 
         default: return set_err((h), SMLP_E_ARG, "unsupported chunk_batch"); \
     }
 
-int dispatch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) { SMLP_DISPATCH_CB(h, launch_fwd, h, A, L); }
-int dispatch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool hd) { SMLP_DISPATCH_CB(h, launch_bwd, h, A, L, hd); }
+// backward kernels: (CB, CBf) pairs -- equal widths, or the forward tensors 2 / 4 times narrower
+// (CBf >= 32, api.cu)
+#define SMLP_DISPATCH_PAIR(h, cb, cbf, fn, ...)                                          \
+    switch ((cb) * 1000 + (cbf)) {                                                       \
+        case 4004: return fn<4, 4>(__VA_ARGS__);                                         \
+        case 8008: return fn<8, 8>(__VA_ARGS__);                                         \
+        case 16016: return fn<16, 16>(__VA_ARGS__);                                      \
+        case 32032: return fn<32, 32>(__VA_ARGS__);                                      \
+        case 64064: return fn<64, 64>(__VA_ARGS__);                                      \
+        case 64032: return fn<64, 32>(__VA_ARGS__);                                      \
+        case 128128: return fn<128, 128>(__VA_ARGS__);                                   \
+        case 128064: return fn<128, 64>(__VA_ARGS__);                                    \
+        case 128032: return fn<128, 32>(__VA_ARGS__);                                    \
+        default: return set_err((h), SMLP_E_ARG, "unsupported (chunk_batch, forward chunk) pair"); \
+    }
 
-template <int CB, int NOUT>
+int dispatch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) { SMLP_DISPATCH_CB(h, h->CBf, launch_fwd, h, A, L); }
+int dispatch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool hd) {
+    SMLP_DISPATCH_PAIR(h, h->CB, h->CBf, launch_bwd, h, A, L, hd);
+}
+
+template <int CB, int CBF, int NOUT>
 int launch_narrow_n(smlp_handle* h, const NarrowArgs& A, const Layer& L, bool fwd) {
     if constexpr (NOUT * CB > NARROW_MAX_ELEMS) {
         return set_err(h, SMLP_E_ARG, "narrow output layer too wide for chunk_batch");
     } else {
         if (fwd) {
-            fwd_narrow_kernel<CB, NOUT><<<L.ngrid, NARROW_WARPS * 32, 0, h->stream>>>(A);
+            fwd_narrow_kernel<CB, CBF, NOUT><<<L.ngrid, NARROW_WARPS * 32, 0, h->stream>>>(A);
             SMLP_CK_LAUNCH(h, "fwd_narrow_kernel");
-            fwd_narrow_finish_kernel<CB, NOUT><<<A.n_out * CB, 32, 0, h->stream>>>(A, L.ngrid);
+            fwd_narrow_finish_kernel<CB, CBF, NOUT><<<A.n_out * CB, 32, 0, h->stream>>>(A, L.ngrid);
             SMLP_CK_LAUNCH(h, "fwd_narrow_finish_kernel");
         } else {
             if constexpr (NOUT <= 16) {
                 if (L.dense) {
                     const int64_t tiles = (A.n_in + 31) / 32;
                     const int64_t blocks = std::min<int64_t>((tiles + NARROW_WARPS - 1) / NARROW_WARPS, (int64_t)h->num_sms * 4);
-                    bwd_narrow_rows_kernel<CB, NOUT><<<(int)std::max<int64_t>(1, blocks), NARROW_WARPS * 32, 0, h->stream>>>(A);
+                    bwd_narrow_rows_kernel<CB, CBF, NOUT>
+                        <<<(int)std::max<int64_t>(1, blocks), NARROW_WARPS * 32, 0, h->stream>>>(A);
                     SMLP_CK_LAUNCH(h, "bwd_narrow_rows_kernel");
                     return SMLP_OK;
                 }
@@ -1711,27 +1772,36 @@ int launch_narrow_n(smlp_handle* h, const NarrowArgs& A, const Layer& L, bool fw
             constexpr int RU = VEC == 4 ? 2 : (VEC == 2 ? 4 : 8);
             const int64_t warps = (A.n_in + RU - 1) / RU;
             const int64_t blocks = std::min<int64_t>((warps + NARROW_WARPS - 1) / NARROW_WARPS, (int64_t)h->num_sms * 3);
-            bwd_narrow_kernel<CB, NOUT><<<(int)std::max<int64_t>(1, blocks), NARROW_WARPS * 32, 0, h->stream>>>(A);
+            bwd_narrow_kernel<CB, CBF, NOUT><<<(int)std::max<int64_t>(1, blocks), NARROW_WARPS * 32, 0, h->stream>>>(A);
             SMLP_CK_LAUNCH(h, "bwd_narrow_kernel");
         }
         return SMLP_OK;
     }
 }
 
-template <int CB>
+// forward: CB = the launch's width (a multiple of CBF = the forward width); backward: the (CB, CBf) pair
+template <int CB, int CBF>
 int launch_narrow(smlp_handle* h, const NarrowArgs& A, const Layer& L, bool fwd) {
     switch (L.nout_pad) {
-        case 2: return launch_narrow_n<CB, 2>(h, A, L, fwd);
-        case 4: return launch_narrow_n<CB, 4>(h, A, L, fwd);
-        case 8: return launch_narrow_n<CB, 8>(h, A, L, fwd);
-        case 16: return launch_narrow_n<CB, 16>(h, A, L, fwd);
-        case 32: return launch_narrow_n<CB, 32>(h, A, L, fwd);
+        case 2: return launch_narrow_n<CB, CBF, 2>(h, A, L, fwd);
+        case 4: return launch_narrow_n<CB, CBF, 4>(h, A, L, fwd);
+        case 8: return launch_narrow_n<CB, CBF, 8>(h, A, L, fwd);
+        case 16: return launch_narrow_n<CB, CBF, 16>(h, A, L, fwd);
+        case 32: return launch_narrow_n<CB, CBF, 32>(h, A, L, fwd);
         default: return set_err(h, SMLP_E_ARG, "narrow layer: bad padded width");
     }
 }
+template <int CB, int CBF>
+int launch_narrow_fwd(smlp_handle* h, const NarrowArgs& A, const Layer& L) { return launch_narrow<CB, CBF>(h, A, L, true); }
+template <int CB, int CBF>
+int launch_narrow_bwd(smlp_handle* h, const NarrowArgs& A, const Layer& L) { return launch_narrow<CB, CBF>(h, A, L, false); }
 
-int dispatch_narrow(smlp_handle* h, const NarrowArgs& A, const Layer& L, bool fwd) {
-    SMLP_DISPATCH_CB(h, launch_narrow, h, A, L, fwd);
+// fwd: `width` columns (CB / CBf forward chunks) per launch; bwd: one backward chunk
+int dispatch_narrow(smlp_handle* h, const NarrowArgs& A, const Layer& L, bool fwd, int width) {
+    if (fwd) {
+        SMLP_DISPATCH_PAIR(h, width, h->CBf, launch_narrow_fwd, h, A, L);
+    }
+    SMLP_DISPATCH_PAIR(h, h->CB, h->CBf, launch_narrow_bwd, h, A, L);
 }
 
 float neg_slope_of(const smlp_handle* h, int l) {
@@ -1754,7 +1824,7 @@ int refresh_mirror_values(smlp_handle* h, Layer& Ly) {
 }
 
 int run_probs(smlp_handle* h, int B, float* probs) {
-    softmax_probs_kernel<<<(B + 127) / 128, 128, 0, h->stream>>>(h->act[h->L], probs, h->sizes[h->L - 1], B, h->CB);
+    softmax_probs_kernel<<<(B + 127) / 128, 128, 0, h->stream>>>(h->act[h->L], probs, h->sizes[h->L - 1], B, h->CBf);
     SMLP_CK_LAUNCH(h, "softmax_probs_kernel");
     return SMLP_OK;
 }
@@ -1810,11 +1880,14 @@ int launch_bits(smlp_handle* h, const BitsArgs& A, const Layer& L2, bool fwd) {
 }
 
 int dispatch_bits(smlp_handle* h, const BitsArgs& A, const Layer& L2, bool fwd) {
-    SMLP_DISPATCH_CB(h, launch_bits, h, A, L2, fwd);
+    SMLP_DISPATCH_CB(h, fwd ? h->CBf : h->CB, launch_bits, h, A, L2, fwd);
 }
 
-NarrowArgs narrow_args(smlp_handle* h, Layer& Ly, int c) {
-    const int CB = h->CB;
+// forward: chunk c of the forward layout; backward: a_{L-1} from forward chunk c CB / CBf (the
+// backward chunk's first columns, FwdPos)
+NarrowArgs narrow_args(smlp_handle* h, Layer& Ly, int c, bool fwd) {
+    const int CB = h->CBf;
+    const int fc = fwd ? c : c * (h->CB / h->CBf);
     const int64_t nin = Ly.n_in, nout = Ly.n_out;
     NarrowArgs A{};
     A.row_ptr = Ly.row_ptr;
@@ -1822,12 +1895,13 @@ NarrowArgs narrow_args(smlp_handle* h, Layer& Ly, int c) {
     A.val = Ly.val;
     A.mom = Ly.mom;
     A.grad = Ly.grad;
-    A.a_prev = h->act[Ly.l - 1] + (int64_t)c * nin * CB;
-    A.a_out = h->act[Ly.l] + (int64_t)c * nout * CB;
+    A.a_prev = h->act[Ly.l - 1] + (int64_t)fc * nin * CB;
+    A.a_out = fwd ? h->act[Ly.l] + (int64_t)c * nout * CB : nullptr;
     A.bias = Ly.bias;
     A.ws = Ly.nws;
     A.n_in = nin;
     A.n_out = (int)nout;
+    A.ncols = CB;
     A.meta = Ly.meta;
     return A;
 }
@@ -1855,7 +1929,7 @@ static void l2_window(smlp_handle* h, const void* base, size_t bytes) {
 
 int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, bool train, uint64_t step,
                 float* probs) {
-    const int CB = h->CB;
+    const int CB = h->CBf;    // the forward tensors' chunk width
     const int nchunks = (B + CB - 1) / CB;
     {
         dim3 grid((unsigned)((h->sizes[0] + 31) / 32), (unsigned)((nchunks * CB + 31) / 32));
@@ -1885,13 +1959,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             const int64_t nin = h->sizes[l - 2], nout = h->sizes[l - 1];
             const int Bc = std::min(CB, B - c * CB);
             const double nnz = (double)Ly.nnz;
-            if (Ly.narrow) {
-                const NarrowArgs A = narrow_args(h, Ly, c);
-                prof_start(h, K_FWD, l, 8.0 * nnz / nchunks + 4.0 * Bc * (double)(nin + nout), 2.0 * nnz * Bc);
-                SMLP_TRY(dispatch_narrow(h, A, Ly, true));
-                prof_stop(h);
-                continue;
-            }
+            if (Ly.narrow) continue;   // after the chunk loop, several chunks per pass
             FwdArgs A{};
             A.a_prev = h->act[l - 1] + (int64_t)c * nin * CB;
             A.a_out = h->act[l] + (int64_t)c * nout * CB;
@@ -1918,12 +1986,30 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             A.step_ptr = h->step_counter;
             A.b0 = c * CB;
             A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
-            A.zero_row = (int)((int64_t)(h->max_chunks - c) * nin);
+            A.zero_row = (int)((int64_t)(h->max_chunks_f - c) * nin);
             A.l2hint = h->l2hint;
             prof_start(h, K_FWD, l, 12.0 * nnz / nchunks + 4.0 * Bc * (double)(nin + nout), 2.0 * nnz * Bc);
             l2_window(h, A.a_prev, (size_t)nin * CB * sizeof(float));
             SMLP_TRY(dispatch_fwd(h, A, Ly));
             l2_window(h, nullptr, 0);
+            prof_stop(h);
+        }
+    }
+    // narrow output layer: one pass over its rows and weights per W columns (W / CBf forward chunks;
+    // the earlier chunks' a_{L-1} slabs come back from HBM, cheaper than one row pass per chunk)
+    if (h->layers[h->L - 2].narrow) {
+        Layer& Ly = h->layers[h->L - 2];
+        const int64_t nin = Ly.n_in, nout = Ly.n_out;
+        int W = CB;
+        if (CB >= 32)
+            while (W < 128 && W < nchunks * CB && (int64_t)Ly.nout_pad * W * 2 <= NARROW_MAX_ELEMS) W *= 2;
+        for (int c = 0; c < nchunks; c += W / CB) {
+            NarrowArgs A = narrow_args(h, Ly, c, true);
+            A.ncols = std::min(W, (nchunks - c) * CB);
+            const int Bc = std::min(A.ncols, B - c * CB);
+            prof_start(h, K_FWD, h->L, 8.0 * (double)Ly.nnz + 4.0 * Bc * (double)(nin + nout),
+                       2.0 * (double)Ly.nnz * Bc);
+            SMLP_TRY(dispatch_narrow(h, A, Ly, true, W));
             prof_stop(h);
         }
     }
@@ -1968,6 +2054,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
         S.B = B;
         S.nchunks = nchunks;
         S.CB = CB;
+        S.CBf = h->CBf;
         S.fused = is_fused ? 1 : 0;
         S.lr = lr;
         S.mu = mu;
@@ -1985,6 +2072,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             Layer& Ly = h->layers[l - 2];
             const int64_t nin = h->sizes[l - 2], nout = h->sizes[l - 1];
             const bool has_dprev = l >= 3;
+            const int fc = c * (CB / h->CBf);                      // first forward chunk of chunk c
             Layer* Lp = has_dprev ? &h->layers[l - 3] : nullptr;   // owner of bias b_{l-1}
             const int Bc = std::min(CB, B - c * CB);
             const double nnz = (double)Ly.nnz;
@@ -1992,11 +2080,11 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             const int dropout_prev = (has_dprev && h->trace_train && h->dropout > 0.f) ? 1 : 0;
             const float keep_scale = (float)(1.0 / (1.0 - (double)h->dropout));
             if (Ly.narrow) {
-                NarrowArgs A = narrow_args(h, Ly, c);
+                NarrowArgs A = narrow_args(h, Ly, c, false);
                 A.d_out = h->delta[l] + (int64_t)c * nout * CB;
                 A.d_prev = has_dprev ? h->delta[l - 1] + (int64_t)c * nin * CB : nullptr;
-                A.zmask_prev = has_dprev ? h->zmask[l - 1] + (int64_t)c * nin : nullptr;
-                A.kmask_prev = has_dprev ? h->kmask[l - 1] + (int64_t)c * nin : nullptr;
+                A.zmask_prev = has_dprev ? h->zmask[l - 1] + (int64_t)fc * nin : nullptr;
+                A.kmask_prev = has_dprev ? h->kmask[l - 1] + (int64_t)fc * nin : nullptr;
                 A.bgs = Ly.bgs;
                 A.bias_prev = Lp ? Lp->bias : nullptr;
                 A.bias_mom_prev = Lp ? Lp->bias_mom : nullptr;
@@ -2012,17 +2100,18 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
                 A.wd = wd;
                 prof_start(h, K_BWD, l, (is_fused ? 20.0 : 12.0) * nnz / nchunks + act_bytes,
                            (has_dprev ? 4.0 : 2.0) * nnz * Bc);
-                SMLP_TRY(dispatch_narrow(h, A, Ly, false));
+                SMLP_TRY(dispatch_narrow(h, A, Ly, false, CB));
                 prof_stop(h);
                 if (last) SMLP_TRY(layer_done(h, l));
                 continue;
             }
             BwdArgs A{};
-            A.a_prev = h->act[l - 1] + (int64_t)c * nin * CB;
+            A.a_prev = h->act[l - 1] + (int64_t)fc * nin * h->CBf;   // forward layout (FwdPos)
             A.d_out = h->delta[l] + (int64_t)c * nout * CB;
             A.d_prev = has_dprev ? h->delta[l - 1] + (int64_t)c * nin * CB : nullptr;
-            A.zmask_prev = has_dprev ? h->zmask[l - 1] + (int64_t)c * nin : nullptr;
-            A.kmask_prev = has_dprev ? h->kmask[l - 1] + (int64_t)c * nin : nullptr;
+            A.zmask_prev = has_dprev ? h->zmask[l - 1] + (int64_t)fc * nin : nullptr;
+            A.kmask_prev = has_dprev ? h->kmask[l - 1] + (int64_t)fc * nin : nullptr;
+            A.n_prev = nin;
             A.seg = Ly.bseg;
             A.multi = Ly.bmulti;
             A.meta = Ly.meta;

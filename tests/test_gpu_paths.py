@@ -56,13 +56,18 @@ def _check_step(g, st, x, y, step, cfg, path_flag):
     return tr, gr
 
 
-@pytest.mark.parametrize("B,chunk,dropout", [(128, 0, 0.0), (128, 32, 0.3), (100, 32, 0.0), (37, 8, 0.3)])
-def test_binary_input_path_parity(B, chunk, dropout):
+@pytest.mark.parametrize("B,chunk,fchunk,dropout", [(128, 0, None, 0.0), (128, 32, None, 0.3), (100, 32, None, 0.0),
+                                                    (37, 8, None, 0.3), (128, 128, 32, 0.3), (100, 64, 32, 0.0)])
+def test_binary_input_path_parity(B, chunk, fchunk, dropout, monkeypatch):
     from paper_2102_01732_b200 import SGD
     torch = _torch()
     cfg = _binary_cfg(batch=B, dropout=dropout)
+    if fchunk:
+        monkeypatch.setenv("SMLP_FWD_CB", str(fchunk))
     g, st = pair(cfg, max_batch=B, chunk_batch=chunk)
-    X, Y = _binary_data(4 * B, cfg.sizes[0], seed=B + chunk)
+    if fchunk:
+        assert g.info()["fwd_chunk_batch"] == fchunk
+    X, Y = _binary_data(4 * B, cfg.sizes[0], seed=B + chunk + (fchunk or 0))
     sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay)
     for s in range(3):
         x, y = X[s * B:(s + 1) * B], Y[s * B:(s + 1) * B]
@@ -138,7 +143,8 @@ def test_generic_output_layer_parity():
 # ----------------------------------------------------------------------------------------- C5 full size
 def test_c5_full_size_sampled_parity():
     """BASELINE configs[4] at full size (65536-500000-500000-500000-2, 52.3M connections) in the
-    bench launch configuration (B = 128, chunk_batch auto = 64 -> 2 chunks, binary-input path, fused
+    bench launch configuration (B = 128, chunk_batch auto = 64 -> 2 backward chunks, forward tensors
+    32 wide -> 4 forward chunks, binary-input path, fused
     update).  Checked: ER topology and values bit-exact (all 52.3M), every forward activation and
     logit of the batch, and for seeded samples of connections / neurons of every layer the
     gradient (unfused) and the Eq. 1 update (fused) against the oracle's cone evaluation."""
@@ -148,7 +154,7 @@ def test_c5_full_size_sampled_parity():
     torch = _torch()
     cfg = get_config("C5")
     g, st = pair(cfg)
-    assert g.info()["chunk_batch"] == 64
+    assert (g.info()["chunk_batch"], g.info()["fwd_chunk_batch"]) == (64, 32)
     assert_topology_equal(g, st, "C5 init")
     for Ly in st.layers:
         e = g.export_layer(Ly.l)
@@ -207,20 +213,34 @@ def test_c5_full_size_sampled_parity():
         assert rel_err(e["v"][ent[l]][ok], Ly.v[ent[l]][ok]) <= TOL, ("v", l)
 
 
-@pytest.mark.parametrize("chunk,B,dropout", [(8, 29, 0.2), (16, 64, 0.0), (32, 77, 0.3), (64, 128, 0.0),
-                                             (128, 128, 0.2)])
-def test_long_rows_and_chunk_widths_parity(chunk, B, dropout):
+# salt: data seed chosen (by the oracle alone) so that no pre-activation of the checked steps
+# sits within rounding of a kink (R30)
+@pytest.mark.parametrize("chunk,fchunk,B,dropout,eps,salt",
+                         [(8, 8, 29, 0.2, 40.0, 0), (16, 16, 64, 0.0, 40.0, 1), (32, 32, 77, 0.3, 40.0, 0),
+                          (64, 64, 128, 0.0, 40.0, 0), (128, 128, 128, 0.2, 40.0, 0),
+                          # mixed layout: forward tensors CBf wide, deltas CB wide (ragged both ways)
+                          (64, 32, 100, 0.3, 40.0, 0), (128, 32, 128, 0.2, 40.0, 0), (128, 64, 77, 0.0, 40.0, 0),
+                          # sparse narrow output layer (bwd_narrow_kernel instead of the dense-capped rows kernel)
+                          (64, 64, 90, 0.2, 5.0, 0), (64, 32, 90, 0.2, 5.0, 0), (128, 32, 128, 0.0, 5.0, 0),
+                          # 3 forward chunks: the output layer's forward pass covers 96 of its 128 columns
+                          (64, 32, 70, 0.2, 5.0, 0), (128, 32, 70, 0.0, 40.0, 0)])
+def test_long_rows_and_chunk_widths_parity(chunk, fchunk, B, dropout, eps, salt, monkeypatch):
     """Rows longer than one 64-entry segment in both orientations (partials + fixed-order finish
     kernels), every chunk width of the row kernels (slot / group layouts, ragged last chunk), the
-    unfused and the fused (Eq. 1 in the backward) update paths."""
+    mixed forward / backward chunk widths (SMLP_FWD_CB), the unfused and the fused (Eq. 1 in the
+    backward) update paths."""
     from paper_2102_01732_b200 import SGD
     torch = _torch()
     # W^(2) 30 x 200 is dense-capped (canonical rows of 200 entries: 4 segments); W^(3) 200 x 150
     # at eps 40 has ~70-entry canonical rows and ~93-entry mirror rows
-    cfg = get_config("C1", sizes=(30, 200, 150, 10), epsilon=40.0, alpha=0.6, dropout=dropout, batch=B)
+    cfg = get_config("C1", sizes=(30, 200, 150, 10), epsilon=eps, alpha=0.6, dropout=dropout, batch=B)
+    monkeypatch.setenv("SMLP_FWD_CB", str(fchunk))
     g, st = pair(cfg, max_batch=B, chunk_batch=chunk)
-    assert max(np.diff(st.layers[1].row_ptr)) > 64
-    rng = np.random.default_rng([chunk, B])
+    assert (g.info()["chunk_batch"], g.info()["fwd_chunk_batch"]) == (chunk, fchunk)
+    assert st.layers[-1].dense_capped == (eps == 40.0)
+    if eps == 40.0:
+        assert max(np.diff(st.layers[1].row_ptr)) > 64
+    rng = np.random.default_rng([chunk, B, salt])
     X = rng.standard_normal((3 * B, 30)).astype(np.float32)
     Y = rng.integers(0, 10, size=3 * B).astype(np.int32)
     sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay)
