@@ -431,9 +431,11 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": cfg.name, "stand_in_for": cfg.stand_in_for, "global_batch": B * world,
                            "step_path": "dp: unfused bwd + per-layer overlapped allreduce + Eq.1 kernel" if dp_path
-                           else "1 GPU: Eq.1 fused into the backward",
+                           else "1 GPU: sparse_mlp_backward with SGD (gradient, then the streaming Eq.1 pass "
+                           "and mirror refresh inside the same call)",
                            "batch_per_rank": B, "layer_sizes": list(cfg.sizes), "epsilon": cfg.epsilon,
                            "nnz": sum(nnz), "chunk_batch": info0["chunk_batch"],
+                           "fwd_chunk_batch": info0["fwd_chunk_batch"],
                            "parallelism": f"dp{world}", "l2_flush": "inputs larger than L2 (resident shard "
                            f"{X.numel() * 4 / 1e9:.1f} GB; per-step traffic {step_bytes / 1e9:.2f} GB)",
                            "create_s": round(t_create, 2), "cuda_graph": graph_note},

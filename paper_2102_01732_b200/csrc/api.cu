@@ -328,6 +328,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     if (const char* e = std::getenv("SMLP_L2HINT")) h->l2hint = std::atoi(e);
     if (const char* e = std::getenv("SMLP_L2PERSIST")) h->l2persist = std::atoi(e);
     if (const char* e = std::getenv("SMLP_FUSED_UPDATE")) h->fused_update = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMLP_OVERLAP_UPDATE")) h->overlap_update = std::atoi(e) != 0;
     const int rc = build_handle(h, cfg);
     if (rc != SMLP_OK) {
         g_create_error = h->err;
@@ -445,11 +446,15 @@ int sparse_mlp_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_
         // measured faster than applying Eq. 1 inside the last chunk's backward: the
         // backward only accumulates the gradient, then one streaming Eq. 1 pass over the whole
         // view (grad_scale 1) and the mirror refresh
-        rc = run_backward(h, labels, y_idx, loss, nullptr);
-        if (rc == SMLP_OK) {
-            smlp_sgd f = *fused;
-            f.grad_scale = 1.f;
-            rc = run_step(h, &f);
+        smlp_sgd f = *fused;
+        f.grad_scale = 1.f;
+        if (h->overlap_update) {
+            // each layer's Eq. 1 slice + mirror refresh start on the aux stream as soon as its
+            // gradient is final, overlapping the rest of the backward; the biases and the join last
+            rc = run_backward(h, labels, y_idx, loss, nullptr, &f);
+        } else {
+            rc = run_backward(h, labels, y_idx, loss, nullptr);
+            if (rc == SMLP_OK) rc = run_step(h, &f);
         }
     } else {
         rc = run_backward(h, labels, y_idx, loss, fused);

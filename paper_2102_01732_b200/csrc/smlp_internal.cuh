@@ -166,10 +166,15 @@ struct smlp_handle {
     std::vector<smlp::ProfRec> prof_recs;
     std::vector<cudaEvent_t> ev_pool;
     int num_sms = 148;
-    int mirror_scatter = 0;
-    int l2hint = 1;                 // tuning knob (env SMLP_L2HINT): L2 eviction policies in the row kernels (on: +0.4%)
-    int l2persist = 0;
-    int fused_update = 0;           // tuning knob (env SMLP_FUSED_UPDATE): Eq. 1 inside the last chunk's backward              // tuning knob (env SMLP_L2PERSIST, percent): persisting-L2 window on gathered slabs                 // tuning knob (env SMLP_L2HINT): L2 eviction policies in the row kernels         // tuning knob (env SMLP_MIRROR_SCATTER): fused update scatters into mval      // tuning knob (env SMLP_GATHER_EVICT_LAST): L2 policy of row gathers
+    // tuning knobs (env, read at create; DESIGN.md §5 has the measurements)
+    int mirror_scatter = 0;         // SMLP_MIRROR_SCATTER: the in-backward Eq. 1 also scatters w into mval
+    int l2hint = 1;                 // SMLP_L2HINT: L2 eviction policies in the row kernels (on: +0.4%)
+    int l2persist = 0;              // SMLP_L2PERSIST (percent): persisting-L2 window on the gathered slabs
+    int fused_update = 0;           // SMLP_FUSED_UPDATE: Eq. 1 inside the last chunk's backward
+    int overlap_update = 0;         // SMLP_OVERLAP_UPDATE: each layer's Eq. 1 pass + mirror refresh on the
+                                    // aux stream as soon as its gradient is final (overlaps the backward;
+                                    // C5: 6.040 -> 6.025 ms, the backward kernels slow down by what the
+                                    // update saves -- all of it is memory-bound)
     int64_t launches = 0;
     std::string err;
 };
@@ -288,7 +293,7 @@ int launch_grid(const smlp_handle* h, int64_t items, int threads);
 int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, bool train,
                 uint64_t step, float* probs);
 int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss,
-                 const smlp_sgd* fused);
+                 const smlp_sgd* fused, const smlp_sgd* overlap_sgd = nullptr);
 int run_step(smlp_handle* h, const smlp_sgd* sgd);
 int refresh_mirror_values(smlp_handle* h, Layer& Ly);
 

@@ -101,6 +101,22 @@ __device__ __forceinline__ float ld_hint(const float* p, uint64_t pol) {
 __device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
 }
+__device__ __forceinline__ float4 ld4_hint(const float* p, uint64_t pol) {   // coherent (read-write data)
+    float4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st4_hint(float* p, float4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+                 ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+__device__ __forceinline__ int4 ldi4_hint(const int32_t* p, uint64_t pol) {
+    int4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
 __device__ __forceinline__ uint64_t gather_policy(int hint) { return hint ? policy_evict_last() : policy_evict_normal(); }
 __device__ __forceinline__ uint64_t stream_policy(int hint) { return hint ? policy_evict_first() : policy_evict_normal(); }
 
@@ -1629,22 +1645,59 @@ __global__ void grad_from_mirror_kernel(const int32_t* __restrict__ nonbinary, c
 // ------------------------------------------------------------------------------------------
 // a6 standalone: Eq. 1 over the whole grad view (K > 1 path), then the mirror refresh
 // ------------------------------------------------------------------------------------------
-__global__ void sgd_update_kernel(float* __restrict__ w, float* __restrict__ v, const float* __restrict__ g,
-                                  int64_t n, int64_t bias_base, float lr, float mu, float wd, float gs) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const float wk = w[k];
-        const float lam = k < bias_base ? wd : 0.f;
-        const float vk = mu * v[k] - lr * (gs * g[k] + lam * wk);
-        v[k] = vk;
-        w[k] = wk + vk;
+// Eq. 1 over one parameter slice (lam = weight decay, 0 for biases), 4 parameters per thread and
+// two float4 groups in flight per iteration.  g and v are streamed once (evict_first); w is kept
+// (evict_last): the mirror gather of the same layer reads it right after.
+__global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w, float* __restrict__ v,
+                                                          const float* __restrict__ g, int64_t n, float lr,
+                                                          float mu, float lam, float gs) {
+    const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+    const int64_t n4 = n >> 2;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    auto upd = [&](float4 wk, float4 vk, float4 gk) {
+        float4 o;
+        o.x = mu * vk.x - lr * (gs * gk.x + lam * wk.x);
+        o.y = mu * vk.y - lr * (gs * gk.y + lam * wk.y);
+        o.z = mu * vk.z - lr * (gs * gk.z + lam * wk.z);
+        o.w = mu * vk.w - lr * (gs * gk.w + lam * wk.w);
+        return o;
+    };
+    int64_t k = tid;
+    for (; k + stride < n4; k += 2 * stride) {
+        const int64_t k2 = k + stride;
+        const float4 w0 = ld4_hint(w + 4 * k, pl), v0 = ld4_hint(v + 4 * k, pf), g0 = ldg4_hint(g + 4 * k, pf);
+        const float4 w1 = ld4_hint(w + 4 * k2, pl), v1 = ld4_hint(v + 4 * k2, pf), g1 = ldg4_hint(g + 4 * k2, pf);
+        const float4 a = upd(w0, v0, g0), b = upd(w1, v1, g1);
+        st4_hint(v + 4 * k, a, pf);
+        st4_hint(w + 4 * k, make_float4(w0.x + a.x, w0.y + a.y, w0.z + a.z, w0.w + a.w), pl);
+        st4_hint(v + 4 * k2, b, pf);
+        st4_hint(w + 4 * k2, make_float4(w1.x + b.x, w1.y + b.y, w1.z + b.z, w1.w + b.w), pl);
+    }
+    if (k < n4) {
+        const float4 w0 = ld4_hint(w + 4 * k, pl), v0 = ld4_hint(v + 4 * k, pf), g0 = ldg4_hint(g + 4 * k, pf);
+        const float4 a = upd(w0, v0, g0);
+        st4_hint(v + 4 * k, a, pf);
+        st4_hint(w + 4 * k, make_float4(w0.x + a.x, w0.y + a.y, w0.z + a.z, w0.w + a.w), pl);
+    }
+    if (tid < n - 4 * n4) {   // tail (n % 4 parameters)
+        const int64_t t = 4 * n4 + tid;
+        const float wk = w[t], vk = mu * v[t] - lr * (gs * g[t] + lam * wk);
+        v[t] = vk;
+        w[t] = wk + vk;
     }
 }
 
-__global__ void mirror_values_kernel(const float* __restrict__ val, const int32_t* __restrict__ mperm,
-                                     const LayerMeta* __restrict__ meta, float* __restrict__ mval) {
-    const int64_t n = meta->nnz;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
-        mval[t] = __ldg(val + __ldg(mperm + t));
+// mirror copy mval[t] = val[mperm[t]], 4 consecutive t per thread (4 independent gathers in flight)
+__global__ void __launch_bounds__(256) mirror_values_kernel(const float* __restrict__ val, const int32_t* __restrict__ mperm,
+                                                            const LayerMeta* __restrict__ meta, float* __restrict__ mval) {
+    const uint64_t pf = policy_evict_first();
+    const int64_t n = meta->nnz, n4 = n >> 2;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = tid; t < n4; t += stride) {
+        const int4 p = ldi4_hint(mperm + 4 * t, pf);
+        st4_hint(mval + 4 * t, make_float4(__ldg(val + p.x), __ldg(val + p.y), __ldg(val + p.z), __ldg(val + p.w)), pf);
+    }
+    if (tid < n - 4 * n4) mval[4 * n4 + tid] = __ldg(val + __ldg(mperm + 4 * n4 + tid));
 }
 
 int persistent_grid(const smlp_handle* h, int64_t groups, int groups_per_warp) {
@@ -1818,7 +1871,7 @@ uint32_t drop_threshold(float rate) {
 
 int refresh_mirror_values(smlp_handle* h, Layer& Ly) {
     if (Ly.cap == 0) return SMLP_OK;
-    mirror_values_kernel<<<launch_grid(h, Ly.cap, 256), 256, 0, h->stream>>>(Ly.val, Ly.mperm, Ly.meta, Ly.mval);
+    mirror_values_kernel<<<launch_grid(h, (Ly.cap + 3) / 4, 256), 256, 0, h->stream>>>(Ly.val, Ly.mperm, Ly.meta, Ly.mval);
     SMLP_CK_LAUNCH(h, "mirror_values_kernel");
     return SMLP_OK;
 }
@@ -2022,6 +2075,41 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
     return SMLP_OK;
 }
 
+// Eq. 1 over the parameter slice [lo, hi) on `stream`: one resident wave (8 CTAs of 256 per SM),
+// two float4 groups per thread and iteration
+static int launch_update(smlp_handle* h, cudaStream_t stream, int64_t lo, int64_t hi, bool decay, const smlp_sgd* sgd) {
+    if (hi <= lo) return SMLP_OK;
+    constexpr int threads = 256;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((hi - lo + 4 * threads - 1) / (4 * threads),
+                                                                 (int64_t)h->num_sms * 8));
+    sgd_update4_kernel<<<grid, threads, 0, stream>>>(h->param + lo, h->mom + lo, h->grad + lo, hi - lo, sgd->lr,
+                                                     sgd->momentum, decay ? sgd->weight_decay : 0.f, sgd->grad_scale);
+    SMLP_CK_LAUNCH(h, "sgd_update4_kernel");
+    return SMLP_OK;
+}
+
+static int ensure_aux(smlp_handle* h) {
+    if (h->aux_stream) return SMLP_OK;
+    SMLP_CK(h, cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking));
+    for (auto& e : h->aux_ev) SMLP_CK(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return SMLP_OK;
+}
+
+// W^(l)'s gradient is final: its Eq. 1 slice and its mirror refresh go to the aux stream, behind
+// everything the main stream has enqueued so far (the backward of the layers below continues)
+static int overlap_layer_update(smlp_handle* h, Layer& Ly, const smlp_sgd* sgd) {
+    SMLP_TRY(ensure_aux(h));
+    SMLP_CK(h, cudaEventRecord(h->aux_ev[0], h->stream));
+    SMLP_CK(h, cudaStreamWaitEvent(h->aux_stream, h->aux_ev[0], 0));
+    SMLP_TRY(launch_update(h, h->aux_stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd));
+    if (!Ly.narrow) {   // narrow layers never read the mirror copy
+        mirror_values_kernel<<<launch_grid(h, (Ly.cap + 3) / 4, 256), 256, 0, h->aux_stream>>>(Ly.val, Ly.mperm,
+                                                                                               Ly.meta, Ly.mval);
+        SMLP_CK_LAUNCH(h, "mirror_values_kernel");
+    }
+    return SMLP_OK;
+}
+
 // W^(l)'s gradient (and b_{l-1}'s) is final: record the layer event (sparse_mlp_wait_layer lets a
 // communication stream start that layer's allreduce while the backward continues)
 static int layer_done(smlp_handle* h, int l) {
@@ -2030,7 +2118,8 @@ static int layer_done(smlp_handle* h, int l) {
     return SMLP_OK;
 }
 
-int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, const smlp_sgd* fused) {
+int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, const smlp_sgd* fused,
+                 const smlp_sgd* overlap_sgd) {
     const int CB = h->CB;
     const int B = h->trace_B;
     const int nchunks = (B + CB - 1) / CB;
@@ -2103,6 +2192,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
                 SMLP_TRY(dispatch_narrow(h, A, Ly, false, CB));
                 prof_stop(h);
                 if (last) SMLP_TRY(layer_done(h, l));
+                if (last && overlap_sgd) SMLP_TRY(overlap_layer_update(h, Ly, overlap_sgd));
                 continue;
             }
             BwdArgs A{};
@@ -2153,6 +2243,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
                 prof_stop(h);
             }
             if (last) SMLP_TRY(layer_done(h, l));
+            if (last && overlap_sgd && !(l == 2 && h->xbits)) SMLP_TRY(overlap_layer_update(h, Ly, overlap_sgd));
         }
     }
     if (h->xbits) {   // binary-input layer 2 (returns at once if not binary)
@@ -2173,6 +2264,14 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             prof_stop(h);
         }
         SMLP_TRY(layer_done(h, 2));
+        if (overlap_sgd) SMLP_TRY(overlap_layer_update(h, L2, overlap_sgd));
+    }
+    if (overlap_sgd) {   // the biases (no weight decay), then join the aux stream
+        prof_start(h, K_SGD, 0, 20.0 * (double)(h->param_count - h->bias_base), 0.0);
+        SMLP_TRY(launch_update(h, h->stream, h->bias_base, h->param_count, false, overlap_sgd));
+        SMLP_CK(h, cudaEventRecord(h->aux_ev[1], h->aux_stream));
+        SMLP_CK(h, cudaStreamWaitEvent(h->stream, h->aux_ev[1], 0));
+        prof_stop(h);
     }
     return SMLP_OK;
 }
@@ -2181,21 +2280,9 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
     // Eq. 1 per layer slice on the handle's stream; each layer's mirror refresh (a gather, bound by
     // L2 requests rather than HBM bytes) runs on a side stream as soon as that slice is updated, so
     // it overlaps the next slice's streaming update
-    const int threads = 256;
     const int64_t n = h->param_count;
-    if (!h->aux_stream) {
-        SMLP_CK(h, cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking));
-        for (auto& e : h->aux_ev) SMLP_CK(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    auto update = [&](int64_t lo, int64_t hi, bool decay) -> int {
-        if (hi <= lo) return SMLP_OK;
-        const int grid = (int)std::min<int64_t>((hi - lo + threads - 1) / threads, (int64_t)h->num_sms * 16);
-        sgd_update_kernel<<<grid, threads, 0, h->stream>>>(h->param + lo, h->mom + lo, h->grad + lo, hi - lo,
-                                                           decay ? hi - lo : 0, sgd->lr, sgd->momentum,
-                                                           sgd->weight_decay, sgd->grad_scale);
-        SMLP_CK_LAUNCH(h, "sgd_update_kernel");
-        return SMLP_OK;
-    };
+    SMLP_TRY(ensure_aux(h));
+    auto update = [&](int64_t lo, int64_t hi, bool decay) { return launch_update(h, h->stream, lo, hi, decay, sgd); };
     prof_start(h, K_SGD, 0, 20.0 * (double)n, 0.0);
     bool side = false;
     for (auto& Ly : h->layers) {
@@ -2203,7 +2290,7 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
         if (Ly.narrow) continue;                                   // narrow layers never read the mirror copy
         SMLP_CK(h, cudaEventRecord(h->aux_ev[0], h->stream));
         SMLP_CK(h, cudaStreamWaitEvent(h->aux_stream, h->aux_ev[0], 0));
-        mirror_values_kernel<<<launch_grid(h, Ly.cap, 256), 256, 0, h->aux_stream>>>(Ly.val, Ly.mperm, Ly.meta,
+        mirror_values_kernel<<<launch_grid(h, (Ly.cap + 3) / 4, 256), 256, 0, h->aux_stream>>>(Ly.val, Ly.mperm, Ly.meta,
                                                                                      Ly.mval);
         SMLP_CK_LAUNCH(h, "mirror_values_kernel");
         side = true;
