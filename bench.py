@@ -102,7 +102,7 @@ def load_data(cfg, rank, world, device):
     from paper_2102_01732_b200.dp import shard_bounds
     from synth.data import c5_device_dataset, make_dataset
     lo, hi = shard_bounds(cfg.n_samples, rank, world)
-    if cfg.name == "C5":
+    if cfg.binary_input:
         return c5_device_dataset(cfg, hi - lo, device, seed_offset=rank)
     X, Y = make_dataset(cfg, n=hi)
     return (torch.from_numpy(np.ascontiguousarray(X[lo:hi])).to(device),
@@ -124,7 +124,7 @@ def cpu_baseline_job(cfg_name: str, batch: int, steps: int) -> dict:
     st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed)
     t_init = time.perf_counter() - t0
     n = batch * steps
-    X, Y = (c5_host_rows(cfg, np.arange(n)) if cfg.name == "C5" else make_dataset(cfg, n=n))
+    X, Y = (c5_host_rows(cfg, np.arange(n)) if cfg.binary_input else make_dataset(cfg, n=n))
     t0 = time.perf_counter()
     for s in range(steps):
         sl = slice(s * batch, (s + 1) * batch)
@@ -143,7 +143,7 @@ def run_reference(args):
         return 0
     from synth import get_config
     cfg = get_config(args.config)
-    sample_B = min(cfg.batch, 8) if cfg.name in ("C5", "C3") else cfg.batch
+    sample_B = min(cfg.batch, 8) if (cfg.binary_input or cfg.name == "C3") else cfg.batch
     warm = max(0, min(args.warmup, 1))
     res = cpu_baseline_job(cfg.name, sample_B, args.steps + warm)
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
@@ -197,8 +197,8 @@ def main():
         import concurrent.futures as cf
         import multiprocessing as mp
         ex = cf.ProcessPoolExecutor(1, mp_context=mp.get_context("spawn"))
-        cpu_B = min(B, 8) if cfg.name in ("C5", "C3") else B
-        cpu_fut = ex.submit(cpu_baseline_job, cfg.name, cpu_B, 2 if cfg.name == "C5" else 20)
+        cpu_B = min(B, 8) if (cfg.binary_input or cfg.name == "C3") else B
+        cpu_fut = ex.submit(cpu_baseline_job, cfg.name, cpu_B, 2 if cfg.binary_input else 20)
 
     t0 = time.perf_counter()
     model = SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed,
@@ -359,7 +359,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         nb = 4
-        if cfg.name == "C5":
+        if cfg.binary_input:
             from synth.data import c5_host_rows
             Xh, Yh = c5_host_rows(cfg, np.arange(rank * nb * B, (rank + 1) * nb * B))
         else:

@@ -87,7 +87,8 @@ typedef struct {
                                     while the widest layer's slab n_l x CB x 4 B exceeds the
                                     L2; the forward tensors (a_l, masks) then use their own
                                     width CBf <= CB, halved (not below 32) while the slab
-                                    exceeds half the L2.  Explicit: CBf = CB.  Env
+                                    exceeds half the L2; if not even a 32-column slab fits
+                                    the L2, CB = CBf = the widest.  Explicit: CBf = CB.  Env
                                     SMLP_FWD_CB overrides CBf (power of 2, <= CB, >= 32 if
                                     narrower; else SMLP_E_ARG)                               */
     int32_t        device;       /* CUDA device ordinal                                       */

@@ -290,13 +290,19 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
         if (l2 <= 0) l2 = 126 << 20;
         int64_t nmax = 0;
         for (int l = 0; l < cfg->n_layers; ++l) nmax = std::max<int64_t>(nmax, cfg->sizes[l]);
-        CB = std::min(128, next_pow2(std::max(4, cfg->max_batch)));
+        const int widest = std::min(128, next_pow2(std::max(4, cfg->max_batch)));
+        CB = widest;
         while (CB > 4 && (double)nmax * CB * 4.0 > 1.0 * (double)l2) CB >>= 1;
         // forward width: the forward gathers a_{l-1} only (no second operand in flight), so a
         // narrower slab that stays L2-resident pays more than the wider chunk's fewer passes
         // (C5: 32 columns / 64 MB forward, 64 columns / 128 MB backward)
         CBf = CB;
         while (CBf > 32 && (double)nmax * CBf * 4.0 > 0.5 * (double)l2) CBf >>= 1;
+        // layers so wide that not even a 32-column slab fits the L2 (Table 4 widths, >= 1M
+        // neurons): the gathers miss either way, so the widest chunk (fewest passes over the
+        // indices, longest rows per gather) wins -- T2 / T3 (2.5M / 5M): 9.2 / 18.7 ms at 128
+        // columns against 11.1 / 22.5 at 64 and 14.5 / 29.3 at 32
+        if (widest >= 32 && (double)nmax * 32 * 4.0 > 1.0 * (double)l2) CB = CBf = widest;
     }
     if (const char* e = std::getenv("SMLP_FWD_CB")) CBf = std::atoi(e);
     if (CBf > CB || CBf < 4 || (CBf & (CBf - 1)) || (CBf < CB && CBf < 32))

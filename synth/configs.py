@@ -31,6 +31,7 @@ class WorkloadConfig:
     prune_percentile: float = 5.0   # rho (Supp. C)
     prune_every: int = 1            # p
     prune_start: int = 0            # tau (paper: 200; C3 uses 0 so it fires in short runs)
+    binary_input: bool = False      # inputs in {0, 1}, Bernoulli(0.05), stored fp32 (C5 and the Table 4 rows)
     data_seed: int = 0
     model_seed: int = 0
 
@@ -78,8 +79,26 @@ CONFIGS = {
     "C5": _cfg(5, name="C5", stand_in_for="make_classification 65536-feature set (PAPER.md:409)",
                sizes=(65536, 500000, 500000, 500000, 2), epsilon=20.0, alpha=0.5,
                dropout=0.0, init="he_uniform", batch=128, lr=0.01,
-               n_samples=100_000, epochs=1),
+               n_samples=100_000, epochs=1, binary_input=True),
 }
+
+# Width scaling: the five architectures of the paper's Table 4
+# ("65536-5M x 4-2" = four hidden layers of 5M neurons), trained there on a
+# 10000 x 65536 make_classification set, 70% train, batch 128, lr 0.01, momentum
+# 0.9, dropout 0.4.  Stand-in data: the C5 binary recipe (Bernoulli(0.05) features, linear
+# teacher), 7000 training rows.  alpha / init / weight decay as C5 (the paper gives none for them).
+_T4_ROWS = {
+    "T1": ((65536, 500_000, 500_000, 2), 10.0),
+    "T2": ((65536, 2_500_000, 2_500_000, 2), 5.0),
+    "T3": ((65536, 5_000_000, 5_000_000, 2), 5.0),
+    "T4": ((65536,) + (5_000_000,) * 4 + (2,), 1.0),
+    "T5": ((65536,) + (5_000_000,) * 10 + (2,), 1.0),
+}
+for _k, (_name, (_sizes, _eps)) in enumerate(_T4_ROWS.items()):
+    CONFIGS[_name] = _cfg(10 + _k, name=_name, stand_in_for=f"Table 4 row {_k + 1} (PAPER.md:426-434), "
+                          "make_classification 65536-feature set (PAPER.md:409)",
+                          sizes=_sizes, epsilon=_eps, alpha=0.5, dropout=0.4, init="he_uniform", batch=128,
+                          lr=0.01, n_samples=7000, epochs=1, binary_input=True)
 
 
 def get_config(name: str, **overrides) -> WorkloadConfig:

@@ -50,7 +50,7 @@ def _params(cfg: WorkloadConfig):
         probe = np.random.default_rng([cfg.data_seed, 424242]).standard_normal((200_000, d))
         thr = float(np.median(np.tanh(probe @ U) @ v))
         return {"U": U, "v": v, "thr": thr}
-    if cfg.name == "C5":
+    if cfg.binary_input:
         r = np.zeros(d)
         k = d // 20
         pos = rng.choice(d, size=k, replace=False)
@@ -84,7 +84,7 @@ def _chunk(cfg: WorkloadConfig, P: dict, c: int, rows: int):
 
 def make_dataset(cfg: WorkloadConfig, n: int | None = None):
     """First ``n`` rows (default: all ``cfg.n_samples``) as (X float32 [n x d], y int32 [n])."""
-    if cfg.name == "C5":
+    if cfg.binary_input:
         n = cfg.n_samples if n is None else n
         return c5_host_rows(cfg, np.arange(n))
     n = cfg.n_samples if n is None else min(n, cfg.n_samples)

@@ -141,25 +141,22 @@ def test_generic_output_layer_parity():
 
 
 # ----------------------------------------------------------------------------------------- C5 full size
-def test_c5_full_size_sampled_parity():
-    """BASELINE configs[4] at full size (65536-500000-500000-500000-2, 52.3M connections) in the
-    bench launch configuration (B = 128, chunk_batch auto = 64 -> 2 backward chunks, forward tensors
-    32 wide -> 4 forward chunks, binary-input path, fused
-    update).  Checked: ER topology and values bit-exact (all 52.3M), every forward activation and
-    logit of the batch, and for seeded samples of connections / neurons of every layer the
-    gradient (unfused) and the Eq. 1 update (fused) against the oracle's cone evaluation."""
+def _full_size_sampled_parity(name, B, widths):
+    """Full-size model in the bench launch configuration (max_batch = cfg.batch).  Checked: ER
+    topology and values bit-exact, every forward activation and logit of a B-row batch, and for
+    seeded samples of connections / neurons of every layer the gradient (unfused) and the Eq. 1
+    update (fused) against the oracle's cone evaluation (oracle/sampled.py)."""
     from oracle import sampled as S
     from paper_2102_01732_b200 import SGD
     from synth.data import c5_host_rows
     torch = _torch()
-    cfg = get_config("C5")
+    cfg = get_config(name)
     g, st = pair(cfg)
-    assert (g.info()["chunk_batch"], g.info()["fwd_chunk_batch"]) == (64, 32)
-    assert_topology_equal(g, st, "C5 init")
+    assert (g.info()["chunk_batch"], g.info()["fwd_chunk_batch"]) == widths
+    assert_topology_equal(g, st, f"{name} init")
     for Ly in st.layers:
         e = g.export_layer(Ly.l)
-        assert np.array_equal(e["w"].view(np.uint32), Ly.w.view(np.uint32)), f"C5 W^({Ly.l}) init values"
-    B = cfg.batch
+        assert np.array_equal(e["w"].view(np.uint32), Ly.w.view(np.uint32)), f"{name} W^({Ly.l}) init values"
     x, y = c5_host_rows(cfg, np.arange(B))
     tr = M.forward(st, x, True, 0)
     g.forward(to_dev(x), train=True, step=0)
@@ -194,6 +191,7 @@ def test_c5_full_size_sampled_parity():
         assert rel_err(gbg[okn], gbo[okn]) <= TOL, ("gb", l)
     assert kept >= 0.75 * 256 * len(st.layers)   # the rest touch a kink-ambiguous element (R30)
     # the fused Eq. 1 update in the bench configuration, on a second handle with the same init
+    del g
     g2, _ = pair(cfg)
     sgd = SGD(cfg.lr, cfg.momentum, cfg.weight_decay)
     g2.forward(to_dev(x), train=True, step=0)
@@ -211,6 +209,21 @@ def test_c5_full_size_sampled_parity():
         e = g2.export_layer(l)
         assert rel_err(e["w"][ent[l]][ok], Ly.w[ent[l]][ok]) <= TOL, ("w", l)
         assert rel_err(e["v"][ent[l]][ok], Ly.v[ent[l]][ok]) <= TOL, ("v", l)
+
+
+def test_c5_full_size_sampled_parity():
+    """BASELINE configs[4] at full size (65536-500000-500000-500000-2, 52.3M connections), B = 128:
+    chunk_batch auto = 64 -> 2 backward chunks, forward tensors 32 wide -> 4 forward chunks,
+    binary-input path, fused update."""
+    _full_size_sampled_parity("C5", 128, (64, 32))
+
+
+def test_width_scaling_t2_full_size_sampled_parity():
+    """Width scaling: Table 4 row 2 at full size (65536-2.5M-2.5M-2,
+    eps 5, 42.8M connections, dropout 0.4) in the bench layout (max_batch 128 -> one 128-column
+    chunk: no 32-column slab of a 2.5M-neuron layer fits the L2), on an 8-row batch (a ragged
+    chunk; the oracle's full forward at 128 rows needs 52 GB and 6 minutes)."""
+    _full_size_sampled_parity("T2", 8, (128, 128))
 
 
 # salt: data seed chosen (by the oracle alone) so that no pre-activation of the checked steps
