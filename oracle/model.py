@@ -247,16 +247,21 @@ def activation_grad(x, l: int, alpha: float, act: str = "all_relu"):
 
 def dropout_keep(seed: int, rank: int, l: int, step: int, B: int, n: int, rate: float) -> np.ndarray:
     """Inverted-dropout keep mask [B x n] of hidden layer l (PAPER.md:957 rate; DESIGN reading 13):
-    element (b, j) -> e = b * n + j, word (e & 3) of Philox(DROPOUT, idx = e >> 2, c3 = step);
-    kept iff word >= floor(rate * 2^32)."""
+    element (b, j) -> word (b & 3) of Philox(DROPOUT, idx = j * 2^32 + (b >> 2), c3 = step), i.e.
+    one Philox block per neuron j and group of 4 consecutive batch rows; kept iff
+    word >= floor(rate * 2^32)."""
     if rate <= 0.0:
         return np.ones((B, n), dtype=bool)
-    e = np.arange(B * n, dtype=np.uint64)
-    words = philox.stream(seed, philox.PURPOSE_DROPOUT, rank, l, step & 0xFFFFFFFF, e >> np.uint64(2))
-    W = np.stack(words, axis=0)                          # [4, B*n]
-    word = W[(e & np.uint64(3)).astype(np.int64), np.arange(B * n)]
+    nb4 = (B + 3) // 4
+    b4 = np.arange(nb4, dtype=np.uint64)[:, None]
+    j = np.arange(n, dtype=np.uint64)[None, :]
+    idx = ((j << np.uint64(32)) | b4).ravel()                     # [nb4 * n], row-major in (b4, j)
+    W = np.stack(philox.stream(seed, philox.PURPOSE_DROPOUT, rank, l, step & 0xFFFFFFFF, idx), axis=0)
+    W = W.reshape(4, nb4, n)                                      # W[w, b4, j]
+    b = np.arange(B)
+    word = W[b & 3, b >> 2, :]                                    # [B x n]
     thr = np.uint64(math.floor(rate * 4294967296.0))
-    return (word.astype(np.uint64) >= thr).reshape(B, n)
+    return word.astype(np.uint64) >= thr
 
 
 # --------------------------------------------------------------------------------------

@@ -19,8 +19,8 @@ without broadcast").  The stream layout below is this build's own spec
     purpose 1 INIT candidates      idx = m (candidate number)        c3 = 0
     purpose 2 INIT dense values    idx = i * n_out + j               c3 = 0
     purpose 3 REGROW candidates    idx = m                           c3 = evolve index e
-    purpose 4 DROPOUT              idx = (b * n_l + j) >> 2          c3 = global step (low 32 bits)
-                                   word = (b * n_l + j) & 3
+    purpose 4 DROPOUT              idx = j * 2^32 + (b >> 2)         c3 = global step (low 32 bits)
+                                   word = b & 3
 """
 from __future__ import annotations
 

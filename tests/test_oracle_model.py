@@ -197,6 +197,12 @@ def test_dropout_mask_statistics():
     assert np.array_equal(keep, M.dropout_keep(5, 0, 2, 17, 64, 1000, 0.3))      # deterministic
     assert not np.array_equal(keep, M.dropout_keep(5, 1, 2, 17, 64, 1000, 0.3))  # rank-dependent
     assert M.dropout_keep(5, 0, 2, 17, 4, 10, 0.0).all()
+    # an element's keep bit depends on (b, j) only: the mask of a smaller batch / narrower layer
+    # is a prefix (so a ragged last batch and every chunking see the same bits)
+    assert np.array_equal(keep[:37], M.dropout_keep(5, 0, 2, 17, 37, 1000, 0.3))
+    assert np.array_equal(keep[:, :333], M.dropout_keep(5, 0, 2, 17, 64, 333, 0.3))
+    # and the four rows of one group of 4 use four different words (no repeated pattern)
+    assert not np.array_equal(keep[0], keep[1]) and not np.array_equal(keep[0], keep[4])
 
 
 # ----------------------------------------------------------------------------- dense equivalence
