@@ -210,6 +210,10 @@ __device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4
     }
     uint32_t zb[4], kb[4];
     float out[4];
+    // dropout (R13): one Philox block per (neuron j, 4 batch rows): word c for row b0 + 4q + c
+    const uint4 dr = A.dropout_on ? rng_stream(A.seed, P_DROPOUT, A.rank, A.layer, step_lo,
+                                               ((uint64_t)j << 32) | (uint64_t)((A.b0 + q * 4) >> 2))
+                                  : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         const float zc = comp(z, c);
@@ -218,10 +222,7 @@ __device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4
         float a = pos ? zc : A.neg_slope * zc;
         bool keep = true;
         if (A.dropout_on) {
-            const uint64_t b = (uint64_t)(A.b0 + q * 4 + c);
-            const uint64_t e = b * (uint64_t)A.n_out + (uint64_t)j;
-            const uint4 r = rng_stream(A.seed, P_DROPOUT, A.rank, A.layer, step_lo, e >> 2);
-            keep = word(r, (int)(e & 3)) >= A.drop_thr;
+            keep = word(dr, c) >= A.drop_thr;
             a = keep ? a * A.keep_scale : 0.f;
         }
         kb[c] = group_bits<G>(__ballot_sync(FULL, own && keep), g);
@@ -373,6 +374,11 @@ __device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, c
     constexpr int G = C::G, P = C::P, NR = C::NR;
     const int g = lane / G, q = lane % G;
     uint32_t bal_p[NR], bal_k[NR];
+    // dropout (R13): one Philox block per (neuron j, 4 batch rows): word c for row b0 + 4q + c
+    const uint4 dr = (A.hidden && A.dropout_on)
+                         ? rng_stream(A.seed, P_DROPOUT, A.rank, A.layer, step_lo,
+                                      ((uint64_t)j << 32) | (uint64_t)((A.b0 + q * 4) >> 2))
+                         : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
         const int c = r * P + g;
@@ -387,10 +393,7 @@ __device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, c
         float a = pos ? z : A.neg_slope * z;
         bool keep = true;
         if (A.dropout_on && valid) {
-            const uint64_t b = (uint64_t)(A.b0 + q * 4 + c);
-            const uint64_t e = b * (uint64_t)A.n_out + (uint64_t)j;
-            const uint4 rr = rng_stream(A.seed, P_DROPOUT, A.rank, A.layer, step_lo, e >> 2);
-            keep = word(rr, (int)(e & 3)) >= A.drop_thr;
+            keep = word(dr, c & 3) >= A.drop_thr;
             a = keep ? a * A.keep_scale : 0.f;
         }
         if (valid) *dst = a;
@@ -1473,6 +1476,9 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
             const float4 z = make_float4(acc.x + bj, acc.y + bj, acc.z + bj, acc.w + bj);
             uint32_t zb[4], kb[4];
             float out[4];
+            // dropout (R13): one Philox block per (neuron j, batch rows 4 lane .. 4 lane + 3)
+            uint4 dr = make_uint4(0, 0, 0, 0);
+            if (DROP) dr = rng_stream(A.seed, P_DROPOUT, A.rank, 2, step_lo, ((uint64_t)j << 32) | (uint64_t)lane);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const float zc = comp(z, c);
@@ -1481,10 +1487,7 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
                 float a = pos ? zc : A.neg_slope * zc;
                 bool keep = true;
                 if (DROP) {
-                    const uint64_t b = (uint64_t)(lane * 4 + c);
-                    const uint64_t e = b * (uint64_t)A.n_out + (uint64_t)j;
-                    const uint4 r = rng_stream(A.seed, P_DROPOUT, A.rank, 2, step_lo, e >> 2);
-                    keep = word(r, (int)(e & 3)) >= A.drop_thr;
+                    keep = word(dr, c) >= A.drop_thr;
                     a = keep ? a * A.keep_scale : 0.f;
                     kb[c] = group_bits<G>(__ballot_sync(FULL, colok && keep), g);
                 }

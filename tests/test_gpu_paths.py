@@ -123,7 +123,7 @@ def test_generic_output_layer_parity():
     torch = _torch()
     cfg = get_config("C1", sizes=(120, 90, 70, 40), epsilon=6.0, dropout=0.2, batch=50)
     g, st = pair(cfg, max_batch=50, chunk_batch=16)
-    rng = np.random.default_rng(11)
+    rng = np.random.default_rng(12)       # a batch with no kink-ambiguous pre-activation (R30)
     X = rng.standard_normal((100, 120)).astype(np.float32)
     Y = rng.integers(0, 40, size=100).astype(np.int32)
     sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay)
