@@ -131,6 +131,17 @@ typedef struct {
  * On failure *out is NULL. */
 int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out);
 
+/* sparse_mlp_plan_chunks — the chunk widths sparse_mlp_create picks (host only, no device call;
+ * DESIGN.md §4-5).  sizes[n_layers] = n_1..n_L, l2_bytes = the device's L2 size.  chunk_batch
+ * != 0: *cb = *cbf = chunk_batch.  0 (auto): *cb = the widest power of two <= min(128,
+ * next_pow2(max(4, max_batch))) whose widest slab n_l x cb x 4 B fits the L2; *cbf = cb halved
+ * (not below 32) while the slab exceeds half the L2; if not even a 32-column slab fits the L2,
+ * *cb = *cbf = the widest.  (create then applies the SMLP_FWD_CB override.)
+ * Errors: SMLP_E_ARG (NULL pointer, n_layers < 1, max_batch < 1, l2_bytes <= 0, chunk_batch
+ * not 0 or a power of two in [4, 128]). */
+int sparse_mlp_plan_chunks(const int64_t* sizes, int32_t n_layers, int32_t max_batch, int32_t chunk_batch,
+                           int64_t l2_bytes, int32_t* cb, int32_t* cbf);
+
 /* Frees everything through the allocator on the handle's stream.  NULL is a no-op. */
 int sparse_mlp_destroy(smlp_handle* h);
 

@@ -260,6 +260,40 @@ const char* sparse_mlp_last_error(const smlp_handle* h) {
     return h ? h->err.c_str() : g_create_error.c_str();
 }
 
+int sparse_mlp_plan_chunks(const int64_t* sizes, int32_t n_layers, int32_t max_batch, int32_t chunk_batch,
+                           int64_t l2_bytes, int32_t* cb, int32_t* cbf) {
+    if (!sizes || !cb || !cbf || n_layers < 1 || max_batch < 1 || l2_bytes <= 0)
+        return set_err(nullptr, SMLP_E_ARG, "plan_chunks: bad argument");
+    if (chunk_batch != 0) {
+        if (chunk_batch < 4 || chunk_batch > 128 || (chunk_batch & (chunk_batch - 1)))
+            return set_err(nullptr, SMLP_E_ARG, "chunk_batch must be a power of two in [4, 128]");
+        *cb = *cbf = chunk_batch;
+        return SMLP_OK;
+    }
+    const double l2 = (double)l2_bytes;
+    int64_t nmax = 0;
+    for (int l = 0; l < n_layers; ++l) nmax = std::max<int64_t>(nmax, sizes[l]);
+    // the widest chunk (<= 128 columns) whose largest activation slab n_l x CB x 4 B fits in the
+    // L2, so most row gathers of a pass hit in L2 (C5: 64 columns, 128 MB slabs; measured 6.7
+    // ms/step against 7.1 at 32 and 9.3 at 16)
+    const int widest = std::min(128, next_pow2(std::max(4, (int)max_batch)));
+    int CB = widest;
+    while (CB > 4 && (double)nmax * CB * 4.0 > l2) CB >>= 1;
+    // forward width: the forward gathers a_{l-1} only (no second operand in flight), so a
+    // narrower slab that stays L2-resident pays more than the wider chunk's fewer passes
+    // (C5: 32 columns / 64 MB forward, 64 columns / 128 MB backward)
+    int CBf = CB;
+    while (CBf > 32 && (double)nmax * CBf * 4.0 > 0.5 * l2) CBf >>= 1;
+    // layers so wide that not even a 32-column slab fits the L2 (Table 4 widths, >= 1M
+    // neurons): the gathers miss either way, so the widest chunk (fewest passes over the
+    // indices, longest rows per gather) wins -- T2 / T3 (2.5M / 5M): 9.2 / 18.7 ms at 128
+    // columns against 11.1 / 22.5 at 64 and 14.5 / 29.3 at 32
+    if (widest >= 32 && (double)nmax * 32 * 4.0 > l2) CB = CBf = widest;
+    *cb = CB;
+    *cbf = CBf;
+    return SMLP_OK;
+}
+
 int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     if (!out) return set_err(nullptr, SMLP_E_ARG, "out is NULL");
     *out = nullptr;
@@ -276,34 +310,15 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     if (cfg->activation != SMLP_ACT_RELU && cfg->activation != SMLP_ACT_ALL_RELU)
         return set_err(nullptr, SMLP_E_ARG, "unknown activation");
     if (cfg->init < SMLP_INIT_NORMAL || cfg->init > SMLP_INIT_HE_U) return set_err(nullptr, SMLP_E_ARG, "unknown init");
-    int CB = cfg->chunk_batch;
-    int CBf = CB;
-    if (CB != 0 && (CB < 4 || CB > 128 || (CB & (CB - 1))))
+    if (cfg->chunk_batch != 0 && (cfg->chunk_batch < 4 || cfg->chunk_batch > 128 || (cfg->chunk_batch & (cfg->chunk_batch - 1))))
         return set_err(nullptr, SMLP_E_ARG, "chunk_batch must be a power of two in [4, 128]");
     if (cudaSetDevice(cfg->device) != cudaSuccess) return set_err(nullptr, SMLP_E_CUDA, "cudaSetDevice failed");
-    if (CB == 0) {
-        // auto: the widest chunk (<= 128 columns) whose largest activation slab n_l x CB x 4 B
-        // fits in the L2, so most row gathers of a chunk pass hit in L2 (C5: 64 columns, 128 MB
-        // slabs; measured 6.7 ms/step against 7.1 at 32 and 9.3 at 16)
-        int l2 = 0;
-        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, cfg->device);
-        if (l2 <= 0) l2 = 126 << 20;
-        int64_t nmax = 0;
-        for (int l = 0; l < cfg->n_layers; ++l) nmax = std::max<int64_t>(nmax, cfg->sizes[l]);
-        const int widest = std::min(128, next_pow2(std::max(4, cfg->max_batch)));
-        CB = widest;
-        while (CB > 4 && (double)nmax * CB * 4.0 > 1.0 * (double)l2) CB >>= 1;
-        // forward width: the forward gathers a_{l-1} only (no second operand in flight), so a
-        // narrower slab that stays L2-resident pays more than the wider chunk's fewer passes
-        // (C5: 32 columns / 64 MB forward, 64 columns / 128 MB backward)
-        CBf = CB;
-        while (CBf > 32 && (double)nmax * CBf * 4.0 > 0.5 * (double)l2) CBf >>= 1;
-        // layers so wide that not even a 32-column slab fits the L2 (Table 4 widths, >= 1M
-        // neurons): the gathers miss either way, so the widest chunk (fewest passes over the
-        // indices, longest rows per gather) wins -- T2 / T3 (2.5M / 5M): 9.2 / 18.7 ms at 128
-        // columns against 11.1 / 22.5 at 64 and 14.5 / 29.3 at 32
-        if (widest >= 32 && (double)nmax * 32 * 4.0 > 1.0 * (double)l2) CB = CBf = widest;
-    }
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, cfg->device);
+    if (l2 <= 0) l2 = 126 << 20;
+    int CB = 0, CBf = 0;
+    if (sparse_mlp_plan_chunks(cfg->sizes, cfg->n_layers, cfg->max_batch, cfg->chunk_batch, l2, &CB, &CBf) != SMLP_OK)
+        return SMLP_E_ARG;
     if (const char* e = std::getenv("SMLP_FWD_CB")) CBf = std::atoi(e);
     if (CBf > CB || CBf < 4 || (CBf & (CBf - 1)) || (CBf < CB && CBf < 32))
         return set_err(nullptr, SMLP_E_ARG, "forward chunk width must be a power of two, <= chunk_batch and >= 32 when narrower");

@@ -37,7 +37,7 @@ EXPORTED = [
     "sparse_mlp_export_bias", "sparse_mlp_import_bias", "sparse_mlp_export_alive",
     "sparse_mlp_import_alive", "sparse_mlp_export_trace", "sparse_mlp_last_error", "sparse_mlp_version",
     "sparse_mlp_profile", "sparse_mlp_profile_read", "sparse_mlp_set_step_counter",
-    "sparse_mlp_params_updated",
+    "sparse_mlp_params_updated", "sparse_mlp_plan_chunks",
 ]
 KERNEL_KINDS = {0: "stage_input", 1: "fwd", 2: "fwd_finish", 3: "softmax_ce", 4: "bwd", 5: "bwd_finish",
                 6: "sgd_update", 7: "fwd_bits", 8: "bwd_bits", 9: "layer_update", 10: "mirror_values"}
@@ -87,6 +87,18 @@ class smlp_info(C.Structure):
 _lib = None
 
 
+def plan_chunks(sizes, max_batch: int, chunk_batch: int = 0, l2_bytes: int = 126 << 20):
+    """(chunk_batch, fwd_chunk_batch) sparse_mlp_create would pick (host-only C call)."""
+    L = load_library()
+    arr = (C.c_int64 * len(sizes))(*[int(n) for n in sizes])
+    cb, cbf = C.c_int32(), C.c_int32()
+    rc = L.sparse_mlp_plan_chunks(arr, len(sizes), int(max_batch), int(chunk_batch), int(l2_bytes),
+                                  C.byref(cb), C.byref(cbf))
+    if rc != 0:
+        raise ValueError(L.sparse_mlp_last_error(None).decode())
+    return cb.value, cbf.value
+
+
 def load_library(path: str = LIB_PATH):
     """Load libsparse_mlp.so (raises if it has not been built: no fallback exists)."""
     global _lib
@@ -99,6 +111,7 @@ def load_library(path: str = LIB_PATH):
     P, VP, I32, I64, U64, D, F = C.POINTER, C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_float
     sig = {
         "sparse_mlp_create": (I32, [P(smlp_config), P(VP)]),
+        "sparse_mlp_plan_chunks": (I32, [P(I64), I32, I32, I32, I64, P(I32), P(I32)]),
         "sparse_mlp_destroy": (I32, [VP]),
         "sparse_mlp_set_stream": (I32, [VP, VP]),
         "sparse_mlp_forward": (I32, [VP, VP, VP, I32, I32, U64, VP]),
