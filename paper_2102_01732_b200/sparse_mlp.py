@@ -17,7 +17,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libsparse_mlp.so")
+LIB_PATH = os.environ.get("SMLP_LIB") or os.path.join(_PKG, "lib", "libsparse_mlp.so")   # SMLP_LIB: A/B builds
 
 SMLP_MAX_LAYERS = 16
 ACTIVATIONS = {"relu": 0, "all_relu": 1}
