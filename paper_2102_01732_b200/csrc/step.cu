@@ -87,18 +87,10 @@ __device__ __forceinline__ void st_f32(float* p, float v, uint64_t pol) {
 
 // L2-hinted variants used by the row kernels (hint = createpolicy register; "evict_normal" when the
 // knob is off, so the instruction count is the same either way)
-#ifndef SMLP_GATHER_L1NA
-#define SMLP_GATHER_L1NA 0
-#endif
 __device__ __forceinline__ float4 ldg4_hint(const float* p, uint64_t pol) {
     float4 v;
-#if SMLP_GATHER_L1NA
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
-#else
     asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
-#endif
     return v;
 }
 __device__ __forceinline__ float ld_hint(const float* p, uint64_t pol) {
