@@ -218,6 +218,13 @@ def test_c5_full_size_sampled_parity():
     _full_size_sampled_parity("C5", 128, (64, 32))
 
 
+def test_width_scaling_t4_full_size_sampled_parity():
+    """Table 4 row 4 at full size (65536-5M x 4-2, eps 1: four 5M-neuron hidden layers, 40.1M
+    connections, ~2 connections per row, a SPARSE narrow output layer of 5M x 2 -> the row-streaming
+    bwd_narrow_kernel), 4-row batch in the 128-column bench layout."""
+    _full_size_sampled_parity("T4", 4, (128, 128))
+
+
 def test_width_scaling_t2_full_size_sampled_parity():
     """Width scaling: Table 4 row 2 at full size (65536-2.5M-2.5M-2,
     eps 5, 42.8M connections, dropout 0.4) in the bench layout (max_batch 128 -> one 128-column
