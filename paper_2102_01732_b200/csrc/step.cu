@@ -1445,12 +1445,7 @@ template <int CB, bool DROP>
 __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
     constexpr int G = CB / 4;                       // lanes per chunk
     __shared__ float2 rec[WARPS_PER_BLOCK][32][XBITS_WORDS];
-    __shared__ float4 lut[16];                      // nibble -> its 4 bits as floats {0, 1}
     if (*A.nonbinary) return;
-    if (threadIdx.x < 16)
-        lut[threadIdx.x] = make_float4((float)(threadIdx.x & 1), (float)((threadIdx.x >> 1) & 1),
-                                       (float)((threadIdx.x >> 2) & 1), (float)((threadIdx.x >> 3) & 1));
-    __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane / G, q = lane % G;            // chunk g, chunk-local lane q
     const bool colok = g < A.nchunks;
@@ -1535,12 +1530,15 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
                 const int stop = min(n, row_end - blk);
                 float2 alo = make_float2(acc.x, acc.y), ahi = make_float2(acc.z, acc.w);
                 const char* rp = reinterpret_cast<const char*>(myrec);
-                const char* lp = reinterpret_cast<const char*>(lut);
 #pragma unroll 4
                 for (; u < stop; ++u) {
                     const float2 r = *reinterpret_cast<const float2*>(rp + u * (XBITS_WORDS * 8));
-                    // x in {0, 1}: fmaf(w, x, acc) is acc + w for x = 1 and acc for x = 0, bit for bit
-                    const float4 m = *reinterpret_cast<const float4*>(lp + (((__float_as_uint(r.y) >> sh) & 15u) << 4));
+                    // x in {0, 1}: fmaf(w, x, acc) is acc + w for x = 1 and acc for x = 0, bit for bit;
+                    // the 4 x's come from the nibble by ALU selects (a shared-memory table read per
+                    // entry kept the L1 / shared pipe at 94%)
+                    const uint32_t nib = __float_as_uint(r.y) >> sh;
+                    const float4 m = make_float4((nib & 1u) ? 1.f : 0.f, (nib & 2u) ? 1.f : 0.f,
+                                                 (nib & 4u) ? 1.f : 0.f, (nib & 8u) ? 1.f : 0.f);
                     alo = ffma2(make_float2(r.x, r.x), make_float2(m.x, m.y), alo);
                     ahi = ffma2(make_float2(r.x, r.x), make_float2(m.z, m.w), ahi);
                 }
