@@ -156,14 +156,17 @@ def test_unfused_step_equals_fused():
     assert_values_close(g2, st, TOL)
 
 
-@pytest.mark.parametrize("B", [128, 100, 33, 5])
-def test_chunked_layout_parity(B):
-    """chunk_batch = 32: the batch is split in ceil(B/32) chunks (ragged last chunk), gradients
-    accumulate over chunks in a fixed order."""
+@pytest.mark.parametrize("B,fchunk", [(128, None), (100, None), (33, None), (5, None), (1, None), (1, 32), (65, 32)])
+def test_chunked_layout_parity(B, fchunk, monkeypatch):
+    """chunk_batch = 32 (64 with a 32-wide forward when fchunk is set): the batch is split in
+    ceil(B/CB) chunks (ragged last chunk; B = 1 is one column), gradients accumulate over chunks in
+    a fixed order."""
     torch = _torch()
     cfg = get_config("C2", batch=B)
     from paper_2102_01732_b200 import SGD
-    g, st = pair(cfg, max_batch=128, chunk_batch=32)
+    if fchunk:
+        monkeypatch.setenv("SMLP_FWD_CB", str(fchunk))
+    g, st = pair(cfg, max_batch=128, chunk_batch=64 if fchunk else 32)
     x, y, tr = _batch(cfg, st, B=B, step=2)
     g.forward(to_dev(x), train=True, step=2)
     g.backward(to_dev(y))
