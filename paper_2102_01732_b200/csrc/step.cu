@@ -123,35 +123,50 @@ __device__ __forceinline__ uint64_t stream_policy(int hint) { return hint ? poli
 // ------------------------------------------------------------------------------------------
 // a1: input staging (transpose + optional row gather), zero padding of columns b >= B
 // ------------------------------------------------------------------------------------------
+// 32 batch rows x 128 features per 1024-thread block: float4 loads along the features (scalar
+// when n_1 or x is not 16-B aligned), a shared-memory transpose (feature 4t + k stored at column
+// 32k + t: conflict-free both ways), then per feature one coalesced row of the chunk layout and
+// one 32-bit word of the bit-packed input
 __global__ void __launch_bounds__(1024) stage_input_kernel(const float* __restrict__ x, const int32_t* __restrict__ x_idx,
                                                            int B, int nchunks, int CB, int64_t n1,
                                                            float* __restrict__ act1, uint32_t* __restrict__ xbits,
-                                                           int32_t* __restrict__ nonbinary) {
-    __shared__ float tile[32][33];
-    const int64_t f0 = (int64_t)blockIdx.x * 32;
+                                                           int32_t* __restrict__ nonbinary, int vec) {
+    __shared__ float tile[32][129];
+    const int64_t f0 = (int64_t)blockIdx.x * 128;
     const int b0 = blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 32
     {
         const int b = b0 + ty;
-        const int64_t f = f0 + tx;
-        float v = 0.f;
-        if (b < B && f < n1) {
+        const int64_t f = f0 + 4 * tx;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (b < B) {
             const int64_t row = x_idx ? (int64_t)__ldg(x_idx + b) : (int64_t)b;
-            v = __ldg(x + row * n1 + f);
+            const float* p = x + row * n1 + f;
+            if (vec && f + 3 < n1) {
+                const float4 t = ldg4(p);
+                v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (f + k < n1) v[k] = __ldg(p + k);
+            }
         }
-        tile[ty][tx] = v;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) tile[ty][32 * k + tx] = v[k];
     }
     __syncthreads();
-    {
-        const int b = b0 + tx;
-        const int64_t f = f0 + ty;
-        const float v = tile[tx][ty];
+    const int b = b0 + tx;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int fl = ty + 32 * r;                       // warp-uniform local feature
+        const int64_t f = f0 + fl;
+        const float v = tile[tx][32 * (fl & 3) + (fl >> 2)];
         if (f < n1 && b < nchunks * CB) {
             const int c = b / CB, lb = b % CB;
             act1[((int64_t)c * n1 + f) * CB + lb] = v;
         }
         if (xbits) {
-            // warp ty holds feature f over batch b0..b0+31: one 32-bit word of the bit-packed
+            // the warp holds feature f over batch b0..b0+31: one 32-bit word of the bit-packed
             // input (bit b%32 = x[b][f] != 0) for the exact binary-input path of layer 2
             const unsigned word = __ballot_sync(FULL, v != 0.f);
             const bool nb = __any_sync(FULL, v != 0.f && v != 1.f);
@@ -1989,11 +2004,12 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
     const int CB = h->CBf;    // the forward tensors' chunk width
     const int nchunks = (B + CB - 1) / CB;
     {
-        dim3 grid((unsigned)((h->sizes[0] + 31) / 32), (unsigned)((nchunks * CB + 31) / 32));
+        dim3 grid((unsigned)((h->sizes[0] + 127) / 128), (unsigned)((nchunks * CB + 31) / 32));
+        const int vec = (h->sizes[0] % 4 == 0) && ((uintptr_t)x % 16 == 0);
         prof_start(h, K_STAGE, 1, 8.0 * (double)B * (double)h->sizes[0], 0.0);
         if (h->xbits) SMLP_CK(h, cudaMemsetAsync(h->d_nonbinary, 0, sizeof(int32_t), h->stream));
         stage_input_kernel<<<grid, dim3(32, 32), 0, h->stream>>>(x, x_idx, B, nchunks, CB, h->sizes[0], h->act[1],
-                                                                 h->xbits, h->d_nonbinary);
+                                                                 h->xbits, h->d_nonbinary, vec);
         SMLP_CK_LAUNCH(h, "stage_input_kernel");
         prof_stop(h);
     }
