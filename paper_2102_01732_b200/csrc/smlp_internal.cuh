@@ -171,6 +171,7 @@ struct smlp_handle {
     int l2hint = 1;                 // SMLP_L2HINT: L2 eviction policies in the row kernels (on: +0.4%)
     int l2persist = 0;              // SMLP_L2PERSIST (percent): persisting-L2 window on the gathered slabs
     int fused_update = 0;           // SMLP_FUSED_UPDATE: Eq. 1 inside the last chunk's backward
+    int update_scatter = 0;         // SMLP_UPDATE_SCATTER: the Eq. 1 pass scatters w into mval (no mirror gather)
     int overlap_update = 0;         // SMLP_OVERLAP_UPDATE: each layer's Eq. 1 pass + mirror refresh on the
                                     // aux stream as soon as its gradient is final (overlaps the backward;
                                     // C5: 6.040 -> 6.025 ms, the backward kernels slow down by what the

@@ -1664,11 +1664,24 @@ __global__ void grad_from_mirror_kernel(const int32_t* __restrict__ nonbinary, c
 // Eq. 1 over one parameter slice (lam = weight decay, 0 for biases), 4 parameters per thread and
 // two float4 groups in flight per iteration.  g and v are streamed once (evict_first); w is kept
 // (evict_last): the mirror gather of the same layer reads it right after.
+// SCATTER: also write each updated w into its mirror slot mval[minv[k]] (k < the layer's device
+// nnz), replacing the separate mirror gather
+template <bool SCATTER>
 __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w, float* __restrict__ v,
                                                           const float* __restrict__ g, int64_t n, float lr,
-                                                          float mu, float lam, float gs) {
+                                                          float mu, float lam, float gs, const int32_t* __restrict__ minv,
+                                                          float* __restrict__ mval, const LayerMeta* __restrict__ meta) {
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     const int64_t n4 = n >> 2;
+    const int64_t nnz = SCATTER ? meta->nnz : 0;
+    auto scatter = [&](int64_t k4, const float4& wn) {   // parameters 4 k4 .. 4 k4 + 3
+        if (!SCATTER || 4 * k4 >= nnz) return;
+        const int4 m = ldi4_hint(minv + 4 * k4, pf);
+        mval[m.x] = wn.x;
+        if (4 * k4 + 1 < nnz) mval[m.y] = wn.y;
+        if (4 * k4 + 2 < nnz) mval[m.z] = wn.z;
+        if (4 * k4 + 3 < nnz) mval[m.w] = wn.w;
+    };
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
     auto upd = [&](float4 wk, float4 vk, float4 gk) {
         float4 o;
@@ -1684,22 +1697,29 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
         const float4 w0 = ld4_hint(w + 4 * k, pl), v0 = ld4_hint(v + 4 * k, pf), g0 = ldg4_hint(g + 4 * k, pf);
         const float4 w1 = ld4_hint(w + 4 * k2, pl), v1 = ld4_hint(v + 4 * k2, pf), g1 = ldg4_hint(g + 4 * k2, pf);
         const float4 a = upd(w0, v0, g0), b = upd(w1, v1, g1);
+        const float4 wa = make_float4(w0.x + a.x, w0.y + a.y, w0.z + a.z, w0.w + a.w);
+        const float4 wb = make_float4(w1.x + b.x, w1.y + b.y, w1.z + b.z, w1.w + b.w);
         st4_hint(v + 4 * k, a, pf);
-        st4_hint(w + 4 * k, make_float4(w0.x + a.x, w0.y + a.y, w0.z + a.z, w0.w + a.w), pl);
+        st4_hint(w + 4 * k, wa, pl);
         st4_hint(v + 4 * k2, b, pf);
-        st4_hint(w + 4 * k2, make_float4(w1.x + b.x, w1.y + b.y, w1.z + b.z, w1.w + b.w), pl);
+        st4_hint(w + 4 * k2, wb, pl);
+        scatter(k, wa);
+        scatter(k2, wb);
     }
     if (k < n4) {
         const float4 w0 = ld4_hint(w + 4 * k, pl), v0 = ld4_hint(v + 4 * k, pf), g0 = ldg4_hint(g + 4 * k, pf);
         const float4 a = upd(w0, v0, g0);
+        const float4 wa = make_float4(w0.x + a.x, w0.y + a.y, w0.z + a.z, w0.w + a.w);
         st4_hint(v + 4 * k, a, pf);
-        st4_hint(w + 4 * k, make_float4(w0.x + a.x, w0.y + a.y, w0.z + a.z, w0.w + a.w), pl);
+        st4_hint(w + 4 * k, wa, pl);
+        scatter(k, wa);
     }
     if (tid < n - 4 * n4) {   // tail (n % 4 parameters)
         const int64_t t = 4 * n4 + tid;
         const float wk = w[t], vk = mu * v[t] - lr * (gs * g[t] + lam * wk);
         v[t] = vk;
         w[t] = wk + vk;
+        if (SCATTER && t < nnz) mval[minv[t]] = wk + vk;
     }
 }
 
@@ -2097,13 +2117,21 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
 
 // Eq. 1 over the parameter slice [lo, hi) on `stream`: one resident wave (8 CTAs of 256 per SM),
 // two float4 groups per thread and iteration
-static int launch_update(smlp_handle* h, cudaStream_t stream, int64_t lo, int64_t hi, bool decay, const smlp_sgd* sgd) {
+static int launch_update(smlp_handle* h, cudaStream_t stream, int64_t lo, int64_t hi, bool decay, const smlp_sgd* sgd,
+                         const Layer* mirror = nullptr) {
     if (hi <= lo) return SMLP_OK;
     constexpr int threads = 256;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((hi - lo + 4 * threads - 1) / (4 * threads),
                                                                  (int64_t)h->num_sms * 8));
-    sgd_update4_kernel<<<grid, threads, 0, stream>>>(h->param + lo, h->mom + lo, h->grad + lo, hi - lo, sgd->lr,
-                                                     sgd->momentum, decay ? sgd->weight_decay : 0.f, sgd->grad_scale);
+    const float lam = decay ? sgd->weight_decay : 0.f;
+    if (mirror)
+        sgd_update4_kernel<true><<<grid, threads, 0, stream>>>(h->param + lo, h->mom + lo, h->grad + lo, hi - lo, sgd->lr,
+                                                               sgd->momentum, lam, sgd->grad_scale, mirror->minv,
+                                                               mirror->mval, mirror->meta);
+    else
+        sgd_update4_kernel<false><<<grid, threads, 0, stream>>>(h->param + lo, h->mom + lo, h->grad + lo, hi - lo,
+                                                                sgd->lr, sgd->momentum, lam, sgd->grad_scale, nullptr,
+                                                                nullptr, nullptr);
     SMLP_CK_LAUNCH(h, "sgd_update4_kernel");
     return SMLP_OK;
 }
@@ -2306,6 +2334,10 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
     prof_start(h, K_SGD, 0, 20.0 * (double)n, 0.0);
     bool side = false;
     for (auto& Ly : h->layers) {
+        if (h->update_scatter && !Ly.narrow) {                     // the update writes the mirror copy too
+            SMLP_TRY(launch_update(h, h->stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd, &Ly));
+            continue;
+        }
         SMLP_TRY(update(Ly.val_off, Ly.val_off + Ly.cap, true));
         if (Ly.narrow) continue;                                   // narrow layers never read the mirror copy
         SMLP_CK(h, cudaEventRecord(h->aux_ev[0], h->stream));
