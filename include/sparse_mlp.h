@@ -57,6 +57,10 @@ extern "C" {
 #define SMLP_INIT_XAVIER_U   1   /* U(-sqrt(6/(n_{l-1}+n_l)), +sqrt(6/(n_{l-1}+n_l)))    */
 #define SMLP_INIT_HE_U       2   /* U(-sqrt(6/n_{l-1}), +sqrt(6/n_{l-1}))                */
 
+/* input kinds (smlp_config.input_kind) */
+#define SMLP_INPUT_AUTO 0
+#define SMLP_INPUT_REAL 1
+
 /* prune flags */
 #define SMLP_PRUNE_OUTGOING  1   /* also remove the outgoing row of a pruned neuron (R17)   */
 
@@ -94,6 +98,10 @@ typedef struct {
     int32_t        device;       /* CUDA device ordinal                                       */
     void*          stream;       /* cudaStream_t the handle enqueues on (NULL = legacy)       */
     const smlp_allocator* allocator; /* NULL = cudaMallocAsync on `stream`                   */
+    int32_t        input_kind;   /* SMLP_INPUT_AUTO: detect {0,1}-only batches on the device and
+                                    take the bit-packed W^(2) path for them (needs max_batch
+                                    <= 128); SMLP_INPUT_REAL: inputs are real-valued, no
+                                    detection and no bit path (4 fewer launches per step)   */
 } smlp_config;
 
 /* Momentum SGD with weight decay, Eq. 1 in velocity form (reading R14):

@@ -223,7 +223,8 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
     }
     h->d_err = zalloc<int32_t>(h, 1, &rc);
     // binary-input path of W^(2): bit-packed input, usable when the padded batch fits 128 columns
-    if ((int64_t)h->max_chunks * CB <= 32 * XBITS_WORDS && (int64_t)h->max_chunks_f * h->CBf <= 32 * XBITS_WORDS) {
+    if (cfg->input_kind != SMLP_INPUT_REAL && (int64_t)h->max_chunks * CB <= 32 * XBITS_WORDS &&
+        (int64_t)h->max_chunks_f * h->CBf <= 32 * XBITS_WORDS) {
         h->xbits = zalloc<uint32_t>(h, (size_t)h->sizes[0] * XBITS_WORDS, &rc);
         h->d_nonbinary = zalloc<int32_t>(h, 1, &rc);
         h->gmirror2 = zalloc<float>(h, (size_t)std::max<int64_t>(h->layers[0].cap, 1), &rc);
@@ -310,6 +311,8 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     if (cfg->activation != SMLP_ACT_RELU && cfg->activation != SMLP_ACT_ALL_RELU)
         return set_err(nullptr, SMLP_E_ARG, "unknown activation");
     if (cfg->init < SMLP_INIT_NORMAL || cfg->init > SMLP_INIT_HE_U) return set_err(nullptr, SMLP_E_ARG, "unknown init");
+    if (cfg->input_kind != SMLP_INPUT_AUTO && cfg->input_kind != SMLP_INPUT_REAL)
+        return set_err(nullptr, SMLP_E_ARG, "unknown input_kind");
     if (cfg->chunk_batch != 0 && (cfg->chunk_batch < 4 || cfg->chunk_batch > 128 || (cfg->chunk_batch & (cfg->chunk_batch - 1))))
         return set_err(nullptr, SMLP_E_ARG, "chunk_batch must be a power of two in [4, 128]");
     if (cudaSetDevice(cfg->device) != cudaSuccess) return set_err(nullptr, SMLP_E_CUDA, "cudaSetDevice failed");

@@ -35,6 +35,7 @@ constexpr int WARPS_PER_BLOCK = 8;        // 256-thread blocks for the warp-per-
 constexpr int NARROW_MAX = 32;            // output layers with n_L <= 32 take the narrow path
 constexpr int NARROW_MAX_ELEMS = 2048;    // ... if next_pow2(n_L) x chunk_batch <= this
 constexpr int NARROW_WARPS = 8;
+constexpr int64_t SMALL_MODEL_PARAMS = 1 << 22;   // run_step: one update + one mirror launch at or below this
 constexpr int XBITS_WORDS = 4;          // bit-packed input: 128 batch columns per input neuron
 
 struct LayerMeta {                         // device-resident counts (graph-stable)

@@ -1669,8 +1669,9 @@ __global__ void grad_from_mirror_kernel(const int32_t* __restrict__ nonbinary, c
 template <bool SCATTER>
 __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w, float* __restrict__ v,
                                                           const float* __restrict__ g, int64_t n, float lr,
-                                                          float mu, float lam, float gs, const int32_t* __restrict__ minv,
-                                                          float* __restrict__ mval, const LayerMeta* __restrict__ meta) {
+                                                          float mu, float wd, int64_t decay_end, float gs,
+                                                          const int32_t* __restrict__ minv, float* __restrict__ mval,
+                                                          const LayerMeta* __restrict__ meta) {
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     const int64_t n4 = n >> 2;
     const int64_t nnz = SCATTER ? meta->nnz : 0;
@@ -1683,7 +1684,10 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
         if (4 * k4 + 3 < nnz) mval[m.w] = wn.w;
     };
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
-    auto upd = [&](float4 wk, float4 vk, float4 gk) {
+    // weight decay on [0, decay_end) (the weight slices), none on the biases after it; decay_end
+    // is a multiple of 32, so a float4 group never straddles it
+    auto upd = [&](float4 wk, float4 vk, float4 gk, int64_t k4) {
+        const float lam = 4 * k4 < decay_end ? wd : 0.f;
         float4 o;
         o.x = mu * vk.x - lr * (gs * gk.x + lam * wk.x);
         o.y = mu * vk.y - lr * (gs * gk.y + lam * wk.y);
@@ -1696,7 +1700,7 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
         const int64_t k2 = k + stride;
         const float4 w0 = ld4_hint(w + 4 * k, pl), v0 = ld4_hint(v + 4 * k, pf), g0 = ldg4_hint(g + 4 * k, pf);
         const float4 w1 = ld4_hint(w + 4 * k2, pl), v1 = ld4_hint(v + 4 * k2, pf), g1 = ldg4_hint(g + 4 * k2, pf);
-        const float4 a = upd(w0, v0, g0), b = upd(w1, v1, g1);
+        const float4 a = upd(w0, v0, g0, k), b = upd(w1, v1, g1, k2);
         const float4 wa = make_float4(w0.x + a.x, w0.y + a.y, w0.z + a.z, w0.w + a.w);
         const float4 wb = make_float4(w1.x + b.x, w1.y + b.y, w1.z + b.z, w1.w + b.w);
         st4_hint(v + 4 * k, a, pf);
@@ -1708,7 +1712,7 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
     }
     if (k < n4) {
         const float4 w0 = ld4_hint(w + 4 * k, pl), v0 = ld4_hint(v + 4 * k, pf), g0 = ldg4_hint(g + 4 * k, pf);
-        const float4 a = upd(w0, v0, g0);
+        const float4 a = upd(w0, v0, g0, k);
         const float4 wa = make_float4(w0.x + a.x, w0.y + a.y, w0.z + a.z, w0.w + a.w);
         st4_hint(v + 4 * k, a, pf);
         st4_hint(w + 4 * k, wa, pl);
@@ -1716,11 +1720,27 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
     }
     if (tid < n - 4 * n4) {   // tail (n % 4 parameters)
         const int64_t t = 4 * n4 + tid;
+        const float lam = t < decay_end ? wd : 0.f;
         const float wk = w[t], vk = mu * v[t] - lr * (gs * g[t] + lam * wk);
         v[t] = vk;
         w[t] = wk + vk;
         if (SCATTER && t < nnz) mval[minv[t]] = wk + vk;
     }
+}
+
+// mirror refresh of several layers in one launch (small models: launch count matters more than
+// overlap); blockIdx.y = layer
+struct MirrorSet {
+    const float* val[SMLP_MAX_LAYERS];
+    const int32_t* mperm[SMLP_MAX_LAYERS];
+    const LayerMeta* meta[SMLP_MAX_LAYERS];
+    float* mval[SMLP_MAX_LAYERS];
+};
+__global__ void __launch_bounds__(256) mirror_values_multi_kernel(const __grid_constant__ MirrorSet M) {
+    const int l = blockIdx.y;
+    const int64_t n = M.meta[l]->nnz;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        M.mval[l][t] = __ldg(M.val[l] + __ldg(M.mperm[l] + t));
 }
 
 // mirror copy mval[t] = val[mperm[t]], 4 consecutive t per thread (4 independent gathers in flight)
@@ -2123,15 +2143,17 @@ static int launch_update(smlp_handle* h, cudaStream_t stream, int64_t lo, int64_
     constexpr int threads = 256;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((hi - lo + 4 * threads - 1) / (4 * threads),
                                                                  (int64_t)h->num_sms * 8));
-    const float lam = decay ? sgd->weight_decay : 0.f;
+    // decay: weights (all of [lo, hi)), or none (biases), or -- for the single whole-view launch of
+    // small models -- everything below bias_base
+    const int64_t decay_end = decay ? std::min(hi, h->bias_base) - lo : 0;
     if (mirror)
         sgd_update4_kernel<true><<<grid, threads, 0, stream>>>(h->param + lo, h->mom + lo, h->grad + lo, hi - lo, sgd->lr,
-                                                               sgd->momentum, lam, sgd->grad_scale, mirror->minv,
-                                                               mirror->mval, mirror->meta);
+                                                               sgd->momentum, sgd->weight_decay, decay_end,
+                                                               sgd->grad_scale, mirror->minv, mirror->mval, mirror->meta);
     else
         sgd_update4_kernel<false><<<grid, threads, 0, stream>>>(h->param + lo, h->mom + lo, h->grad + lo, hi - lo,
-                                                                sgd->lr, sgd->momentum, lam, sgd->grad_scale, nullptr,
-                                                                nullptr, nullptr);
+                                                                sgd->lr, sgd->momentum, sgd->weight_decay, decay_end,
+                                                                sgd->grad_scale, nullptr, nullptr, nullptr);
     SMLP_CK_LAUNCH(h, "sgd_update4_kernel");
     return SMLP_OK;
 }
@@ -2329,6 +2351,32 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
     // L2 requests rather than HBM bytes) runs on a side stream as soon as that slice is updated, so
     // it overlaps the next slice's streaming update
     const int64_t n = h->param_count;
+    if (n <= SMALL_MODEL_PARAMS) {
+        // small models are launch-bound: one Eq. 1 launch over the whole view (decay below
+        // bias_base) and one mirror refresh for all layers, both on the handle's stream
+        prof_start(h, K_SGD, 0, 20.0 * (double)n, 0.0);
+        SMLP_TRY(launch_update(h, h->stream, 0, n, true, sgd));
+        MirrorSet M{};
+        int nl = 0;
+        int64_t cmax = 1;
+        for (auto& Ly : h->layers) {
+            if (Ly.narrow) continue;                               // narrow layers never read the mirror copy
+            M.val[nl] = Ly.val;
+            M.mperm[nl] = Ly.mperm;
+            M.meta[nl] = Ly.meta;
+            M.mval[nl] = Ly.mval;
+            cmax = std::max<int64_t>(cmax, Ly.cap);
+            ++nl;
+        }
+        if (nl > 0) {
+            const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((cmax + 255) / 256, h->num_sms * 4)),
+                            (unsigned)nl);
+            mirror_values_multi_kernel<<<grid, 256, 0, h->stream>>>(M);
+            SMLP_CK_LAUNCH(h, "mirror_values_multi_kernel");
+        }
+        prof_stop(h);
+        return SMLP_OK;
+    }
     SMLP_TRY(ensure_aux(h));
     auto update = [&](int64_t lo, int64_t hi, bool decay) { return launch_update(h, h->stream, lo, hi, decay, sgd); };
     prof_start(h, K_SGD, 0, 20.0 * (double)n, 0.0);

@@ -62,7 +62,7 @@ class smlp_config(C.Structure):
                 ("activation", C.c_int32), ("alpha", C.c_float), ("dropout", C.c_float),
                 ("init", C.c_int32), ("seed", C.c_uint64), ("rank", C.c_int32), ("max_batch", C.c_int32),
                 ("chunk_batch", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p),
-                ("allocator", C.POINTER(smlp_allocator))]
+                ("allocator", C.POINTER(smlp_allocator)), ("input_kind", C.c_int32)]
 
 
 class smlp_sgd(C.Structure):
@@ -191,7 +191,7 @@ class SparseMLP:
     def __init__(self, sizes: Sequence[int], epsilon: float, activation: str = "all_relu", alpha: float = 0.5,
                  dropout: float = 0.0, init: str = "he_uniform", seed: int = 0, rank: int = 0,
                  max_batch: int = 128, chunk_batch: int = 0, device: Optional[int] = None,
-                 use_torch_allocator: bool = True):
+                 use_torch_allocator: bool = True, input_kind: int = 0):
         import torch
         self._torch = torch
         self.lib = load_library()
@@ -220,7 +220,7 @@ class SparseMLP:
             stream = torch.cuda.current_stream().cuda_stream
             cfg = smlp_config(self.L, self._sizes_c, float(epsilon), ACTIVATIONS[activation], float(alpha),
                               float(dropout), INITS[init], int(seed) & (2**64 - 1), int(rank), int(max_batch),
-                              int(chunk_batch), self.device, C.c_void_p(stream), alloc_p)
+                              int(chunk_batch), self.device, C.c_void_p(stream), alloc_p, int(input_kind))
             h = C.c_void_p()
             rc = self.lib.sparse_mlp_create(C.byref(cfg), C.byref(h))
         if rc != 0:
@@ -472,5 +472,8 @@ class SparseMLP:
 def from_config(cfg, seed: Optional[int] = None, rank: int = 0, max_batch: Optional[int] = None,
                 chunk_batch: int = 0, device: Optional[int] = None) -> SparseMLP:
     """Build a SparseMLP from a synth.WorkloadConfig-like object (sizes, epsilon, ...)."""
+    # configs whose inputs are known real-valued skip the {0,1} detection and the bit path
+    kind = 0 if getattr(cfg, "binary_input", True) else 1
     return SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init,
-                     cfg.model_seed if seed is None else seed, rank, max_batch or cfg.batch, chunk_batch, device)
+                     cfg.model_seed if seed is None else seed, rank, max_batch or cfg.batch, chunk_batch, device,
+                     input_kind=kind)

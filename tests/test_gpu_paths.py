@@ -94,6 +94,32 @@ def test_binary_path_falls_back_on_non_binary_input():
     _check_step(g2, st2, X, Y, 0, cfg, 1.0)
 
 
+def test_real_input_kind_skips_the_bit_path():
+    """input_kind = SMLP_INPUT_REAL: no {0,1} detection and no bit path (trace flag -1), the fp32
+    gather kernels serve layer 2 even for a binary batch, same parity; and the small-model update
+    (one Eq. 1 launch over the whole view + one mirror launch) matches the oracle's Eq. 1."""
+    from paper_2102_01732_b200 import SGD, SparseMLP
+    torch = _torch()
+    cfg = _binary_cfg(batch=64, dropout=0.3)
+    st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed)
+    g = SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed, 0, 64,
+                  32, input_kind=1)
+    X, Y = _binary_data(128, cfg.sizes[0], seed=21)
+    sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay)
+    for s_ in range(2):
+        x, y = X[s_ * 64:(s_ + 1) * 64], Y[s_ * 64:(s_ + 1) * 64]
+        tr = M.forward(st, x, True, s_)
+        assert sum(tr.ambiguous) == 0
+        g.forward(to_dev(x), train=True, step=s_)
+        assert g.sparse_mlp_export_trace(4, 0)[0] == -1.0
+        for l in range(2, cfg.n_layers):
+            assert rel_err(g.sparse_mlp_export_trace(0, l, 64), tr.a[l - 1]) <= TOL, ("a", l)
+        g.backward(to_dev(y), fused=sgd)
+        M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, s_)
+    torch.cuda.synchronize()
+    assert_values_close(g, st, TOL * 2, "real input kind")
+
+
 def test_binary_and_fp32_paths_agree_on_forward():
     """The bit path and the fp32 gather path compute the same a_2 up to the summation order
     (each is a fixed order, R27): every batch row but the changed one agrees to fp32 rounding."""
