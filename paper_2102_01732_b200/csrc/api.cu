@@ -165,6 +165,9 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
     h->param = zalloc<float>(h, (size_t)off, &rc);
     h->mom = zalloc<float>(h, (size_t)off, &rc);
     h->grad = zalloc<float>(h, (size_t)off, &rc);
+    // the fused path's last backward chunk writes its own gradient buffer, so no chunk kernel
+    // re-reads the earlier chunks' sum (the Eq. 1 pass adds the two); large models only
+    if (off > SMALL_MODEL_PARAMS) h->grad2 = zalloc<float>(h, (size_t)off, &rc);
     if (rc) return rc;
     const int CB = h->CB;
     for (auto& Ly : h->layers) {
@@ -353,6 +356,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     if (const char* e = std::getenv("SMLP_L2PERSIST")) h->l2persist = std::atoi(e);
     if (const char* e = std::getenv("SMLP_FUSED_UPDATE")) h->fused_update = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_OVERLAP_UPDATE")) h->overlap_update = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMLP_SPLIT_GRAD")) h->split_grad = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_UPDATE_SCATTER")) h->update_scatter = std::atoi(e) != 0;
     const int rc = build_handle(h, cfg);
     if (rc != SMLP_OK) {
@@ -476,9 +480,9 @@ int sparse_mlp_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_
         if (h->overlap_update) {
             // each layer's Eq. 1 slice + mirror refresh start on the aux stream as soon as its
             // gradient is final, overlapping the rest of the backward; the biases and the join last
-            rc = run_backward(h, labels, y_idx, loss, nullptr, &f);
+            rc = run_backward(h, labels, y_idx, loss, nullptr, &f, h->split_grad);
         } else {
-            rc = run_backward(h, labels, y_idx, loss, nullptr);
+            rc = run_backward(h, labels, y_idx, loss, nullptr, nullptr, h->split_grad);
             if (rc == SMLP_OK) rc = run_step(h, &f);
         }
     } else {

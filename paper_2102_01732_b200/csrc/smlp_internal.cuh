@@ -82,6 +82,7 @@ struct Layer {
     int nout_pad = 0;       // next power of two >= n_out (>= 2)
     int ngrid = 0;          // CTAs of the narrow forward
     float* nws = nullptr;   // [ngrid][nout_pad][CB] CTA partial logits
+    bool split = false;     // the last backward chunk's gradient is in grad2 (the Eq. 1 pass adds it)
     // biases of neuron layer l live in param/mom/grad at bias_off
     float* bias = nullptr;
     float* bias_mom = nullptr;
@@ -128,6 +129,7 @@ struct smlp_handle {
     float* param = nullptr;
     float* mom = nullptr;
     float* grad = nullptr;
+    float* grad2 = nullptr;         // large models: the last chunk's gradient of the fused path
     int64_t param_count = 0;
     int64_t bias_base = 0;
 
@@ -173,6 +175,7 @@ struct smlp_handle {
     int l2persist = 0;              // SMLP_L2PERSIST (percent): persisting-L2 window on the gathered slabs
     int fused_update = 0;           // SMLP_FUSED_UPDATE: Eq. 1 inside the last chunk's backward
     int update_scatter = 0;         // SMLP_UPDATE_SCATTER: the Eq. 1 pass scatters w into mval (no mirror gather)
+    int split_grad = 1;             // SMLP_SPLIT_GRAD: fused path, last chunk's gradient to grad2 (no re-read)
     int overlap_update = 0;         // SMLP_OVERLAP_UPDATE: each layer's Eq. 1 pass + mirror refresh on the
                                     // aux stream as soon as its gradient is final (overlaps the backward;
                                     // C5: 6.040 -> 6.025 ms, the backward kernels slow down by what the
@@ -295,7 +298,7 @@ int launch_grid(const smlp_handle* h, int64_t items, int threads);
 int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, bool train,
                 uint64_t step, float* probs);
 int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss,
-                 const smlp_sgd* fused, const smlp_sgd* overlap_sgd = nullptr);
+                 const smlp_sgd* fused, const smlp_sgd* overlap_sgd = nullptr, bool split_last = false);
 int run_step(smlp_handle* h, const smlp_sgd* sgd);
 int refresh_mirror_values(smlp_handle* h, Layer& Ly);
 

@@ -648,6 +648,7 @@ struct BwdArgs {
     float keep_scale_prev;
     int dropout_prev;
     int first, last;          // first / last chunk processed for this layer (grad accumulation)
+    int no_gold;              // the last chunk writes its own gradient buffer (the Eq. 1 pass adds both)
     int fused;
     float lr, mu, wd;
     const int32_t* skip_if_binary;   // layer 2 with the binary-input path: return if *flag == 0
@@ -1666,9 +1667,10 @@ __global__ void grad_from_mirror_kernel(const int32_t* __restrict__ nonbinary, c
 // (evict_last): the mirror gather of the same layer reads it right after.
 // SCATTER: also write each updated w into its mirror slot mval[minv[k]] (k < the layer's device
 // nnz), replacing the separate mirror gather
-template <bool SCATTER>
+template <bool SCATTER, bool G2>
 __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w, float* __restrict__ v,
-                                                          const float* __restrict__ g, int64_t n, float lr,
+                                                          const float* __restrict__ g, const float* __restrict__ g2,
+                                                          int64_t n, float lr,
                                                           float mu, float wd, int64_t decay_end, float gs,
                                                           const int32_t* __restrict__ minv, float* __restrict__ mval,
                                                           const LayerMeta* __restrict__ meta) {
@@ -1695,11 +1697,21 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
         o.w = mu * vk.w - lr * (gs * gk.w + lam * wk.w);
         return o;
     };
+    // the gradient: g, or (split last chunk) g2 + g = the last chunk's partial + the earlier
+    // chunks' sum, the same two operands the in-kernel accumulation adds
+    auto gload = [&](int64_t k4) {
+        float4 a = ldg4_hint(g + 4 * k4, pf);
+        if (G2) {
+            const float4 b = ldg4_hint(g2 + 4 * k4, pf);
+            a = make_float4(b.x + a.x, b.y + a.y, b.z + a.z, b.w + a.w);
+        }
+        return a;
+    };
     int64_t k = tid;
     for (; k + stride < n4; k += 2 * stride) {
         const int64_t k2 = k + stride;
-        const float4 w0 = ld4_hint(w + 4 * k, pl), v0 = ld4_hint(v + 4 * k, pf), g0 = ldg4_hint(g + 4 * k, pf);
-        const float4 w1 = ld4_hint(w + 4 * k2, pl), v1 = ld4_hint(v + 4 * k2, pf), g1 = ldg4_hint(g + 4 * k2, pf);
+        const float4 w0 = ld4_hint(w + 4 * k, pl), v0 = ld4_hint(v + 4 * k, pf), g0 = gload(k);
+        const float4 w1 = ld4_hint(w + 4 * k2, pl), v1 = ld4_hint(v + 4 * k2, pf), g1 = gload(k2);
         const float4 a = upd(w0, v0, g0, k), b = upd(w1, v1, g1, k2);
         const float4 wa = make_float4(w0.x + a.x, w0.y + a.y, w0.z + a.z, w0.w + a.w);
         const float4 wb = make_float4(w1.x + b.x, w1.y + b.y, w1.z + b.z, w1.w + b.w);
@@ -1711,7 +1723,7 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
         scatter(k2, wb);
     }
     if (k < n4) {
-        const float4 w0 = ld4_hint(w + 4 * k, pl), v0 = ld4_hint(v + 4 * k, pf), g0 = ldg4_hint(g + 4 * k, pf);
+        const float4 w0 = ld4_hint(w + 4 * k, pl), v0 = ld4_hint(v + 4 * k, pf), g0 = gload(k);
         const float4 a = upd(w0, v0, g0, k);
         const float4 wa = make_float4(w0.x + a.x, w0.y + a.y, w0.z + a.z, w0.w + a.w);
         st4_hint(v + 4 * k, a, pf);
@@ -1721,7 +1733,8 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
     if (tid < n - 4 * n4) {   // tail (n % 4 parameters)
         const int64_t t = 4 * n4 + tid;
         const float lam = t < decay_end ? wd : 0.f;
-        const float wk = w[t], vk = mu * v[t] - lr * (gs * g[t] + lam * wk);
+        const float gt = G2 ? g2[t] + g[t] : g[t];
+        const float wk = w[t], vk = mu * v[t] - lr * (gs * gt + lam * wk);
         v[t] = vk;
         w[t] = wk + vk;
         if (SCATTER && t < nnz) mval[minv[t]] = wk + vk;
@@ -1795,7 +1808,7 @@ int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
 template <int CB, int CBF>
 int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev) {
     constexpr int P = 32 / (CB / 4);
-    const bool gold = !A.first, upd = A.last && A.fused, drop = A.dropout_prev != 0;
+    const bool gold = !A.first && !A.no_gold, upd = A.last && A.fused, drop = A.dropout_prev != 0;
     const int mode = (has_dprev ? 8 : 0) | (gold ? 4 : 0) | (upd ? 2 : 0) | (drop ? 1 : 0);
 #define SMLP_BWD_ROWS(HD, GO, UP, DR)                                                                          \
 case (HD ? 8 : 0) | (GO ? 4 : 0) | (UP ? 2 : 0) | (DR ? 1 : 0):                                         \
@@ -2138,7 +2151,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
 // Eq. 1 over the parameter slice [lo, hi) on `stream`: one resident wave (8 CTAs of 256 per SM),
 // two float4 groups per thread and iteration
 static int launch_update(smlp_handle* h, cudaStream_t stream, int64_t lo, int64_t hi, bool decay, const smlp_sgd* sgd,
-                         const Layer* mirror = nullptr) {
+                         const Layer* mirror = nullptr, bool g2 = false) {
     if (hi <= lo) return SMLP_OK;
     constexpr int threads = 256;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((hi - lo + 4 * threads - 1) / (4 * threads),
@@ -2146,14 +2159,24 @@ static int launch_update(smlp_handle* h, cudaStream_t stream, int64_t lo, int64_
     // decay: weights (all of [lo, hi)), or none (biases), or -- for the single whole-view launch of
     // small models -- everything below bias_base
     const int64_t decay_end = decay ? std::min(hi, h->bias_base) - lo : 0;
-    if (mirror)
-        sgd_update4_kernel<true><<<grid, threads, 0, stream>>>(h->param + lo, h->mom + lo, h->grad + lo, hi - lo, sgd->lr,
-                                                               sgd->momentum, sgd->weight_decay, decay_end,
-                                                               sgd->grad_scale, mirror->minv, mirror->mval, mirror->meta);
+    float* w = h->param + lo;
+    float* v = h->mom + lo;
+    const float* g = h->grad + lo;
+    const float* gb = g2 ? h->grad2 + lo : nullptr;
+    const float lr = sgd->lr, mu = sgd->momentum, wd = sgd->weight_decay, gs = sgd->grad_scale;
+    const int64_t n = hi - lo;
+    if (mirror && g2)
+        sgd_update4_kernel<true, true><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs,
+                                                                     mirror->minv, mirror->mval, mirror->meta);
+    else if (mirror)
+        sgd_update4_kernel<true, false><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs,
+                                                                      mirror->minv, mirror->mval, mirror->meta);
+    else if (g2)
+        sgd_update4_kernel<false, true><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs,
+                                                                      nullptr, nullptr, nullptr);
     else
-        sgd_update4_kernel<false><<<grid, threads, 0, stream>>>(h->param + lo, h->mom + lo, h->grad + lo, hi - lo,
-                                                                sgd->lr, sgd->momentum, sgd->weight_decay, decay_end,
-                                                                sgd->grad_scale, nullptr, nullptr, nullptr);
+        sgd_update4_kernel<false, false><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs,
+                                                                       nullptr, nullptr, nullptr);
     SMLP_CK_LAUNCH(h, "sgd_update4_kernel");
     return SMLP_OK;
 }
@@ -2171,7 +2194,8 @@ static int overlap_layer_update(smlp_handle* h, Layer& Ly, const smlp_sgd* sgd) 
     SMLP_TRY(ensure_aux(h));
     SMLP_CK(h, cudaEventRecord(h->aux_ev[0], h->stream));
     SMLP_CK(h, cudaStreamWaitEvent(h->aux_stream, h->aux_ev[0], 0));
-    SMLP_TRY(launch_update(h, h->aux_stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd));
+    SMLP_TRY(launch_update(h, h->aux_stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd, nullptr, Ly.split));
+    Ly.split = false;
     if (!Ly.narrow) {   // narrow layers never read the mirror copy
         mirror_values_kernel<<<launch_grid(h, (Ly.cap + 3) / 4, 256), 256, 0, h->aux_stream>>>(Ly.val, Ly.mperm,
                                                                                                Ly.meta, Ly.mval);
@@ -2189,7 +2213,7 @@ static int layer_done(smlp_handle* h, int l) {
 }
 
 int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, const smlp_sgd* fused,
-                 const smlp_sgd* overlap_sgd) {
+                 const smlp_sgd* overlap_sgd, bool split_last) {
     const int CB = h->CB;
     const int B = h->trace_B;
     const int nchunks = (B + CB - 1) / CB;
@@ -2296,6 +2320,15 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.mu = mu;
             A.wd = wd;
             A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
+            // the last of several chunks writes its gradient to grad2 instead of adding the earlier
+            // chunks' sum (read back from grad); the Eq. 1 pass that follows adds the two
+            // (W^(2) with the bit path keeps one buffer: its gradient may come from the bit kernels)
+            Ly.split = false;
+            if (split_last && !fused && last && !first && h->grad2 && !(l == 2 && h->xbits)) {
+                A.grad = h->grad2 + Ly.val_off;
+                A.no_gold = 1;
+                Ly.split = true;
+            }
             A.zero_row = (int)((int64_t)(h->max_chunks - c) * nout);
             A.l2hint = h->l2hint;
             A.mval_scatter = (h->mirror_scatter && !(l == 2 && h->xbits)) ? 1 : 0;
@@ -2382,11 +2415,13 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
     prof_start(h, K_SGD, 0, 20.0 * (double)n, 0.0);
     bool side = false;
     for (auto& Ly : h->layers) {
+        const bool g2 = Ly.split;
+        Ly.split = false;
         if (h->update_scatter && !Ly.narrow) {                     // the update writes the mirror copy too
-            SMLP_TRY(launch_update(h, h->stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd, &Ly));
+            SMLP_TRY(launch_update(h, h->stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd, &Ly, g2));
             continue;
         }
-        SMLP_TRY(update(Ly.val_off, Ly.val_off + Ly.cap, true));
+        SMLP_TRY(launch_update(h, h->stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd, nullptr, g2));
         if (Ly.narrow) continue;                                   // narrow layers never read the mirror copy
         SMLP_CK(h, cudaEventRecord(h->aux_ev[0], h->stream));
         SMLP_CK(h, cudaStreamWaitEvent(h->aux_stream, h->aux_ev[0], 0));
