@@ -394,14 +394,14 @@ __device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, c
                          ? rng_stream(A.seed, P_DROPOUT, A.rank, A.layer, step_lo,
                                       ((uint64_t)j << 32) | (uint64_t)((A.b0 + q * 4) >> 2))
                          : make_uint4(0, 0, 0, 0);
+    float out[NR];
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
         const int c = r * P + g;
         const bool valid = c < 4;
         const float z = comp(acc, c & 3) + bj;
-        float* dst = A.a_out + j * CB + q * 4 + (c & 3);
         if (!A.hidden) {
-            if (valid) *dst = z;
+            out[r] = z;
             continue;
         }
         const bool pos = z > 0.f;
@@ -411,9 +411,18 @@ __device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, c
             keep = word(dr, c & 3) >= A.drop_thr;
             a = keep ? a * A.keep_scale : 0.f;
         }
-        if (valid) *dst = a;
+        out[r] = a;
         bal_p[r] = __ballot_sync(FULL, valid && pos);
         bal_k[r] = __ballot_sync(FULL, valid && keep);
+    }
+    if constexpr (P == 1) {   // the lane holds its 4 columns: one 16-B store
+        st4(A.a_out + j * CB + q * 4, make_float4(out[0], out[1], out[2], out[3]));
+    } else {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const int c = r * P + g;
+            if (c < 4) A.a_out[j * CB + q * 4 + c] = out[r];
+        }
     }
     if (A.hidden && lane == 0) {
         uint32_t zb[4], kb[4];
@@ -802,16 +811,27 @@ __device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, c
     const int g = lane / G, q = lane % G;
     const uint4 zb = sd.zb, kb = sd.kb;
     float s = 0.f;
+    float out[NR];
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
         const int c = r * P + g;
+        out[r] = 0.f;
         if (c < 4) {
             const bool pos = (word(zb, c) >> qb) & 1u;
             const bool keep = (word(kb, c) >> qb) & 1u;
             const float v = d[r] * (pos ? 1.f : A.neg_slope_prev);
             const float o = A.dropout_prev ? (keep ? v * A.keep_scale_prev : 0.f) : v;
-            A.d_prev[i * CB + q * 4 + c] = o;
+            out[r] = o;
             s += o;
+        }
+    }
+    if constexpr (P == 1) {   // the lane holds its 4 columns: one 16-B store
+        st4(A.d_prev + i * CB + q * 4, make_float4(out[0], out[1], out[2], out[3]));
+    } else {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const int c = r * P + g;
+            if (c < 4) A.d_prev[i * CB + q * 4 + c] = out[r];
         }
     }
 #pragma unroll
