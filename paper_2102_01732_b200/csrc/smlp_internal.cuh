@@ -176,6 +176,7 @@ struct smlp_handle {
     int fused_update = 0;           // SMLP_FUSED_UPDATE: Eq. 1 inside the last chunk's backward
     int update_scatter = 0;         // SMLP_UPDATE_SCATTER: the Eq. 1 pass scatters w into mval (no mirror gather)
     int split_grad = 1;             // SMLP_SPLIT_GRAD: fused path, last chunk's gradient to grad2 (no re-read)
+    int short_rows = 1;             // SMLP_SHORT_ROWS: row-streaming forward for 128-column layers of < 8 entries per row
     int overlap_update = 0;         // SMLP_OVERLAP_UPDATE: each layer's Eq. 1 pass + mirror refresh on the
                                     // aux stream as soon as its gradient is final (overlaps the backward;
                                     // C5: 6.040 -> 6.025 ms, the backward kernels slow down by what the

@@ -98,6 +98,11 @@ __device__ __forceinline__ float ld_hint(const float* p, uint64_t pol) {
     asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_hint_i(const int32_t* p, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
 __device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
 }
@@ -208,6 +213,7 @@ struct FwdArgs {
     const int32_t* skip_if_binary;   // layer 2 with the binary-input path: return if *flag == 0
     int zero_row;                    // row index (relative to a_prev) of the zero row after the last chunk
     int l2hint;                      // L2 policies: gathers evict_last, streamed operands evict_first
+    const int32_t* mrow_ptr;         // mirror row pointers (short-row streaming kernel)
 };
 
 // Epilogue of one output row j per group: all 32 lanes call it (ballots); `own` marks the
@@ -537,6 +543,77 @@ __global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(F
             ix[r] = ix_n[r];
             w[r] = w_n[r];
         }
+    }
+}
+
+// Short-row forward (128-column chunks, rows averaging < 8 entries: Table 4's eps = 1 layers).
+// The row kernel above spends one window / descriptor / batch round per row and has ~2 gathers
+// in flight per warp there.  This one streams a unit of 32 consecutive mirror rows as one entry
+// range: lane t loads entry t of each 32-entry block (coalesced), and the warp gathers 8 entries'
+// rows at a time across row boundaries (the lane's float4 = its 4 columns), then consumes them in
+// order, finishing each row (fwd_rows_epilogue) as its last entry is added -- the same sequential
+// sum per row as the row kernel, so the result is identical.
+constexpr int SHORT_ROWS = 32;
+__global__ void __launch_bounds__(256, 4) fwd_short_rows_kernel(FwdArgs A) {
+    constexpr int CB = 128, GU = 4;                 // gathers in flight per warp (4 x 16 B, 64 regs)
+    __shared__ int2 rec_all[WARPS_PER_BLOCK][32 + GU];
+    if (A.skip_if_binary && *A.skip_if_binary == 0) return;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int2* rec = rec_all[wib];
+    if (lane < GU) rec[32 + lane] = make_int2(A.zero_row, 0);          // never-consumed tail
+    const uint64_t pg = gather_policy(A.l2hint), ps = stream_policy(A.l2hint);
+    const uint32_t step_lo = A.step_ptr ? (uint32_t)(*A.step_ptr) : A.step_lo;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nunits = (A.n_out + SHORT_ROWS - 1) / SHORT_ROWS;
+    for (int64_t u0 = warp; u0 < nunits; u0 += nwarps) {
+        const int64_t j0 = u0 * SHORT_ROWS;
+        const int nrows = (int)(A.n_out - j0 < SHORT_ROWS ? A.n_out - j0 : SHORT_ROWS);
+        const int rp_l = __ldg(A.mrow_ptr + j0 + min(lane, nrows));      // lane t: start of local row t
+        const float b_l = lane < nrows ? __ldg(A.bias + j0 + lane) : 0.f;
+        const int E0 = __shfl_sync(FULL, rp_l, 0), E1 = __ldg(A.mrow_ptr + j0 + nrows);
+        int row = 0;
+        int row_end = nrows > 1 ? __shfl_sync(FULL, rp_l, 1) : E1;
+        float4 acc = f4zero();
+        auto finish_rows_at = [&](int e) {          // finish every row ending at entry e (empty rows too)
+            while (row < nrows && e == row_end) {
+                fwd_rows_epilogue<CB>(A, j0 + row, acc, __shfl_sync(FULL, b_l, row), lane, step_lo);
+                acc = f4zero();
+                ++row;
+                row_end = row + 1 < nrows ? __shfl_sync(FULL, rp_l, min(row + 1, 31)) : E1;
+            }
+        };
+        for (int blk = E0; blk < E1; blk += 32) {
+            const int n = min(32, E1 - blk);
+            __syncwarp();
+            rec[lane] = lane < n ? make_int2(ld_hint_i(A.msrc + blk + lane, ps), __float_as_int(ld_hint(A.mval + blk + lane, ps)))
+                                 : make_int2(A.zero_row, 0);
+            __syncwarp();
+            for (int v0 = 0; v0 < n; v0 += GU) {
+                float4 x[GU];
+                float wv[GU];
+#pragma unroll
+                for (int k = 0; k < GU; ++k) {      // GU rows in flight, across row boundaries
+                    const int2 e = rec[v0 + k];
+                    wv[k] = __int_as_float(e.y);
+                    x[k] = ldg4_hint(A.a_prev + (int64_t)e.x * CB + lane * 4, pg);
+                }
+                // consume in order, one row segment at a time (one epilogue call site): entries
+                // k .. stop-1 of this group belong to the current row
+                const int kmax = min(GU, n - v0);
+                int k = 0;
+                for (;;) {
+                    finish_rows_at(blk + v0 + k);
+                    if (k >= kmax) break;
+                    const int stop = min(kmax, row_end - (blk + v0));
+#pragma unroll
+                    for (int kk = 0; kk < GU; ++kk)
+                        if (kk >= k && kk < stop) fma4p(acc, wv[kk], x[kk]);
+                    k = stop;
+                }
+            }
+        }
+        finish_rows_at(E1);
     }
 }
 
@@ -1815,6 +1892,15 @@ int rows_grid(const smlp_handle* h, K kernel, int64_t segs) {
 template <int CB>
 int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
     constexpr int P = 32 / (CB / 4);
+    if constexpr (CB == 128) {
+        // layers of short rows (< 8 entries per mirror row on average): stream whole rows
+        if (h->short_rows && L.nnz < 8 * L.n_out) {
+            const int64_t units = (L.n_out + SHORT_ROWS - 1) / SHORT_ROWS;
+            fwd_short_rows_kernel<<<rows_grid(h, fwd_short_rows_kernel, units), WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+            SMLP_CK_LAUNCH(h, "fwd_short_rows_kernel");
+            return SMLP_OK;
+        }
+    }
     fwd_rows_kernel<CB><<<rows_grid(h, fwd_rows_kernel<CB>, L.fseg_cap), WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
     SMLP_CK_LAUNCH(h, "fwd_rows_kernel");
     if (L.fslot_cap > 0) {
@@ -2114,6 +2200,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             A.kmask = hidden ? h->kmask[l] + (int64_t)c * nout : nullptr;
             A.seg = Ly.fseg;
             A.multi = Ly.fmulti;
+            A.mrow_ptr = Ly.mrow_ptr;
             A.meta = Ly.meta;
             A.msrc = Ly.msrc;
             A.mval = Ly.mval;
