@@ -740,6 +740,8 @@ struct BwdArgs {
     const int32_t* skip_if_binary;   // layer 2 with the binary-input path: return if *flag == 0
     int zero_row;                    // row index (relative to d_out) of the zero row after the last chunk
     int l2hint;                      // L2 policies: gathers evict_last, streamed operands evict_first
+    const int32_t* row_ptr;          // canonical row pointers (short-row streaming kernel)
+    const int32_t* rowid;            // canonical row of each entry (short-row streaming kernel)
 };
 
 // Forward-layout position of a backward chunk's local column lc (CB = R CBF, R in {1, 2, 4}; the
@@ -1866,6 +1868,117 @@ __global__ void __launch_bounds__(256) mirror_values_kernel(const float* __restr
     if (tid < n - 4 * n4) mval[4 * n4 + tid] = __ldg(val + __ldg(mperm + 4 * n4 + tid));
 }
 
+// Short-row backward (128-column chunks, canonical rows averaging < 8 entries: the eps = 1
+// widths), the counterpart of fwd_short_rows_kernel: a warp streams 32 consecutive canonical rows
+// as one entry range (col, w, row id loaded coalesced per 32-entry block), gathers 4 entries'
+// delta_l[j] rows and a_{l-1}[i] rows at a time across row boundaries; per entry the SDDMM
+// partial is summed over the 32 lanes by a fixed butterfly and kept by lane (entry mod 32) for
+// one coalesced gradient store per block; delta_{l-1} rows are accumulated in entry order and
+// finished (bwd_rows_epilogue) as each row's last entry is added, with the rows' mask bits and
+// bias data loaded once per unit (lane t = row t).  No Eq. 1 in-kernel (the fused path's UPD
+// variant keeps the row kernel).
+template <bool HAS_DPREV, bool GOLD, bool DROP>
+__global__ void __launch_bounds__(256, 4) bwd_short_rows_kernel(BwdArgs A) {
+    constexpr int CB = 128, GU = 4, NR = RowCfg<CB>::NR;
+    __shared__ int4 rec_all[WARPS_PER_BLOCK][32 + GU];
+    if (A.skip_if_binary && *A.skip_if_binary == 0) return;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int4* rec = rec_all[wib];
+    const uint64_t pg = gather_policy(A.l2hint), ps = stream_policy(A.l2hint);
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nunits = (A.n_prev + SHORT_ROWS - 1) / SHORT_ROWS;
+    for (int64_t u0 = warp; u0 < nunits; u0 += nwarps) {
+        const int64_t i0 = u0 * SHORT_ROWS;
+        const int nrows = (int)(A.n_prev - i0 < SHORT_ROWS ? A.n_prev - i0 : SHORT_ROWS);
+        const int rp_l = __ldg(A.row_ptr + i0 + min(lane, nrows));
+        const int E0 = __shfl_sync(FULL, rp_l, 0), E1 = __ldg(A.row_ptr + i0 + nrows);
+        if (lane < GU) rec[32 + lane] = make_int4(A.zero_row, 0, (int)i0, 0);   // padding: zero delta row
+        // the unit's rows' epilogue side data, lane t = row t (loaded once, shuffled at the finish)
+        uint4 zb_l = make_uint4(0, 0, 0, 0), kb_l = make_uint4(FULL, FULL, FULL, FULL);
+        float bgs_l = 0.f, bmom_l = 0.f, bval_l = 0.f;
+        if (HAS_DPREV && lane < nrows) {
+            zb_l = A.zmask_prev[i0 + lane];
+            if (DROP) kb_l = A.kmask_prev[i0 + lane];
+            if (!A.first) bgs_l = A.bgs[i0 + lane];
+            if (A.last && A.fused) {
+                bmom_l = A.bias_mom_prev[i0 + lane];
+                bval_l = A.bias_prev[i0 + lane];
+            }
+        }
+        int row = 0;
+        int row_end = nrows > 1 ? __shfl_sync(FULL, rp_l, 1) : E1;
+        float4 dacc = f4zero();
+        auto finish_rows_at = [&](int e) {
+            while (row < nrows && e == row_end) {
+                if (HAS_DPREV) {
+                    BwdSide sd;
+                    sd.zb = make_uint4(__shfl_sync(FULL, zb_l.x, row), __shfl_sync(FULL, zb_l.y, row),
+                                       __shfl_sync(FULL, zb_l.z, row), __shfl_sync(FULL, zb_l.w, row));
+                    sd.kb = DROP ? make_uint4(__shfl_sync(FULL, kb_l.x, row), __shfl_sync(FULL, kb_l.y, row),
+                                              __shfl_sync(FULL, kb_l.z, row), __shfl_sync(FULL, kb_l.w, row))
+                                 : make_uint4(FULL, FULL, FULL, FULL);
+                    sd.bgs = __shfl_sync(FULL, bgs_l, row);
+                    sd.bmom = __shfl_sync(FULL, bmom_l, row);
+                    sd.bval = __shfl_sync(FULL, bval_l, row);
+                    const float d[NR] = {dacc.x, dacc.y, dacc.z, dacc.w};
+                    bwd_rows_epilogue<CB>(A, i0 + row, d, sd, lane, lane);
+                }
+                dacc = f4zero();
+                ++row;
+                row_end = row + 1 < nrows ? __shfl_sync(FULL, rp_l, min(row + 1, 31)) : E1;
+            }
+        };
+        for (int blk = E0; blk < E1; blk += 32) {
+            const int n = min(32, E1 - blk);
+            __syncwarp();
+            if (lane < n) {
+                const int k = blk + lane;
+                rec[lane] = make_int4(ld_hint_i(A.col + k, ps), __float_as_int(ld_hint(A.val + k, ps)),
+                                      ld_hint_i(A.rowid + k, ps), 0);
+            } else {
+                rec[lane] = make_int4(A.zero_row, 0, (int)i0, 0);
+            }
+            const float gold_l = GOLD && lane < n ? ld_hint(A.grad + blk + lane, ps) : 0.f;
+            __syncwarp();
+            float gval = 0.f;                              // lane t: the SDDMM gradient of entry t
+            for (int v0 = 0; v0 < n; v0 += GU) {
+                float4 x[GU], a[GU];
+                float wv[GU];
+#pragma unroll
+                for (int k = 0; k < GU; ++k) {
+                    const int4 e = rec[v0 + k];
+                    wv[k] = __int_as_float(e.y);
+                    x[k] = ldg4_hint(A.d_out + (int64_t)e.x * CB + lane * 4, pg);
+                    a[k] = ldg4_hint(A.a_prev + (int64_t)e.z * CB + lane * 4, ps);
+                }
+#pragma unroll
+                for (int k = 0; k < GU; ++k) {             // g = <a_{l-1}[i], delta_l[j]>, fixed butterfly
+                    float p = dot4p(a[k], x[k]);
+#pragma unroll
+                    for (int m = 16; m >= 1; m >>= 1) p += __shfl_xor_sync(FULL, p, m);
+                    if (lane == v0 + k) gval = p;
+                }
+                if (HAS_DPREV) {                           // delta_{l-1} rows, one row segment at a time
+                    const int kmax = min(GU, n - v0);
+                    int k = 0;
+                    for (;;) {
+                        finish_rows_at(blk + v0 + k);
+                        if (k >= kmax) break;
+                        const int stop = min(kmax, row_end - (blk + v0));
+#pragma unroll
+                        for (int kk = 0; kk < GU; ++kk)
+                            if (kk >= k && kk < stop) fma4p(dacc, wv[kk], x[kk]);
+                        k = stop;
+                    }
+                }
+            }
+            if (lane < n) st_hint(A.grad + blk + lane, gval + gold_l, ps);
+        }
+        if (HAS_DPREV) finish_rows_at(E1);
+    }
+}
+
 // grid of the finish kernels: their row count lives in device memory (graph-stable), so the grid
 // is sized for the capacity but capped at 2 blocks per SM (grid-stride loops): split rows are rare
 // (C5: ~0.03% of the rows), and a wider grid of mostly idle blocks costs a few microseconds per launch
@@ -1915,6 +2028,26 @@ template <int CB, int CBF>
 int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev) {
     constexpr int P = 32 / (CB / 4);
     const bool gold = !A.first && !A.no_gold, upd = A.last && A.fused, drop = A.dropout_prev != 0;
+    if constexpr (CB == 128 && CBF == 128) {
+        // layers of short canonical rows (< 8 entries on average): stream whole rows
+        if (h->short_rows && !upd && L.nnz < 8 * L.n_in) {
+            const int64_t units = (L.n_in + SHORT_ROWS - 1) / SHORT_ROWS;
+#define SMLP_BWD_SHORT(HD, GO, DR)                                                                          \
+    if (has_dprev == HD && gold == GO && drop == DR) {                                                    \
+        bwd_short_rows_kernel<HD, GO, DR><<<rows_grid(h, bwd_short_rows_kernel<HD, GO, DR>, units),             \
+                                            WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);                       \
+        SMLP_CK_LAUNCH(h, "bwd_short_rows_kernel");                                                       \
+        return SMLP_OK;                                                                                   \
+    }
+            SMLP_BWD_SHORT(true, false, false)
+            SMLP_BWD_SHORT(true, false, true)
+            SMLP_BWD_SHORT(true, true, false)
+            SMLP_BWD_SHORT(true, true, true)
+            SMLP_BWD_SHORT(false, false, false)
+            SMLP_BWD_SHORT(false, true, false)
+#undef SMLP_BWD_SHORT
+        }
+    }
     const int mode = (has_dprev ? 8 : 0) | (gold ? 4 : 0) | (upd ? 2 : 0) | (drop ? 1 : 0);
 #define SMLP_BWD_ROWS(HD, GO, UP, DR)                                                                          \
 case (HD ? 8 : 0) | (GO ? 4 : 0) | (UP ? 2 : 0) | (DR ? 1 : 0):                                         \
@@ -2403,6 +2536,8 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.zmask_prev = has_dprev ? h->zmask[l - 1] + (int64_t)fc * nin : nullptr;
             A.kmask_prev = has_dprev ? h->kmask[l - 1] + (int64_t)fc * nin : nullptr;
             A.n_prev = nin;
+            A.row_ptr = Ly.row_ptr;
+            A.rowid = Ly.rowid;
             A.seg = Ly.bseg;
             A.multi = Ly.bmulti;
             A.meta = Ly.meta;

@@ -269,7 +269,9 @@ def test_width_scaling_t2_full_size_sampled_parity():
                           # sparse narrow output layer (bwd_narrow_kernel instead of the dense-capped rows kernel)
                           (64, 64, 90, 0.2, 5.0, 0), (64, 32, 90, 0.2, 5.0, 0), (128, 32, 128, 0.0, 5.0, 0),
                           # 3 forward chunks: the output layer's forward pass covers 96 of its 128 columns
-                          (64, 32, 70, 0.2, 5.0, 0), (128, 32, 70, 0.0, 40.0, 0)])
+                          (64, 32, 70, 0.2, 5.0, 0), (128, 32, 70, 0.0, 40.0, 0),
+                          # eps = 1: ~1-8 entries per row -> the row-streaming short-row kernels
+                          (128, 128, 128, 0.2, 1.0, 0), (128, 128, 77, 0.0, 1.0, 0)])
 def test_long_rows_and_chunk_widths_parity(chunk, fchunk, B, dropout, eps, salt, monkeypatch):
     """Rows longer than one 64-entry segment in both orientations (partials + fixed-order finish
     kernels), every chunk width of the row kernels (slot / group layouts, ragged last chunk), the
