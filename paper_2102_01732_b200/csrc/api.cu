@@ -357,6 +357,9 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     if (const char* e = std::getenv("SMLP_FUSED_UPDATE")) h->fused_update = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_OVERLAP_UPDATE")) h->overlap_update = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_SHORT_ROWS")) h->short_rows = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMLP_SHORT_MAX_FWD")) h->short_max_fwd = std::atoi(e);
+    if (const char* e = std::getenv("SMLP_SHORT_MAX_BWD")) h->short_max_bwd = std::atoi(e);
+    if (const char* e = std::getenv("SMLP_SHORT_MIN_ROWS")) h->short_min_rows = std::atoll(e);
     if (const char* e = std::getenv("SMLP_SPLIT_GRAD")) h->split_grad = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_UPDATE_SCATTER")) h->update_scatter = std::atoi(e) != 0;
     const int rc = build_handle(h, cfg);

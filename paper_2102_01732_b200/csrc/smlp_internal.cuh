@@ -176,6 +176,9 @@ struct smlp_handle {
     int fused_update = 0;           // SMLP_FUSED_UPDATE: Eq. 1 inside the last chunk's backward
     int update_scatter = 0;         // SMLP_UPDATE_SCATTER: the Eq. 1 pass scatters w into mval (no mirror gather)
     int split_grad = 1;             // SMLP_SPLIT_GRAD: fused path, last chunk's gradient to grad2 (no re-read)
+    int64_t short_min_rows = -1;    // SMLP_SHORT_MIN_ROWS: -1 = one 32-row unit per resident warp
+    int short_max_fwd = 16;         // SMLP_SHORT_MAX_FWD / _BWD: average entries per row below which the
+    int short_max_bwd = 8;          //   streaming kernels run (T2/T3 at ~10: forward -5%, backward +80%)
     int short_rows = 1;             // SMLP_SHORT_ROWS: row-streaming forward for 128-column layers of < 8 entries per row
     int overlap_update = 0;         // SMLP_OVERLAP_UPDATE: each layer's Eq. 1 pass + mirror refresh on the
                                     // aux stream as soon as its gradient is final (overlaps the backward;

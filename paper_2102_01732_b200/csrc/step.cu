@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(F
     }
 }
 
-// Short-row forward (128-column chunks, rows averaging < 8 entries: Table 4's eps = 1 layers).
+// Short-row forward (128-column chunks, rows averaging < 16 entries: Table 4's eps <= 5 layers).
 // The row kernel above spends one window / descriptor / batch round per row and has ~2 gathers
 // in flight per warp there.  This one streams a unit of 32 consecutive mirror rows as one entry
 // range: lane t loads entry t of each 32-entry block (coalesced), and the warp gathers 8 entries'
@@ -2002,12 +2002,20 @@ int rows_grid(const smlp_handle* h, K kernel, int64_t segs) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)per_sm * h->num_sms));
 }
 
+// rows a layer needs for the streaming short-row kernels: one 32-row unit per resident warp
+// (SMLP_SHORT_MIN_ROWS overrides, e.g. 0 for small parity tests)
+static int64_t short_min_rows(const smlp_handle* h) {
+    return h->short_min_rows >= 0 ? h->short_min_rows : (int64_t)SHORT_ROWS * 32 * h->num_sms;
+}
+
 template <int CB>
 int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
     constexpr int P = 32 / (CB / 4);
     if constexpr (CB == 128) {
-        // layers of short rows (< 8 entries per mirror row on average): stream whole rows
-        if (h->short_rows && L.nnz < 8 * L.n_out) {
+        // layers of short rows (< 16 entries per mirror row on average): stream whole rows
+        // (and enough 32-row units to give every resident warp one: a narrow layer keeps the row kernel)
+        if (h->short_rows && L.nnz < (int64_t)h->short_max_fwd * L.n_out &&
+            L.n_out >= short_min_rows(h)) {
             const int64_t units = (L.n_out + SHORT_ROWS - 1) / SHORT_ROWS;
             fwd_short_rows_kernel<<<rows_grid(h, fwd_short_rows_kernel, units), WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
             SMLP_CK_LAUNCH(h, "fwd_short_rows_kernel");
@@ -2030,7 +2038,8 @@ int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev)
     const bool gold = !A.first && !A.no_gold, upd = A.last && A.fused, drop = A.dropout_prev != 0;
     if constexpr (CB == 128 && CBF == 128) {
         // layers of short canonical rows (< 8 entries on average): stream whole rows
-        if (h->short_rows && !upd && L.nnz < 8 * L.n_in) {
+        if (h->short_rows && !upd && L.nnz < (int64_t)h->short_max_bwd * L.n_in &&
+            L.n_in >= short_min_rows(h)) {
             const int64_t units = (L.n_in + SHORT_ROWS - 1) / SHORT_ROWS;
 #define SMLP_BWD_SHORT(HD, GO, DR)                                                                          \
     if (has_dprev == HD && gold == GO && drop == DR) {                                                    \

@@ -283,6 +283,8 @@ def test_long_rows_and_chunk_widths_parity(chunk, fchunk, B, dropout, eps, salt,
     # at eps 40 has ~70-entry canonical rows and ~93-entry mirror rows
     cfg = get_config("C1", sizes=(30, 200, 150, 10), epsilon=eps, alpha=0.6, dropout=dropout, batch=B)
     monkeypatch.setenv("SMLP_FWD_CB", str(fchunk))
+    if eps == 1.0:   # the row-streaming short-row kernels, at this small size too
+        monkeypatch.setenv("SMLP_SHORT_MIN_ROWS", "0")
     g, st = pair(cfg, max_batch=B, chunk_batch=chunk)
     assert (g.info()["chunk_batch"], g.info()["fwd_chunk_batch"]) == (chunk, fchunk)
     assert st.layers[-1].dense_capped == (eps == 40.0)
