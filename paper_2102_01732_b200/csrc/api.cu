@@ -201,6 +201,9 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
         // narrow output layer: stream the canonical rows instead of gathering
         Ly.nout_pad = std::max(2, next_pow2((int)std::min<int64_t>(Ly.n_out, 1 << 20)));
         Ly.narrow = Ly.l == L && Ly.n_out <= NARROW_MAX && (int64_t)Ly.nout_pad * CB <= NARROW_MAX_ELEMS;
+        // backward: the row streaming pays for dense-capped rows (all n_L outputs per input row);
+        // a sparse output layer's short canonical rows go through the row kernels (C3: 70 -> 19 us)
+        Ly.narrow_bwd = Ly.narrow && (Ly.dense || h->narrow_sparse_bwd);
         if (Ly.narrow) {
             Ly.ngrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->num_sms * 4, (Ly.n_in + 63) / 64));
             // CTA partials of a forward pass of up to 128 columns (several forward chunks)
@@ -357,6 +360,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     if (const char* e = std::getenv("SMLP_FUSED_UPDATE")) h->fused_update = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_OVERLAP_UPDATE")) h->overlap_update = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_SHORT_ROWS")) h->short_rows = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMLP_NARROW_SPARSE_BWD")) h->narrow_sparse_bwd = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_SHORT_MAX_FWD")) h->short_max_fwd = std::atoi(e);
     if (const char* e = std::getenv("SMLP_SHORT_MAX_BWD")) h->short_max_bwd = std::atoi(e);
     if (const char* e = std::getenv("SMLP_SHORT_MIN_ROWS")) h->short_min_rows = std::atoll(e);

@@ -83,6 +83,7 @@ struct Layer {
     int ngrid = 0;          // CTAs of the narrow forward
     float* nws = nullptr;   // [ngrid][nout_pad][CB] CTA partial logits
     bool split = false;     // the last backward chunk's gradient is in grad2 (the Eq. 1 pass adds it)
+    bool narrow_bwd = false; // the backward of a narrow layer streams its rows too (dense-capped only by default)
     // biases of neuron layer l live in param/mom/grad at bias_off
     float* bias = nullptr;
     float* bias_mom = nullptr;
@@ -176,6 +177,7 @@ struct smlp_handle {
     int fused_update = 0;           // SMLP_FUSED_UPDATE: Eq. 1 inside the last chunk's backward
     int update_scatter = 0;         // SMLP_UPDATE_SCATTER: the Eq. 1 pass scatters w into mval (no mirror gather)
     int split_grad = 1;             // SMLP_SPLIT_GRAD: fused path, last chunk's gradient to grad2 (no re-read)
+    int narrow_sparse_bwd = 0;      // SMLP_NARROW_SPARSE_BWD: narrow row-streaming backward also for a sparse output layer
     int64_t short_min_rows = -1;    // SMLP_SHORT_MIN_ROWS: -1 = one 32-row unit per resident warp
     int short_max_fwd = 16;         // SMLP_SHORT_MAX_FWD / _BWD: average entries per row below which the
     int short_max_bwd = 8;          //   streaming kernels run (T2/T3 at ~10: forward -5%, backward +80%)

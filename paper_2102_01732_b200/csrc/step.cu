@@ -2511,7 +2511,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             const double act_bytes = 4.0 * Bc * (double)(nin + nout + (has_dprev ? nin : 0));
             const int dropout_prev = (has_dprev && h->trace_train && h->dropout > 0.f) ? 1 : 0;
             const float keep_scale = (float)(1.0 / (1.0 - (double)h->dropout));
-            if (Ly.narrow) {
+            if (Ly.narrow_bwd) {
                 NarrowArgs A = narrow_args(h, Ly, c, false);
                 A.d_out = h->delta[l] + (int64_t)c * nout * CB;
                 A.d_prev = has_dprev ? h->delta[l - 1] + (int64_t)c * nin * CB : nullptr;

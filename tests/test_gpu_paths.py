@@ -266,7 +266,8 @@ def test_width_scaling_t2_full_size_sampled_parity():
                           (64, 64, 128, 0.0, 40.0, 0), (128, 128, 128, 0.2, 40.0, 0),
                           # mixed layout: forward tensors CBf wide, deltas CB wide (ragged both ways)
                           (64, 32, 100, 0.3, 40.0, 0), (128, 32, 128, 0.2, 40.0, 0), (128, 64, 77, 0.0, 40.0, 0),
-                          # sparse narrow output layer (bwd_narrow_kernel instead of the dense-capped rows kernel)
+                          # sparse narrow output layer: row-streaming forward; backward through the row
+                          # kernels, or (chunk == fchunk == 64) the narrow bwd_narrow_kernel (SMLP_NARROW_SPARSE_BWD)
                           (64, 64, 90, 0.2, 5.0, 0), (64, 32, 90, 0.2, 5.0, 0), (128, 32, 128, 0.0, 5.0, 0),
                           # 3 forward chunks: the output layer's forward pass covers 96 of its 128 columns
                           (64, 32, 70, 0.2, 5.0, 0), (128, 32, 70, 0.0, 40.0, 0),
@@ -285,6 +286,8 @@ def test_long_rows_and_chunk_widths_parity(chunk, fchunk, B, dropout, eps, salt,
     monkeypatch.setenv("SMLP_FWD_CB", str(fchunk))
     if eps == 1.0:   # the row-streaming short-row kernels, at this small size too
         monkeypatch.setenv("SMLP_SHORT_MIN_ROWS", "0")
+    if eps == 5.0 and chunk == fchunk == 64:
+        monkeypatch.setenv("SMLP_NARROW_SPARSE_BWD", "1")
     g, st = pair(cfg, max_batch=B, chunk_batch=chunk)
     assert (g.info()["chunk_batch"], g.info()["fwd_chunk_batch"]) == (chunk, fchunk)
     assert st.layers[-1].dense_capped == (eps == 40.0)
