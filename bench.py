@@ -261,6 +261,7 @@ def main():
                     model.forward(X, x_idx=iw, train=True, step=0)
                     model.backward(Y, y_idx=iw, loss=loss, fused=sgd_g)
                     counter.add_(1)
+                model.join()                                 # the library's side-stream work rejoins the capture
         torch.cuda.current_stream().wait_stream(cap_stream)
         launches_per_step = (model.info()["launches"] - l_cap0) / G
         torch.cuda.synchronize()

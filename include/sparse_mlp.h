@@ -206,6 +206,15 @@ int sparse_mlp_train_step_host_async(smlp_handle* h, const float* x_host, const 
  * deferred device error (SMLP_E_DATA label out of range). */
 int sparse_mlp_sync(smlp_handle* h);
 
+/* sparse_mlp_join — enqueue on the handle's stream the waits for work the library left running
+ * on its side stream: the Eq. 1 pass (sparse_mlp_backward with SGD / sparse_mlp_step) refreshes
+ * each layer's mirror-ordered weight copy there and joins it lazily (the next forward waits for
+ * layer l's copy right before layer l; every other call joins all first).  No host sync; CUDA-
+ * graph capturable.  A stream capture that contains a training step must call it before the
+ * capture ends (the side-stream work has to rejoin the capturing stream).  Errors: SMLP_E_ARG
+ * (NULL handle), SMLP_E_CUDA. */
+int sparse_mlp_join(smlp_handle* h);
+
 /* Contiguous device views [values of W^(2..L) at their capacity offsets || biases b_2..b_L],
  * identical layout on every replica, stable for the life of the handle (holes left by
  * pruning are zero).  grad view: filled by an unfused backward (X1 allreduce, SUM).

@@ -151,6 +151,8 @@ struct smlp_handle {
     cudaStream_t copy_stream = nullptr;        // H2D of the next host batch, overlapping the current step
     cudaStream_t aux_stream = nullptr;         // mirror refreshes overlapping the Eq. 1 pass (run_step)
     cudaEvent_t aux_ev[2] = {nullptr, nullptr};
+    cudaEvent_t mirror_ev[SMLP_MAX_LAYERS + 1] = {nullptr};   // deferred mirror refresh of layer l (aux stream)
+    bool mirror_pending[SMLP_MAX_LAYERS + 1] = {false};
     cudaEvent_t ev_copied[2] = {nullptr, nullptr};
     cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
     int stage_idx = 0;
@@ -182,6 +184,9 @@ struct smlp_handle {
     int short_max_fwd = 16;         // SMLP_SHORT_MAX_FWD / _BWD: average entries per row below which the
     int short_max_bwd = 8;          //   streaming kernels run (T2/T3 at ~10: forward -5%, backward +80%)
     int short_rows = 1;             // SMLP_SHORT_ROWS: row-streaming forward for 128-column layers of < 8 entries per row
+    int defer_mirror = 0;           // SMLP_DEFER_MIRROR: join each layer's mirror refresh at its next use
+                                    // (C5: neutral, 5.82 vs 5.82 ms -- the overlapped forward slows by
+                                    // what the update region saves; off)
     int overlap_update = 0;         // SMLP_OVERLAP_UPDATE: each layer's Eq. 1 pass + mirror refresh on the
                                     // aux stream as soon as its gradient is final (overlaps the backward;
                                     // C5: 6.040 -> 6.025 ms, the backward kernels slow down by what the
@@ -306,6 +311,8 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
 int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss,
                  const smlp_sgd* fused, const smlp_sgd* overlap_sgd = nullptr, bool split_last = false);
 int run_step(smlp_handle* h, const smlp_sgd* sgd);
+int join_mirror(smlp_handle* h, int l);
+int join_mirrors(smlp_handle* h);   // every API call but forward runs this first (deferred mirror refreshes)
 int refresh_mirror_values(smlp_handle* h, Layer& Ly);
 
 // evolve.cu / prune.cu

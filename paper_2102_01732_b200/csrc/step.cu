@@ -2317,6 +2317,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
     const bool drop = train && h->dropout > 0.f;
     if (h->xbits) {   // binary-input layer 2, all chunks in one pass (returns at once if not binary)
         Layer& L2 = h->layers[0];
+        SMLP_TRY(join_mirror(h, 2));
         BitsArgs A = bits_args(h, L2, nchunks);
         A.dropout_on = drop ? 1 : 0;
         A.step_lo = (uint32_t)step;
@@ -2334,6 +2335,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             const int Bc = std::min(CB, B - c * CB);
             const double nnz = (double)Ly.nnz;
             if (Ly.narrow) continue;   // after the chunk loop, several chunks per pass
+            SMLP_TRY(join_mirror(h, l));
             FwdArgs A{};
             A.a_prev = h->act[l - 1] + (int64_t)c * nin * CB;
             A.a_out = h->act[l] + (int64_t)c * nout * CB;
@@ -2679,7 +2681,15 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
         mirror_values_kernel<<<launch_grid(h, (Ly.cap + 3) / 4, 256), 256, 0, h->aux_stream>>>(Ly.val, Ly.mperm, Ly.meta,
                                                                                      Ly.mval);
         SMLP_CK_LAUNCH(h, "mirror_values_kernel");
-        side = true;
+        if (h->defer_mirror) {
+            // joined lazily: the next forward waits for layer l's copy right before layer l
+            // (join_mirrors for every other consumer), so the refresh overlaps its first layers
+            if (!h->mirror_ev[Ly.l]) SMLP_CK(h, cudaEventCreateWithFlags(&h->mirror_ev[Ly.l], cudaEventDisableTiming));
+            SMLP_CK(h, cudaEventRecord(h->mirror_ev[Ly.l], h->aux_stream));
+            h->mirror_pending[Ly.l] = true;
+        } else {
+            side = true;
+        }
     }
     SMLP_TRY(update(h->bias_base, n, false));                      // biases: no weight decay
     if (side) {
@@ -2687,6 +2697,18 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
         SMLP_CK(h, cudaStreamWaitEvent(h->stream, h->aux_ev[1], 0));
     }
     prof_stop(h);
+    return SMLP_OK;
+}
+
+// the handle's stream waits for layer l's pending mirror refresh (deferred by run_step)
+int join_mirror(smlp_handle* h, int l) {
+    if (!h->mirror_pending[l]) return SMLP_OK;
+    SMLP_CK(h, cudaStreamWaitEvent(h->stream, h->mirror_ev[l], 0));
+    h->mirror_pending[l] = false;
+    return SMLP_OK;
+}
+int join_mirrors(smlp_handle* h) {
+    for (int l = 2; l <= h->L; ++l) SMLP_TRY(join_mirror(h, l));
     return SMLP_OK;
 }
 

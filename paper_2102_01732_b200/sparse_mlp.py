@@ -37,7 +37,7 @@ EXPORTED = [
     "sparse_mlp_export_bias", "sparse_mlp_import_bias", "sparse_mlp_export_alive",
     "sparse_mlp_import_alive", "sparse_mlp_export_trace", "sparse_mlp_last_error", "sparse_mlp_version",
     "sparse_mlp_profile", "sparse_mlp_profile_read", "sparse_mlp_set_step_counter",
-    "sparse_mlp_params_updated", "sparse_mlp_plan_chunks",
+    "sparse_mlp_params_updated", "sparse_mlp_plan_chunks", "sparse_mlp_join",
 ]
 KERNEL_KINDS = {0: "stage_input", 1: "fwd", 2: "fwd_finish", 3: "softmax_ce", 4: "bwd", 5: "bwd_finish",
                 6: "sgd_update", 7: "fwd_bits", 8: "bwd_bits", 9: "layer_update", 10: "mirror_values"}
@@ -112,6 +112,7 @@ def load_library(path: str = LIB_PATH):
     sig = {
         "sparse_mlp_create": (I32, [P(smlp_config), P(VP)]),
         "sparse_mlp_plan_chunks": (I32, [P(I64), I32, I32, I32, I64, P(I32), P(I32)]),
+        "sparse_mlp_join": (I32, [VP]),
         "sparse_mlp_destroy": (I32, [VP]),
         "sparse_mlp_set_stream": (I32, [VP, VP]),
         "sparse_mlp_forward": (I32, [VP, VP, VP, I32, I32, U64, VP]),
@@ -279,6 +280,11 @@ class SparseMLP:
 
     def sparse_mlp_sync(self):
         self._check(self.lib.sparse_mlp_sync(self.h))
+
+    def sparse_mlp_join(self):
+        """Rejoin the library's side-stream work (deferred mirror refreshes) on the handle's stream;
+        call before ending a CUDA-graph capture that contains a training step."""
+        self._check(self.lib.sparse_mlp_join(self.h))
 
     def sparse_mlp_gradient_flow(self) -> float:
         """Squared L2 norm of the pending (unfused) gradient."""
@@ -467,6 +473,7 @@ class SparseMLP:
     retain_valid_updates = sparse_mlp_retain_valid_updates
     view_layout = sparse_mlp_view_layout
     sync = sparse_mlp_sync
+    join = sparse_mlp_join
 
 
 def from_config(cfg, seed: Optional[int] = None, rank: int = 0, max_batch: Optional[int] = None,

@@ -94,6 +94,7 @@ class Trainer:
                     self.m.forward(self.X, x_idx=idx, train=True, step=0)
                     self.m.backward(self.Y, y_idx=idx, loss=self.loss_buf[k:k + 1], fused=lr)
                     self.counter.add_(1)
+                self.m.join()                        # the library's side-stream work rejoins the capture
         torch.cuda.current_stream().wait_stream(s)
         self.graph = g
         self._graph_lr = lr
