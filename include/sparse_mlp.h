@@ -153,7 +153,9 @@ int sparse_mlp_plan_chunks(const int64_t* sizes, int32_t n_layers, int32_t max_b
 /* Frees everything through the allocator on the handle's stream.  NULL is a no-op. */
 int sparse_mlp_destroy(smlp_handle* h);
 
-/* Replace the stream subsequent calls enqueue on (e.g. torch's current stream). */
+/* Replace the stream subsequent calls enqueue on (e.g. torch's current stream).  When the stream
+ * changes, pending side-stream work (deferred mirror refreshes, SMLP_DEFER_MIRROR) is first joined
+ * on the old one.  Errors: SMLP_E_ARG (NULL handle), SMLP_E_CUDA. */
 int sparse_mlp_set_stream(smlp_handle* h, void* stream);
 
 /* sparse_mlp_forward — a_1 = x; for l = 2..L: z_l = a_{l-1} W^(l) + b_l; for hidden l,
