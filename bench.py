@@ -202,7 +202,7 @@ def main():
 
     t0 = time.perf_counter()
     model = SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed,
-                      rank, B, args.chunk_batch, local, input_kind=0 if cfg.binary_input else 1)
+                      rank, B, args.chunk_batch, local, input_kind=2 if cfg.binary_input else 1)
     t_create = time.perf_counter() - t0
     X, Y = load_data(cfg, rank, world, device)
     n_local = X.shape[0]

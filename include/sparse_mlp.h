@@ -60,6 +60,9 @@ extern "C" {
 /* input kinds (smlp_config.input_kind) */
 #define SMLP_INPUT_AUTO 0
 #define SMLP_INPUT_REAL 1
+#define SMLP_INPUT_BINARY 2   /* inputs promised {0,1}: only the bit path is launched; a batch that
+                                 breaks the promise sets the data flag (SMLP_E_DATA at the next
+                                 synchronising call) and its step must be discarded            */
 
 /* prune flags */
 #define SMLP_PRUNE_OUTGOING  1   /* also remove the outgoing row of a pruned neuron (R17)   */
@@ -101,7 +104,8 @@ typedef struct {
     int32_t        input_kind;   /* SMLP_INPUT_AUTO: detect {0,1}-only batches on the device and
                                     take the bit-packed W^(2) path for them (needs max_batch
                                     <= 128); SMLP_INPUT_REAL: inputs are real-valued, no
-                                    detection and no bit path (4 fewer launches per step)   */
+                                    detection and no bit path (4 fewer launches per step);
+                                    SMLP_INPUT_BINARY: see the define                        */
 } smlp_config;
 
 /* Momentum SGD with weight decay, Eq. 1 in velocity form (reading R14):

@@ -130,6 +130,7 @@ int check_data_flag(smlp_handle* h) {
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) return set_err(h, SMLP_E_CUDA, "sync");
     if (flag) {
         cudaMemsetAsync(h->d_err, 0, 4, h->stream);
+        if (flag & 2) return set_err(h, SMLP_E_DATA, "an input value outside {0, 1} with SMLP_INPUT_BINARY");
         return set_err(h, SMLP_E_DATA, "a label outside [0, n_L) was passed to backward");
     }
     return SMLP_OK;
@@ -235,6 +236,10 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
         h->d_nonbinary = zalloc<int32_t>(h, 1, &rc);
         h->gmirror2 = zalloc<float>(h, (size_t)std::max<int64_t>(h->layers[0].cap, 1), &rc);
     }
+    if (cfg->input_kind == SMLP_INPUT_BINARY) {
+        if (!h->xbits) return set_err(h, SMLP_E_ARG, "SMLP_INPUT_BINARY needs max_batch <= 128");
+        h->input_binary = true;
+    }
     h->d_loss = zalloc<float>(h, 1, &rc);
     if (rc) return rc;
     // --- Erdos-Renyi initialisation (R1, R2)
@@ -317,7 +322,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
     if (cfg->activation != SMLP_ACT_RELU && cfg->activation != SMLP_ACT_ALL_RELU)
         return set_err(nullptr, SMLP_E_ARG, "unknown activation");
     if (cfg->init < SMLP_INIT_NORMAL || cfg->init > SMLP_INIT_HE_U) return set_err(nullptr, SMLP_E_ARG, "unknown init");
-    if (cfg->input_kind != SMLP_INPUT_AUTO && cfg->input_kind != SMLP_INPUT_REAL)
+    if (cfg->input_kind != SMLP_INPUT_AUTO && cfg->input_kind != SMLP_INPUT_REAL && cfg->input_kind != SMLP_INPUT_BINARY)
         return set_err(nullptr, SMLP_E_ARG, "unknown input_kind");
     if (cfg->chunk_batch != 0 && (cfg->chunk_batch < 4 || cfg->chunk_batch > 128 || (cfg->chunk_batch & (cfg->chunk_batch - 1))))
         return set_err(nullptr, SMLP_E_ARG, "chunk_batch must be a power of two in [4, 128]");

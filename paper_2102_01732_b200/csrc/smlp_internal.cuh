@@ -184,6 +184,7 @@ struct smlp_handle {
     int short_max_fwd = 16;         // SMLP_SHORT_MAX_FWD / _BWD: average entries per row below which the
     int short_max_bwd = 8;          //   streaming kernels run (T2/T3 at ~10: forward -5%, backward +80%)
     int short_rows = 1;             // SMLP_SHORT_ROWS: row-streaming forward for 128-column layers of < 8 entries per row
+    bool input_binary = false;      // SMLP_INPUT_BINARY: layer 2 only through the bit path
     int defer_mirror = 0;           // SMLP_DEFER_MIRROR: join each layer's mirror refresh at its next use
                                     // (C5: neutral, 5.82 vs 5.82 ms -- the overlapped forward slows by
                                     // what the update region saves; off)

@@ -1526,6 +1526,7 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_rows_kernel(Narr
 struct BitsArgs {
     const uint32_t* xbits;    // [n_1][XBITS_WORDS]
     const int32_t* nonbinary; // device flag
+    int32_t* err;             // SMLP_INPUT_BINARY: set bit 2 when the batch is not binary (else null)
     const int32_t* mrow_ptr;
     const int32_t* msrc;
     const int32_t* mperm;
@@ -1560,7 +1561,10 @@ template <int CB, bool DROP>
 __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
     constexpr int G = CB / 4;                       // lanes per chunk
     __shared__ float2 rec[WARPS_PER_BLOCK][32][XBITS_WORDS];
-    if (*A.nonbinary) return;
+    if (*A.nonbinary) {
+        if (A.err && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.err, 2);   // promise broken
+        return;
+    }
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane / G, q = lane % G;            // chunk g, chunk-local lane q
     const bool colok = g < A.nchunks;
@@ -2206,6 +2210,7 @@ BitsArgs bits_args(smlp_handle* h, Layer& L2, int nchunks) {
     BitsArgs A{};
     A.xbits = h->xbits;
     A.nonbinary = h->d_nonbinary;
+    A.err = h->input_binary ? h->d_err : nullptr;
     A.mrow_ptr = L2.mrow_ptr;
     A.msrc = L2.msrc;
     A.mperm = L2.mperm;
@@ -2335,6 +2340,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             const int Bc = std::min(CB, B - c * CB);
             const double nnz = (double)Ly.nnz;
             if (Ly.narrow) continue;   // after the chunk loop, several chunks per pass
+            if (l == 2 && h->input_binary) continue;   // the bit path only
             SMLP_TRY(join_mirror(h, l));
             FwdArgs A{};
             A.a_prev = h->act[l - 1] + (int64_t)c * nin * CB;
@@ -2503,6 +2509,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
     for (int c = nchunks - 1; c >= 0; --c) {
         const bool first = c == nchunks - 1, last = c == 0;
         for (int l = L; l >= 2; --l) {
+            if (l == 2 && h->input_binary) continue;               // the bit path only (below)
             Layer& Ly = h->layers[l - 2];
             const int64_t nin = h->sizes[l - 2], nout = h->sizes[l - 1];
             const bool has_dprev = l >= 3;

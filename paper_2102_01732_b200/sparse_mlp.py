@@ -479,8 +479,9 @@ class SparseMLP:
 def from_config(cfg, seed: Optional[int] = None, rank: int = 0, max_batch: Optional[int] = None,
                 chunk_batch: int = 0, device: Optional[int] = None) -> SparseMLP:
     """Build a SparseMLP from a synth.WorkloadConfig-like object (sizes, epsilon, ...)."""
-    # configs whose inputs are known real-valued skip the {0,1} detection and the bit path
-    kind = 0 if getattr(cfg, "binary_input", True) else 1
+    # known {0,1} inputs: the bit path only; known real-valued: no detection, no bit path; else auto
+    b = getattr(cfg, "binary_input", None)
+    kind = 0 if b is None else (2 if b else 1)
     return SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init,
                      cfg.model_seed if seed is None else seed, rank, max_batch or cfg.batch, chunk_batch, device,
                      input_kind=kind)

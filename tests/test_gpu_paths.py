@@ -120,6 +120,49 @@ def test_real_input_kind_skips_the_bit_path():
     assert_values_close(g, st, TOL * 2, "real input kind")
 
 
+def test_binary_input_kind_bit_path_only():
+    """input_kind = SMLP_INPUT_BINARY: layer 2 runs only through the bit kernels (no fp32 launches
+    for it), same parity; a batch that breaks the promise raises SMLP_E_DATA at the next sync."""
+    from paper_2102_01732_b200 import SGD, SparseMLP, SparseMLPError
+    torch = _torch()
+    cfg = _binary_cfg(batch=64, dropout=0.3)
+    st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed)
+    g = SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed, 0, 64,
+                  32, input_kind=2)
+    X, Y = _binary_data(128, cfg.sizes[0], seed=21)
+    sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay)
+    l0 = g.info()["launches"]
+    for s_ in range(2):
+        x, y = X[s_ * 64:(s_ + 1) * 64], Y[s_ * 64:(s_ + 1) * 64]
+        tr = M.forward(st, x, True, s_)
+        assert sum(tr.ambiguous) == 0
+        g.forward(to_dev(x), train=True, step=s_)
+        assert g.sparse_mlp_export_trace(4, 0)[0] == 1.0
+        for l in range(2, cfg.n_layers):
+            assert rel_err(g.sparse_mlp_export_trace(0, l, 64), tr.a[l - 1]) <= TOL, ("a", l)
+        g.backward(to_dev(y), fused=sgd)
+        M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, s_)
+    g.sync()
+    assert_values_close(g, st, TOL * 2, "binary input kind")
+    # fewer launches than the auto path (no fp32 layer-2 kernels)
+    ga = SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed, 0, 64, 32)
+    a0 = ga.info()["launches"]
+    ga.forward(to_dev(X[:64]), train=True, step=0)
+    ga.backward(to_dev(Y[:64]), fused=sgd)
+    g2_0 = g.info()["launches"]
+    g.forward(to_dev(X[:64]), train=True, step=2)
+    g.backward(to_dev(Y[:64]), fused=sgd)
+    assert g.info()["launches"] - g2_0 < ga.info()["launches"] - a0
+    # the promise broken: flagged at the next synchronising call
+    xb = X[:64].copy()
+    xb[3, 7] = 0.5
+    g.forward(to_dev(xb), train=True, step=3)
+    g.backward(to_dev(Y[:64]), fused=sgd)
+    with pytest.raises(SparseMLPError):
+        g.sync()
+    torch.cuda.synchronize()
+
+
 def test_binary_and_fp32_paths_agree_on_forward():
     """The bit path and the fp32 gather path compute the same a_2 up to the summation order
     (each is a fixed order, R27): every batch row but the changed one agrees to fp32 rounding."""
