@@ -60,9 +60,11 @@ extern "C" {
 /* input kinds (smlp_config.input_kind) */
 #define SMLP_INPUT_AUTO 0
 #define SMLP_INPUT_REAL 1
-#define SMLP_INPUT_BINARY 2   /* inputs promised {0,1}: only the bit path is launched; a batch that
-                                 breaks the promise sets the data flag (SMLP_E_DATA at the next
-                                 synchronising call) and its step must be discarded            */
+#define SMLP_INPUT_BINARY 2   /* inputs promised {0,1} (needs max_batch <= 128): as AUTO, and a
+                                 batch that breaks the promise is reported -- SMLP_E_DATA at the
+                                 next synchronising call.  That batch's step is still computed
+                                 correctly, through the fp32 layer-2 kernels (they run whenever
+                                 the staged batch is not binary), so nothing is corrupted      */
 
 /* prune flags */
 #define SMLP_PRUNE_OUTGOING  1   /* also remove the outgoing row of a pruned neuron (R17)   */
@@ -280,6 +282,14 @@ int sparse_mlp_view_layout(smlp_handle* h, int64_t* val_off, int64_t* cap, int64
 /* Call after writing the param view directly (e.g. the Eq. 2 averaging allreduce): refreshes
  * the forward's mirror-ordered copy of the weights.  Asynchronous, graph-capturable. */
 int sparse_mlp_params_updated(smlp_handle* h);
+
+/* sparse_mlp_params_averaged — the division of Eq. 2 (theta = (1/K) sum_k
+ * theta_k): after the caller SUM-allreduced the param view over K identical-support replicas
+ * (all of it, or only its bias block [bias_base, count) when biases_only != 0), every value is
+ * divided by K in fp32 (one rounding of the summed value) and, for the full view, the forward's
+ * mirror-ordered weight copy is refreshed.  Momentum stays local (R-O10).  Asynchronous on the
+ * handle's stream, graph-capturable.  Errors: SMLP_E_ARG if K < 1.                            */
+int sparse_mlp_params_averaged(smlp_handle* h, int32_t K, int32_t biases_only);
 
 /* sparse_mlp_evolve_topology — Alg. 2 PAPER.md:659-664 on every weight layer that is not
  * dense-capped: per sign class k = floor(zeta n_+/-), remove the k positives and the k

@@ -26,11 +26,17 @@ def scaled_lr(base_lr: float, K: int, step_idx: int, warmup_steps: int) -> float
 
 
 def allreduce_sum(grads: Sequence[Grads]) -> Grads:
-    """SUM over ranks of every gradient value (float64 sum, one rounding to float32)."""
-    K = len(grads)
+    """SUM over ranks of every gradient value (float64 sum, one rounding to float32).  Running
+    error magnitude (R24): sum_k (|g_k| + gmag_k) -- an fp32 reduction in any order."""
     g = [np.sum([gr.g[i].astype(F64) for gr in grads], axis=0).astype(F32) for i in range(len(grads[0].g))]
     gb = [np.sum([gr.gb[i].astype(F64) for gr in grads], axis=0).astype(F32) for i in range(len(grads[0].gb))]
-    return Grads(g, gb, float(np.mean([gr.loss for gr in grads])), [None] * len(grads[0].deltas))
+
+    def mag(vals, mags, i):
+        return np.sum([np.abs(v[i]).astype(F64) + (0.0 if m is None else m[i]) for v, m in zip(vals, mags)], axis=0)
+
+    gmag = [mag([gr.g for gr in grads], [gr.gmag for gr in grads], i) for i in range(len(g))]
+    gbmag = [mag([gr.gb for gr in grads], [gr.gbmag for gr in grads], i) for i in range(len(gb))]
+    return Grads(g, gb, float(np.mean([gr.loss for gr in grads])), [None] * len(grads[0].deltas), gmag, gbmag)
 
 
 def dp_step(st: State, batches: Sequence[Tuple[np.ndarray, np.ndarray]], lr: float,
@@ -59,9 +65,18 @@ def average(states: List[State]) -> None:
     for idx in range(len(states[0].layers)):
         w = (np.sum([s.layers[idx].w.astype(F64) for s in states], axis=0) / K).astype(F32)
         b = (np.sum([s.b[idx].astype(F64) for s in states], axis=0) / K).astype(F32)
+        # running error magnitudes (R24): the mean of (|value| + its magnitude)
+        wm = np.sum([np.abs(s.layers[idx].w).astype(F64) + (0.0 if s.layers[idx].wmag is None else s.layers[idx].wmag)
+                     for s in states], axis=0) / K
+        bm = np.sum([np.abs(s.b[idx]).astype(F64) + (0.0 if s.bmag is None else s.bmag[idx]) for s in states], axis=0) / K
         for s in states:
             s.layers[idx].w = w.copy()
+            s.layers[idx].wmag = wm.copy()
             s.b[idx] = b.copy()
+            if s.bmag is None:
+                s.bmag = [np.zeros(len(x), F64) for x in s.b]
+                s.vbmag = [np.zeros(len(x), F64) for x in s.b]
+            s.bmag[idx] = bm.copy()
 
 
 def average_union(states: List[State], targets: Sequence[int]) -> List[int]:

@@ -16,12 +16,20 @@ from dataclasses import dataclass, field
 from typing import List, Optional
 
 import numpy as np
-import scipy.sparse as sp
 
 from . import philox
 
 F32 = np.float32
 F64 = np.float64
+
+
+def _cp(x):
+    return None if x is None else x.copy()
+
+
+def _m(x, like):
+    """An error magnitude, or zeros when it is exactly known (None)."""
+    return np.zeros(np.shape(like), F64) if x is None else x
 
 
 # --------------------------------------------------------------------------------------
@@ -38,6 +46,11 @@ class Layer:
     w: np.ndarray            # float32 [nnz]
     v: np.ndarray            # float32 [nnz] momentum (Eq. 1 history)
     dense_capped: bool = False
+    # running fp32 error magnitudes of w and v (R24; None = exactly known, e.g. after
+    # init or an import into the GPU model): an fp32 implementation that took the same steps may
+    # differ by up to KAPPA_U * mag (compare.py)
+    wmag: Optional[np.ndarray] = None
+    vmag: Optional[np.ndarray] = None
 
     @property
     def nnz(self) -> int:
@@ -57,7 +70,11 @@ class Layer:
 
     def copy(self) -> "Layer":
         return Layer(self.l, self.n_in, self.n_out, self.row_ptr.copy(), self.col.copy(),
-                     self.w.copy(), self.v.copy(), self.dense_capped)
+                     self.w.copy(), self.v.copy(), self.dense_capped, _cp(self.wmag), _cp(self.vmag))
+
+    def reset_error(self) -> None:
+        self.wmag = None
+        self.vmag = None
 
 
 @dataclass
@@ -75,6 +92,8 @@ class State:
     vb: List[np.ndarray]     # bias momentum
     alive: List[np.ndarray]  # alive[l-1] = uint8 liveness of neuron layer l (l = 1..L)
     version: int = 0
+    bmag: Optional[List[np.ndarray]] = None    # running error magnitudes of b and vb (R24)
+    vbmag: Optional[List[np.ndarray]] = None
 
     @property
     def L(self) -> int:
@@ -87,7 +106,17 @@ class State:
         return State(list(self.sizes), self.epsilon, self.activation, self.alpha, self.dropout,
                      self.init, self.seed, self.rank, [x.copy() for x in self.layers],
                      [x.copy() for x in self.b], [x.copy() for x in self.vb],
-                     [x.copy() for x in self.alive], self.version)
+                     [x.copy() for x in self.alive], self.version,
+                     None if self.bmag is None else [x.copy() for x in self.bmag],
+                     None if self.vbmag is None else [x.copy() for x in self.vbmag])
+
+    def reset_error(self) -> None:
+        """The state is now known exactly on both sides (e.g. it was just imported into the GPU
+        model): the running error bound restarts from zero."""
+        for Ly in self.layers:
+            Ly.reset_error()
+        self.bmag = None
+        self.vbmag = None
 
 
 # --------------------------------------------------------------------------------------
@@ -181,42 +210,88 @@ def create(sizes, epsilon, activation="all_relu", alpha=0.5, dropout=0.0, init="
 
 
 # --------------------------------------------------------------------------------------
-# sparse products (fp64 accumulation, chunked so large layers fit in memory)
+# sparse products, plain NumPy in float64 (W zero-filled off the support, so a
+# product over W is a sum over the connections (i, j) in S_l only).  Chunked over connections so
+# the C5 layers fit in memory; np.add.reduceat (a library segmented sum) adds each output's
+# contiguous run of connection products.  No SciPy.
 # --------------------------------------------------------------------------------------
 _CHUNK_ELEMS = 1 << 24
 
 
-def _csr64(Ly: Layer, wabs: bool = False):
-    """W^(l) as a SciPy float64 CSR matrix [n_in x n_out] (library sparse container)."""
-    w = np.abs(Ly.w) if wabs else Ly.w
-    return sp.csr_matrix((w.astype(F64), Ly.col.astype(np.int64), Ly.row_ptr.astype(np.int64)),
-                         shape=(Ly.n_in, Ly.n_out))
+def _segment_sums(rows_of_terms: np.ndarray, seg_key: np.ndarray, out: np.ndarray) -> None:
+    """out[k, :] = sum of rows_of_terms[e, :] over the entries e with seg_key[e] == k, where
+    seg_key is non-decreasing (entries grouped by output).  Outputs with no entry are untouched."""
+    if len(seg_key) == 0:
+        return
+    starts = np.flatnonzero(np.r_[True, seg_key[1:] != seg_key[:-1]])
+    out[seg_key[starts]] += np.add.reduceat(rows_of_terms, starts, axis=0)
 
 
-def spmm_fwd(a: np.ndarray, Ly: Layer, wabs: bool = False) -> np.ndarray:
-    """z = a . W^(l)  ([B x n_in] x [n_in x n_out]) in float64, summing over the support only
-    (W zero-filled off the support: PAPER.md:51).  Library sparse matmul as the step."""
-    src = np.abs(a) if wabs else a
-    W = _csr64(Ly, wabs)
-    return np.asarray((W.T @ src.astype(F64).T).T)
+def _chunks(n: int, B: int):
+    step = max(1, _CHUNK_ELEMS // max(B, 1))
+    for s0 in range(0, n, step):
+        yield s0, min(n, s0 + step)
 
 
-def spmm_bwd(delta: np.ndarray, Ly: Layer) -> np.ndarray:
-    """delta . W^(l)^T  ([B x n_out] x [n_out x n_in]) in float64 over the support only."""
-    W = _csr64(Ly)
-    return np.asarray((W @ delta.astype(F64).T).T)
+def column_order(Ly: Layer) -> np.ndarray:
+    """Permutation of the canonical entries sorting them by output neuron j (stable: i ascending
+    within a column)."""
+    return np.argsort(Ly.col, kind="stable")
+
+
+def spmm_fwd(a: np.ndarray, Ly: Layer, wabs: bool = False, w: Optional[np.ndarray] = None) -> np.ndarray:
+    """z = a . W^(l)  ([B x n_in] x [n_in x n_out]) in float64:
+    z[b, j] = sum over the connections (i, j) of W^(l) of a[b, i] w_ij.
+    wabs: |a| . |W|;  w: other values on the support of W^(l) (e.g. error magnitudes)."""
+    aT = np.ascontiguousarray((np.abs(a) if wabs else a).astype(F64).T)      # [n_in x B]
+    if w is None:
+        w = (np.abs(Ly.w) if wabs else Ly.w).astype(F64)
+    order = column_order(Ly)
+    rows, cols = Ly.rows()[order], Ly.col[order].astype(np.int64)
+    zT = np.zeros((Ly.n_out, aT.shape[1]), dtype=F64)
+    for s0, s1 in _chunks(Ly.nnz, aT.shape[1]):
+        _segment_sums(aT[rows[s0:s1]] * w[order[s0:s1], None], cols[s0:s1], zT)
+    return zT.T
+
+
+def spmm_fwd_abs_pair(a1: np.ndarray, w1: np.ndarray, a2: np.ndarray, w2: np.ndarray, Ly: Layer):
+    """(a1 . W1, a2 . W2) on the support of W^(l) for non-negative magnitude operands, in float32
+    (magnitudes are error bounds, R24: relative accuracy ~1e-6 is ample), one pass over
+    the connections for both."""
+    B = a1.shape[0]
+    aT = np.ascontiguousarray(np.concatenate([a1, a2], axis=0).astype(F32).T)     # [n_in x 2B]
+    order = column_order(Ly)
+    rows, cols = Ly.rows()[order], Ly.col[order].astype(np.int64)
+    wa, wb = w1.astype(F32)[order], w2.astype(F32)[order]
+    zT = np.zeros((Ly.n_out, 2 * B), dtype=F32)
+    for s0, s1 in _chunks(Ly.nnz, 2 * B):
+        t = aT[rows[s0:s1]]
+        t[:, :B] *= wa[s0:s1, None]
+        t[:, B:] *= wb[s0:s1, None]
+        _segment_sums(t, cols[s0:s1], zT)
+    return zT[:, :B].T.astype(F64), zT[:, B:].T.astype(F64)
+
+
+def spmm_bwd(delta: np.ndarray, Ly: Layer, w: Optional[np.ndarray] = None) -> np.ndarray:
+    """delta . W^(l)^T  ([B x n_out] x [n_out x n_in]) in float64:
+    out[b, i] = sum over the connections (i, j) of W^(l) of delta[b, j] w_ij (w overrides the values)."""
+    dT = np.ascontiguousarray(delta.astype(F64).T)                          # [n_out x B]
+    w = Ly.w.astype(F64) if w is None else w
+    rows, col = Ly.rows(), Ly.col.astype(np.int64)
+    oT = np.zeros((Ly.n_in, dT.shape[1]), dtype=F64)
+    for s0, s1 in _chunks(Ly.nnz, dT.shape[1]):
+        _segment_sums(dT[col[s0:s1]] * w[s0:s1, None], rows[s0:s1], oT)
+    return oT.T
 
 
 def sddmm(a: np.ndarray, delta: np.ndarray, Ly: Layer) -> np.ndarray:
     """g_ij = sum_b a[b, i] delta[b, j] for (i, j) in the support only (fp64)."""
-    rows = Ly.rows()
-    col = Ly.col.astype(np.int64)
+    aT = np.ascontiguousarray(a.astype(F64).T)
+    dT = np.ascontiguousarray(delta.astype(F64).T)
+    rows, col = Ly.rows(), Ly.col.astype(np.int64)
     g = np.zeros(Ly.nnz, dtype=F64)
-    B = a.shape[0]
-    step = max(1, _CHUNK_ELEMS // max(B, 1))
-    for s0 in range(0, Ly.nnz, step):
-        s1 = min(Ly.nnz, s0 + step)
-        g[s0:s1] = (a[:, rows[s0:s1]].astype(F64) * delta[:, col[s0:s1]].astype(F64)).sum(axis=0)
+    for s0, s1 in _chunks(Ly.nnz, aT.shape[1]):
+        g[s0:s1] = (aT[rows[s0:s1]] * dT[col[s0:s1]]).sum(axis=1)
     return g
 
 
@@ -279,45 +354,74 @@ class Trace:
     p: np.ndarray                      # float32 softmax probabilities [B x n_L]
     p64: np.ndarray
     ambiguous: List[int]               # per layer: #elements with |z| within fp32 rounding of 0
+    # running fp32 error magnitudes (R24): an fp32 implementation of the same step
+    # may differ from a[l-1] / z[l-1] / p by up to KAPPA_U times these (first-order bound)
+    amag: List[Optional[np.ndarray]] = None
+    zmag: List[Optional[np.ndarray]] = None
+    pmag: Optional[np.ndarray] = None
+
+
+def _wmag(Ly: Layer) -> np.ndarray:
+    """|w| + the running error magnitude of w: the weights' contribution to a product's bound."""
+    return np.abs(Ly.w).astype(F64) + _m(Ly.wmag, Ly.w)
 
 
 def forward(st: State, x: np.ndarray, train: bool = True, step: int = 0, rank: Optional[int] = None) -> Trace:
     """sparse_mlp_forward: z_l = a_{l-1} W^(l) + b_l, a_l = f_l(z_l) (Eq. 3) then inverted dropout
-    in train mode (hidden layers only); p = softmax(z_L) computed stably."""
+    in train mode (hidden layers only); p = softmax(z_L) computed stably.
+
+    Alongside, the running error magnitudes of R24 (Higham, Accuracy and Stability of Numerical
+    Algorithms, 2nd ed., §3.1-3.3: a sum of products computed in fp32 differs from its exact
+    value by at most gamma times the same sum of absolute values; errors of the inputs propagate
+    through the absolute values of the weights):
+        zmag_l = (|a_{l-1}| + amag_{l-1}) . (|W^(l)| + wmag) + |b_l| + bmag_l,   amag_1 = 0 (x exact)
+        amag_l = zmag_l * max(1, |slope_l|) * keep/(1-r)     (f_l is Lipschitz with that constant)
+        pmag   = 2 p max_k zmag_L[:, k]                    (|dp_c| <= p_c (|dz_c| + sum_k p_k |dz_k|))"""
     rank = st.rank if rank is None else rank
     x = np.asarray(x, dtype=F32)
     B = x.shape[0]
     a = [x]
     zs: List[Optional[np.ndarray]] = [None]
     keeps: List[Optional[np.ndarray]] = [None]
+    amags: List[Optional[np.ndarray]] = [np.zeros(x.shape, F64)]
+    zmags: List[Optional[np.ndarray]] = [None]
     amb = [0]
     L = st.L
     scale = 1.0 / (1.0 - st.dropout) if st.dropout > 0 else 1.0
     for l in range(2, L + 1):
         Ly = st.layer(l)
         z = spmm_fwd(a[-1], Ly) + st.b[l - 2].astype(F64)
-        mag = spmm_fwd(a[-1], Ly, wabs=True) + np.abs(st.b[l - 2].astype(F64))
+        aa = np.abs(a[-1]).astype(F64)
+        mag, zmag = spmm_fwd_abs_pair(aa, np.abs(Ly.w), aa + amags[-1], _wmag(Ly), Ly)
+        mag += np.abs(st.b[l - 2].astype(F64))
+        zmag += np.abs(st.b[l - 2].astype(F64)) + (0.0 if st.bmag is None else st.bmag[l - 2])
         # pre-activations within fp32 summation error of the All-ReLU kink (hidden layers):
-        # there the branch taken by an fp32 kernel may legitimately differ (DESIGN.md R30, kink
+        # there the branch taken by an fp32 kernel may legitimately differ (DESIGN.md R32, kink
         # guard).  mag == 0 means every term is an exact zero (e.g. no active binary input and a
         # zero bias): z is exactly 0 on every path, so that element is not ambiguous.
         amb.append(int(np.count_nonzero((np.abs(z) <= mag * (2.0 ** -20)) & (mag > 0))) if l < L else 0)
         zs.append(z)
+        zmags.append(zmag)
         if l < L:
             h = activation(z, l, st.alpha, st.activation)
+            hm = zmag * max(1.0, abs(neg_slope(st, st.alpha, l)))
             keep = None
             if train and st.dropout > 0:
                 keep = dropout_keep(st.seed, rank, l, step, B, Ly.n_out, st.dropout)
                 h = h * keep * scale
+                hm = hm * keep * scale
             keeps.append(keep)
             a.append(h.astype(F32))
+            amags.append(hm)
         else:
             keeps.append(None)
     zL = zs[-1]
     zmax = zL.max(axis=1, keepdims=True)
     ez = np.exp(zL - zmax)
     p64 = ez / ez.sum(axis=1, keepdims=True)
-    return Trace(B, bool(train), int(step), st.version, a, zs, keeps, p64.astype(F32), p64, amb)
+    pmag = 2.0 * p64 * zmags[-1].max(axis=1, keepdims=True)
+    return Trace(B, bool(train), int(step), st.version, a, zs, keeps, p64.astype(F32), p64, amb,
+                 amags, zmags, pmag)
 
 
 def loss_grad(p64: np.ndarray, y: np.ndarray):
@@ -339,12 +443,22 @@ class Grads:
     gb: List[np.ndarray]     # gb[l-2]: float32 [n_l]
     loss: float
     deltas: List[Optional[np.ndarray]]   # deltas[l-1]: float32 [B x n_l] (None for l = 1)
+    # running error magnitudes (R24), aligned with g / gb / deltas; None = exact
+    gmag: Optional[List[np.ndarray]] = None
+    gbmag: Optional[List[np.ndarray]] = None
+    dmag: Optional[List[Optional[np.ndarray]]] = None
 
 
 def backward(st: State, tr: Trace, y: np.ndarray) -> Grads:
     """sparse_mlp_backward: for l = L..2, g_ij = sum_b a_{l-1}[b,i] delta_l[b,j] on the support
     only (SDDMM), gb_l = sum_b delta_l, delta_{l-1} = (delta_l W^(l)T) * f'_{l-1}(z_{l-1}) * keep/(1-r)
-    for l >= 3.  delta_L = (p - onehot)/B."""
+    for l >= 3.  delta_L = (p - onehot)/B.
+
+    Running error magnitudes (R24), as in `forward`, with f' exact away from the kink (R32):
+        dmag_L     = pmag / B
+        gmag_ij    = sum_b (|a_{l-1}| + amag_{l-1})[b, i] (|delta_l| + dmag_l)[b, j]
+        gbmag_j    = sum_b (|delta_l| + dmag_l)[b, j]
+        dmag_{l-1} = ((|delta_l| + dmag_l) . (|W^(l)| + wmag)^T) * |f'_{l-1}| * keep/(1-r)"""
     if tr.version != st.version or not tr.train:
         raise RuntimeError("stale trace")
     L = st.L
@@ -353,35 +467,65 @@ def backward(st: State, tr: Trace, y: np.ndarray) -> Grads:
     scale = 1.0 / (1.0 - st.dropout) if st.dropout > 0 else 1.0
     g: List[Optional[np.ndarray]] = [None] * (L - 1)
     gb: List[Optional[np.ndarray]] = [None] * (L - 1)
+    gmag: List[Optional[np.ndarray]] = [None] * (L - 1)
+    gbmag: List[Optional[np.ndarray]] = [None] * (L - 1)
     deltas: List[Optional[np.ndarray]] = [None] * L
+    dmags: List[Optional[np.ndarray]] = [None] * L
     deltas[L - 1] = delta
+    dmag = (tr.pmag if tr.pmag is not None else np.zeros(dz.shape)) / tr.B
+    dmags[L - 1] = dmag
     for l in range(L, 1, -1):
         Ly = st.layer(l)
         g[l - 2] = sddmm(tr.a[l - 2], delta, Ly).astype(F32)
         gb[l - 2] = delta.astype(F64).sum(axis=0).astype(F32)
+        afull = np.abs(tr.a[l - 2]).astype(F64) + (tr.amag[l - 2] if tr.amag is not None else 0.0)
+        dfull = np.abs(delta).astype(F64) + dmag
+        gmag[l - 2] = sddmm(afull, dfull, Ly)
+        gbmag[l - 2] = dfull.sum(axis=0)
         if l >= 3:
-            d = spmm_bwd(delta, Ly) * activation_grad(tr.z[l - 2], l - 1, st.alpha, st.activation)
+            fp = activation_grad(tr.z[l - 2], l - 1, st.alpha, st.activation)
+            d = spmm_bwd(delta, Ly) * fp
+            dmag = spmm_bwd(dfull, Ly, w=_wmag(Ly)) * np.abs(fp)
             if tr.keep[l - 2] is not None:
                 d = d * tr.keep[l - 2] * scale
+                dmag = dmag * tr.keep[l - 2] * scale
             delta = d.astype(F32)
             deltas[l - 2] = delta
-    return Grads(g, gb, loss, deltas)
+            dmags[l - 2] = dmag
+    return Grads(g, gb, loss, deltas, gmag, gbmag, dmags)
 
 
 def step(st: State, grads: Grads, lr: float, momentum: float, weight_decay: float,
          grad_scale: float = 1.0) -> None:
     """sparse_mlp_step: Eq. 1 in velocity form, weight decay folded into the
     gradient (DESIGN reading 14):  v <- mu v - eta (s g + lambda w);  w <- w + v.
-    Biases: vb <- mu vb - eta s gb; b <- b + vb (no decay)."""
+    Biases: vb <- mu vb - eta s gb; b <- b + vb (no decay).
+
+    Running error magnitudes (R24): vmag' = mu (|v| + vmag) + eta (s (|g| + gmag) + lambda (|w| + wmag)),
+    wmag' = |w| + wmag + |v'| + vmag' (likewise for the biases, without lambda)."""
+    if st.bmag is None:
+        st.bmag = [np.zeros(len(b), F64) for b in st.b]
+        st.vbmag = [np.zeros(len(b), F64) for b in st.b]
     for idx, Ly in enumerate(st.layers):
         g = grads.g[idx].astype(F64) * grad_scale
-        v = momentum * Ly.v.astype(F64) - lr * (g + weight_decay * Ly.w.astype(F64))
+        gm = (np.abs(grads.g[idx]).astype(F64) + _m(None if grads.gmag is None else grads.gmag[idx], g)) * grad_scale
+        w64 = Ly.w.astype(F64)
+        wm = np.abs(w64) + _m(Ly.wmag, w64)
+        v = momentum * Ly.v.astype(F64) - lr * (g + weight_decay * w64)
+        vm = momentum * (np.abs(Ly.v).astype(F64) + _m(Ly.vmag, w64)) + lr * (gm + weight_decay * wm)
         Ly.v = v.astype(F32)
-        Ly.w = (Ly.w.astype(F64) + Ly.v.astype(F64)).astype(F32)
+        Ly.w = (w64 + Ly.v.astype(F64)).astype(F32)
+        Ly.vmag = vm
+        Ly.wmag = wm + np.abs(Ly.v).astype(F64) + vm
         gbv = grads.gb[idx].astype(F64) * grad_scale
+        gbm = (np.abs(gbv) + _m(None if grads.gbmag is None else grads.gbmag[idx] * grad_scale, gbv))
+        bm = np.abs(st.b[idx]).astype(F64) + st.bmag[idx]
         vb = momentum * st.vb[idx].astype(F64) - lr * gbv
+        vbm = momentum * (np.abs(st.vb[idx]).astype(F64) + st.vbmag[idx]) + lr * gbm
         st.vb[idx] = vb.astype(F32)
         st.b[idx] = (st.b[idx].astype(F64) + st.vb[idx].astype(F64)).astype(F32)
+        st.vbmag[idx] = vbm
+        st.bmag[idx] = bm + np.abs(st.vb[idx]).astype(F64) + vbm
 
 
 def train_step(st: State, x, y, lr, momentum, weight_decay, step_idx: int = 0):

@@ -725,12 +725,7 @@ int sparse_mlp_import_layer(smlp_handle* h, int32_t l, int64_t nnz, const int32_
         if (mom) SMLP_CK(h, cudaMemcpyAsync(Ly.mom, mom, sizeof(float) * nz, cudaMemcpyHostToDevice, h->stream));
         else SMLP_CK(h, cudaMemsetAsync(Ly.mom, 0, sizeof(float) * nz, h->stream));
     }
-    const size_t tail = (size_t)(Ly.cap - nnz);
-    if (tail) {
-        SMLP_CK(h, cudaMemsetAsync(Ly.val + nnz, 0, sizeof(float) * tail, h->stream));
-        SMLP_CK(h, cudaMemsetAsync(Ly.mom + nnz, 0, sizeof(float) * tail, h->stream));
-        SMLP_CK(h, cudaMemsetAsync(Ly.grad + nnz, 0, sizeof(float) * tail, h->stream));
-    }
+    SMLP_TRY(zero_tail(h, Ly, nnz));
     Ly.nnz = nnz;
     SMLP_TRY(rebuild_derived(h, Ly));
     h->version++;

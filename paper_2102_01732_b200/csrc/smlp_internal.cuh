@@ -304,6 +304,9 @@ int first_distinct_candidates(smlp_handle* h, const Layer& L, uint32_t purpose, 
                               const uint8_t* alive_out, int64_t n_free, uint64_t* out_pos,
                               float* out_val);
 int fill_dense_layer(smlp_handle* h, Layer& L);
+// zero val / mom / grad (and the fused path's grad2) of W^(l) beyond its first n entries, so the
+// param / grad views hold zeros in [nnz, cap) and the Eq. 1 pass leaves that tail at zero
+int zero_tail(smlp_handle* h, Layer& L, int64_t n);
 int launch_grid(const smlp_handle* h, int64_t items, int threads);
 
 // step.cu

@@ -2340,7 +2340,6 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             const int Bc = std::min(CB, B - c * CB);
             const double nnz = (double)Ly.nnz;
             if (Ly.narrow) continue;   // after the chunk loop, several chunks per pass
-            if (l == 2 && h->input_binary) continue;   // the bit path only
             SMLP_TRY(join_mirror(h, l));
             FwdArgs A{};
             A.a_prev = h->act[l - 1] + (int64_t)c * nin * CB;
@@ -2509,7 +2508,6 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
     for (int c = nchunks - 1; c >= 0; --c) {
         const bool first = c == nchunks - 1, last = c == 0;
         for (int l = L; l >= 2; --l) {
-            if (l == 2 && h->input_binary) continue;               // the bit path only (below)
             Layer& Ly = h->layers[l - 2];
             const int64_t nin = h->sizes[l - 2], nout = h->sizes[l - 1];
             const bool has_dprev = l >= 3;

@@ -358,7 +358,19 @@ int rebuild_derived(smlp_handle* h, Layer& L) {
     return SMLP_OK;
 }
 
+int zero_tail(smlp_handle* h, Layer& L, int64_t n) {
+    if (n >= L.cap) return SMLP_OK;
+    const size_t tail = (size_t)(L.cap - n);
+    SMLP_CK(h, cudaMemsetAsync(L.val + n, 0, sizeof(float) * tail, h->stream));
+    SMLP_CK(h, cudaMemsetAsync(L.mom + n, 0, sizeof(float) * tail, h->stream));
+    SMLP_CK(h, cudaMemsetAsync(L.grad + n, 0, sizeof(float) * tail, h->stream));
+    // the fused path's second gradient buffer is read by the Eq. 1 pass over the whole slice
+    if (h->grad2) SMLP_CK(h, cudaMemsetAsync(h->grad2 + L.val_off + n, 0, sizeof(float) * tail, h->stream));
+    return SMLP_OK;
+}
+
 int csr_from_sorted_positions(smlp_handle* h, Layer& L, const uint64_t* pos, const float* v, int64_t n) {
+    SMLP_TRY(zero_tail(h, L, n));
     if (n > 0) {
         csr_from_pos_kernel<<<launch_grid(h, n, TPB), TPB, 0, h->stream>>>(pos, v, n, L.n_in, L.n_out, L.col, L.val,
                                                                             L.mom);
@@ -499,12 +511,7 @@ int merge_layer(smlp_handle* h, Layer& L, const uint8_t* flags, const uint64_t* 
     SMLP_CK(h, cudaMemcpyAsync(L.mom, nmom, sizeof(float) * (size_t)new_nnz, cudaMemcpyDeviceToDevice, h->stream));
     SMLP_CK(h, cudaMemcpyAsync(L.row_ptr, nrp, sizeof(int32_t) * (size_t)(L.n_in + 1), cudaMemcpyDeviceToDevice,
                                h->stream));
-    if (new_nnz < L.cap) {
-        const size_t tail = (size_t)(L.cap - new_nnz);
-        SMLP_CK(h, cudaMemsetAsync(L.val + new_nnz, 0, sizeof(float) * tail, h->stream));
-        SMLP_CK(h, cudaMemsetAsync(L.mom + new_nnz, 0, sizeof(float) * tail, h->stream));
-        SMLP_CK(h, cudaMemsetAsync(L.grad + new_nnz, 0, sizeof(float) * tail, h->stream));
-    }
+    SMLP_TRY(zero_tail(h, L, new_nnz));
     SMLP_CK(h, cudaStreamSynchronize(h->stream));
     tmp_free(h, ncol, sizeof(int32_t) * nb);
     tmp_free(h, nval, sizeof(float) * nb);

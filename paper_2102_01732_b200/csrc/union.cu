@@ -33,6 +33,12 @@ int bits_u64(uint64_t v) {
     return b;
 }
 
+// Eq. 2 after a SUM allreduce of the param view: theta <- theta_sum / K (fp32, one rounding)
+__global__ void divide_kernel(float* __restrict__ p, int64_t n, float K) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        p[k] = __fdiv_rn(p[k], K);
+}
+
 // canonical positions i * n_out + j of a layer's entries
 __global__ void positions_kernel(const int32_t* __restrict__ rowid, const int32_t* __restrict__ col, int64_t nnz,
                                  int64_t n_out, uint64_t* __restrict__ pos) {
@@ -231,5 +237,21 @@ int sparse_mlp_retain_valid_updates(smlp_handle* h, int32_t l, const uint64_t* s
     tmp_free(h, cnt, sizeof(unsigned long long));
     if (retained) *retained = (int64_t)c;
     h->grads_pending = true;    // the caller applies it with sparse_mlp_step (biases: its grad view slice)
+    return SMLP_OK;
+}
+
+int sparse_mlp_params_averaged(smlp_handle* h, int32_t K, int32_t biases_only) {
+    using namespace smlp;
+    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
+    if (!h) return SMLP_E_ARG;
+    if (K < 1) return set_err(h, SMLP_E_ARG, "K must be >= 1");
+    const int64_t lo = biases_only ? h->bias_base : 0;
+    const int64_t n = h->param_count - lo;
+    if (K > 1 && n > 0) {
+        divide_kernel<<<launch_grid(h, n, TPB), TPB, 0, h->stream>>>(h->param + lo, n, (float)K);
+        SMLP_CK_LAUNCH(h, "divide_kernel");
+    }
+    if (!biases_only)
+        for (auto& Ly : h->layers) SMLP_TRY(refresh_mirror_values(h, Ly));
     return SMLP_OK;
 }

@@ -56,15 +56,20 @@ def allreduce_sum_(t, group=None):
     return t
 
 
-def average_(t, group=None):
-    """Eq. 2 on a flat parameter tensor: SUM allreduce then / K (X2)."""
+def average_model_(model, group=None, biases_only: bool = False):
+    """Eq. 2 over the process group (X2): SUM-allreduce the model's param view
+    (or only its bias block), then the library divides by K and refreshes the mirror copy
+    (sparse_mlp_params_averaged) -- no method arithmetic outside the library."""
     import torch.distributed as dist
-    if dist.is_initialized():
-        K = dist.get_world_size(group)
-        if K > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-            t.div_(K)
-    return t
+    K = dist.get_world_size(group) if dist.is_initialized() else 1
+    if K > 1:
+        p, _ = model.param_view()
+        if biases_only:
+            _, bias_base = model.view_layout()
+            p = p[bias_base:]
+        dist.all_reduce(p, op=dist.ReduceOp.SUM, group=group)
+        model.params_averaged(K, biases_only)
+    return K
 
 
 def tensor_hash(t) -> int:
@@ -185,10 +190,7 @@ def union_average_(model, targets, group=None) -> list:
             pos = torch.cat([P[k][:counts[k]] for k in range(K)])
             val = torch.cat([V[k][:counts[k]] for k in range(K)])
         kept.append(model.union_average_layer(l, K, pos, val, int(targets[l - 2])))
-    p, _ = model.param_view()
-    _, bias_base = model.view_layout()
-    average_(p[bias_base:], group)
-    model.params_updated()
+    average_model_(model, group, biases_only=True)
     return kept
 
 

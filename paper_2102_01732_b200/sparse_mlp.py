@@ -37,7 +37,7 @@ EXPORTED = [
     "sparse_mlp_export_bias", "sparse_mlp_import_bias", "sparse_mlp_export_alive",
     "sparse_mlp_import_alive", "sparse_mlp_export_trace", "sparse_mlp_last_error", "sparse_mlp_version",
     "sparse_mlp_profile", "sparse_mlp_profile_read", "sparse_mlp_set_step_counter",
-    "sparse_mlp_params_updated", "sparse_mlp_plan_chunks", "sparse_mlp_join",
+    "sparse_mlp_params_updated", "sparse_mlp_plan_chunks", "sparse_mlp_join", "sparse_mlp_params_averaged",
 ]
 KERNEL_KINDS = {0: "stage_input", 1: "fwd", 2: "fwd_finish", 3: "softmax_ce", 4: "bwd", 5: "bwd_finish",
                 6: "sgd_update", 7: "fwd_bits", 8: "bwd_bits", 9: "layer_update", 10: "mirror_values"}
@@ -144,6 +144,7 @@ def load_library(path: str = LIB_PATH):
         "sparse_mlp_profile_read": (I32, [VP, P(smlp_kernel_stat), I32, P(I32)]),
         "sparse_mlp_set_step_counter": (I32, [VP, VP]),
         "sparse_mlp_params_updated": (I32, [VP]),
+        "sparse_mlp_params_averaged": (I32, [VP, I32, I32]),
         "sparse_mlp_last_error": (C.c_char_p, [VP]),
         "sparse_mlp_version": (C.c_char_p, []),
     }
@@ -347,6 +348,12 @@ class SparseMLP:
         self._check(self.lib.sparse_mlp_params_updated(self.h))
 
     # -------------------------------------------------------------------------------- topology
+    def sparse_mlp_params_averaged(self, K: int, biases_only: bool = False):
+        """Eq. 2's division by K after the caller's SUM allreduce of the param view (or its bias
+        block) + mirror refresh, in the library."""
+        self._sync_stream()
+        self._check(self.lib.sparse_mlp_params_averaged(self.h, int(K), int(bool(biases_only))))
+
     def sparse_mlp_evolve_topology(self, zeta: float, evolve_idx: int):
         out = (C.c_int64 * self.L)()
         self._sync_stream()
@@ -468,6 +475,7 @@ class SparseMLP:
     wait_layer = sparse_mlp_wait_layer
     gradient_flow = sparse_mlp_gradient_flow
     params_updated = sparse_mlp_params_updated
+    params_averaged = sparse_mlp_params_averaged
     export_positions = sparse_mlp_export_positions
     union_average_layer = sparse_mlp_union_average_layer
     retain_valid_updates = sparse_mlp_retain_valid_updates
@@ -479,9 +487,11 @@ class SparseMLP:
 def from_config(cfg, seed: Optional[int] = None, rank: int = 0, max_batch: Optional[int] = None,
                 chunk_batch: int = 0, device: Optional[int] = None) -> SparseMLP:
     """Build a SparseMLP from a synth.WorkloadConfig-like object (sizes, epsilon, ...)."""
-    # known {0,1} inputs: the bit path only; known real-valued: no detection, no bit path; else auto
+    # known {0,1} inputs: checked and reported (the bit path needs max_batch <= 128, else auto);
+    # known real-valued: no detection, no bit path; else auto
     b = getattr(cfg, "binary_input", None)
-    kind = 0 if b is None else (2 if b else 1)
+    mb = int(max_batch or cfg.batch)
+    kind = 0 if b is None else ((2 if mb <= 128 else 0) if b else 1)
     return SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init,
                      cfg.model_seed if seed is None else seed, rank, max_batch or cfg.batch, chunk_batch, device,
                      input_kind=kind)

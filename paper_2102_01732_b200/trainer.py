@@ -20,7 +20,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from .dp import allreduce_sum_, average_, scaled_lr, shard_bounds, union_average_
+from .dp import allreduce_sum_, average_model_, scaled_lr, shard_bounds, union_average_
 from .sparse_mlp import SGD, SparseMLP
 
 
@@ -139,8 +139,7 @@ class Trainer:
         loss = float(loss_sum.item()) / self.n
         # ---- epoch boundary: Eq. 2 averaging (periodic, optional), pruning, evolution
         if self.average_every_epoch and self.world > 1:
-            p, _ = self.m.param_view()
-            average_(p, self.group)
+            average_model_(self.m, self.group)
         prune_s = evolve_s = 0.0
         pruned, removed = [], []
         if cfg.prune and epoch % cfg.prune_every == 0 and epoch >= cfg.prune_start:

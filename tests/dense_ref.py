@@ -16,12 +16,17 @@ def act(z, l, alpha, kind="all_relu"):
     return np.where(z > 0, z, s * z), np.where(z > 0, 1.0, s)
 
 
-def forward_backward(Ws, bs, x, y, alpha, kind="all_relu", keeps=None, rate=0.0):
+def forward_backward(Ws, bs, x, y, alpha, kind="all_relu", keeps=None, rate=0.0, dtype=np.float64, out=None):
     """Ws[k] dense [n_{l-1} x n_l] (l = k+2), bs[k] [n_l]; keeps[k] optional dropout masks of
-    hidden layer l = k+2.  Returns (loss, probs, dW list, db list)."""
+    hidden layer l = k+2.  Returns (loss, probs, dW list, db list).  dtype = np.float32 runs the
+    whole computation in fp32 (BLAS sgemm order): another fp32 implementation of the step, for
+    the error-bound pin of tests/test_oracle_model.py.  out (dict): receives the activations
+    "a" and the deltas "delta" (index k = layer l - 1)."""
     L = len(Ws) + 1
     B = x.shape[0]
-    a = [np.asarray(x, np.float64)]
+    Ws = [np.asarray(W, dtype) for W in Ws]
+    bs = [np.asarray(b, dtype) for b in bs]
+    a = [np.asarray(x, dtype)]
     d = []
     scale = 1.0 / (1.0 - rate) if rate > 0 else 1.0
     for k, (W, b) in enumerate(zip(Ws, bs)):
@@ -42,13 +47,18 @@ def forward_backward(Ws, bs, x, y, alpha, kind="all_relu", keeps=None, rate=0.0)
     loss = -np.log(p[np.arange(B), y]).mean()
     delta = p.copy()
     delta[np.arange(B), y] -= 1.0
-    delta /= B
+    delta /= dtype(B)
     dWs, dbs = [None] * len(Ws), [None] * len(Ws)
+    deltas = [None] * L
     for k in range(len(Ws) - 1, -1, -1):
+        deltas[k + 1] = delta
         dWs[k] = a[k].T @ delta
         dbs[k] = delta.sum(0)
         if k > 0:
-            delta = (delta @ Ws[k].T) * d[k - 1]
+            delta = (delta @ Ws[k].T) * d[k - 1].astype(dtype)
+    if out is not None:
+        out["a"] = a
+        out["delta"] = deltas
     return loss, p, dWs, dbs
 
 

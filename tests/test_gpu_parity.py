@@ -21,9 +21,9 @@ def _torch():
     return torch
 
 
-def _batch(cfg, st, B=None, step=0, tries=6):
+def _batch(cfg, st, B=None, step=0, tries=12):
     """A seeded batch whose hidden pre-activations are not within fp32 rounding of the All-ReLU
-    kink; the oracle reports the count, the batch is skipped if > 0."""
+    kink (R32): the first of `tries` candidate batches the oracle reports kink-free."""
     B = B or cfg.batch
     X, y = make_dataset(cfg, n=B * tries)
     for t in range(tries):
@@ -31,7 +31,7 @@ def _batch(cfg, st, B=None, step=0, tries=6):
         tr = M.forward(st, x, True, step)
         if sum(tr.ambiguous) == 0:
             return x, yy, tr
-    pytest.skip("no kink-free batch found")
+    raise AssertionError("no kink-free batch among the candidates")
 
 
 def _tiny(**kw):
@@ -72,13 +72,13 @@ def test_forward_parity(name):
     torch.cuda.synchronize()
     for l in range(1, cfg.n_layers):
         a = g.sparse_mlp_export_trace(0, l, B)
-        assert rel_err(a, tr.a[l - 1]) <= TOL, (name, l, rel_err(a, tr.a[l - 1]))
+        assert rel_err(a, tr.a[l - 1], tr.amag[l - 1]) <= TOL, (name, l, rel_err(a, tr.a[l - 1], tr.amag[l - 1]))
         if l >= 2 and cfg.dropout > 0:
             # dropout masks are integer decisions: exactly the same zeros
             assert np.array_equal(a == 0, tr.a[l - 1] == 0)
     zL = g.sparse_mlp_export_trace(0, cfg.n_layers, B)
-    assert rel_err(zL, tr.z[-1]) <= TOL
-    assert rel_err(probs.cpu().numpy(), tr.p) <= TOL
+    assert rel_err(zL, tr.z[-1], tr.zmag[-1]) <= TOL
+    assert rel_err(probs.cpu().numpy(), tr.p, tr.pmag) <= TOL
 
 
 def test_eval_forward_has_no_dropout():
@@ -89,7 +89,7 @@ def test_eval_forward_has_no_dropout():
     probs = torch.empty((len(x), 10), device="cuda")
     g.forward(to_dev(x), train=False, step=0, probs=probs)
     tr = M.forward(st, x, False, 0)
-    assert rel_err(probs.cpu().numpy(), tr.p) <= TOL
+    assert rel_err(probs.cpu().numpy(), tr.p, tr.pmag) <= TOL
 
 
 # ----------------------------------------------------------------------------------------- backward
@@ -109,13 +109,15 @@ def test_backward_parity_unfused(name):
     for Ly in st.layers:
         l = Ly.l
         gg = g.sparse_mlp_export_trace(2, l)
-        assert rel_err(gg, gr.g[l - 2]) <= TOL, (name, l, "g", rel_err(gg, gr.g[l - 2]))
+        e = rel_err(gg, gr.g[l - 2], gr.gmag[l - 2])
+        assert e <= TOL, (name, l, "g", e)
         gb = g.sparse_mlp_export_trace(3, l)
-        assert rel_err(gb, gr.gb[l - 2]) <= TOL, (name, l, "gb", rel_err(gb, gr.gb[l - 2]))
-        if l >= 2:
+        e = rel_err(gb, gr.gb[l - 2], gr.gbmag[l - 2])
+        assert e <= TOL, (name, l, "gb", e)
+        if l >= 3 or l == cfg.n_layers:
             d = g.sparse_mlp_export_trace(1, l, B)
-            if l >= 3 or l == cfg.n_layers:
-                assert rel_err(d, gr.deltas[l - 1]) <= TOL, (name, l, "delta")
+            e = rel_err(d, gr.deltas[l - 1], gr.dmag[l - 1])
+            assert e <= TOL, (name, l, "delta", e)
 
 
 @pytest.mark.parametrize("name", SMALL)
@@ -131,8 +133,8 @@ def test_fused_steps_parity(name):
         g.forward(to_dev(x), train=True, step=s)
         g.backward(to_dev(y), fused=sgd)
         M.train_step(st, x, y, cfg.lr, cfg.momentum, cfg.weight_decay, s)
-    torch.cuda.synchronize()
-    assert_values_close(g, st, TOL * 3, name)
+        torch.cuda.synchronize()
+        assert_values_close(g, st, TOL, f"{name} step {s}")          # 1e-4 after every step
 
 
 def test_unfused_step_equals_fused():
@@ -173,8 +175,8 @@ def test_chunked_layout_parity(B, fchunk, monkeypatch):
     torch.cuda.synchronize()
     gr = M.backward(st, tr, y)
     for Ly in st.layers:
-        assert rel_err(g.sparse_mlp_export_trace(2, Ly.l), gr.g[Ly.l - 2]) <= TOL
-        assert rel_err(g.sparse_mlp_export_trace(3, Ly.l), gr.gb[Ly.l - 2]) <= TOL
+        assert rel_err(g.sparse_mlp_export_trace(2, Ly.l), gr.g[Ly.l - 2], gr.gmag[Ly.l - 2]) <= TOL
+        assert rel_err(g.sparse_mlp_export_trace(3, Ly.l), gr.gb[Ly.l - 2], gr.gbmag[Ly.l - 2]) <= TOL
     sgd = SGD(cfg.lr, cfg.momentum, cfg.weight_decay)
     g.step(sgd)
     M.step(st, gr, cfg.lr, cfg.momentum, cfg.weight_decay)
@@ -191,7 +193,7 @@ def test_index_gather_and_errors():
     idx = np.array([5, 3, 60, 7, 7, 11, 0, 2, 9, 13, 40, 41, 1], np.int32)
     g.forward(to_dev(X), x_idx=to_dev(idx), train=True, step=0)
     tr = M.forward(st, X[idx], True, 0)
-    assert rel_err(g.sparse_mlp_export_trace(0, 2, len(idx)), tr.a[1]) <= TOL
+    assert rel_err(g.sparse_mlp_export_trace(0, 2, len(idx)), tr.a[1], tr.amag[1]) <= TOL
     g.backward(to_dev(Y), y_idx=to_dev(idx))
     with pytest.raises(SparseMLPError, match="E_STALE"):
         g.backward(to_dev(Y), y_idx=to_dev(idx))                  # trace consumed
@@ -283,29 +285,61 @@ def test_prune_rho_zero_removes_nothing():
 
 
 # ----------------------------------------------------------------------------------------- after prune: training still matches
-def test_training_after_prune_and_evolve_parity():
+def _kink_free(st, X, Y, B, step):
+    """The first batch of X (in B-row slices) with no kink-ambiguous pre-activation (R32), decided
+    by the oracle alone."""
+    for t in range(len(X) // B):
+        x, y = X[t * B:(t + 1) * B], Y[t * B:(t + 1) * B]
+        tr = M.forward(st, x, True, step)
+        if sum(tr.ambiguous) == 0:
+            return x, y, tr
+    raise AssertionError("no kink-free batch among the candidates")
+
+
+@pytest.mark.parametrize("name", ["C2", "big"])
+def test_training_after_prune_and_evolve_parity(name):
+    """Alg. 2's epoch order: train, Importance Pruning, SET evolution, train on.
+    Op by op on identical state: a fused GPU step (which, on the > 4M-parameter model with B > CB,
+    fills the split last-chunk gradient buffer), then prune and evolve on both sides (bit-exact,
+    the layers shrink), then another fused step compared within R24 -- and the param view holds
+    zeros in every layer's pruned tail (the second gradient buffer's stale tail must
+    not leak into the Eq. 1 pass)."""
     torch = _torch()
     from paper_2102_01732_b200 import SGD
-    cfg = get_config("C2")
-    g, st = pair(cfg)
-    X, Y = make_dataset(cfg, n=cfg.batch * 2)
-    M.train_step(st, X[:128], Y[:128], 0.1, 0.9, 2e-4, 0)
-    T.prune(st, 20.0)
-    T.evolve(st, 0.3, 0)
-    load_oracle_state_into_gpu(g, st)
-    x, y = X[128:], Y[128:]
-    tr = M.forward(st, x, True, 1)
-    if sum(tr.ambiguous):
-        pytest.skip("kink-ambiguous batch")
-    g.forward(to_dev(x), train=True, step=1)
-    g.backward(to_dev(y), fused=SGD(cfg.lr, cfg.momentum, cfg.weight_decay))
-    M.step(st, M.backward(st, tr, y), cfg.lr, cfg.momentum, cfg.weight_decay)
+    if name == "big":
+        cfg = get_config("C2", sizes=(784, 12000, 12000, 10), epsilon=120.0, dropout=0.2, batch=128)
+        g, st = pair(cfg, chunk_batch=32)
+        assert sum(L.nnz for L in st.layers) > (1 << 22) and g.info()["chunk_batch"] < cfg.batch
+    else:
+        cfg = get_config("C2")
+        g, st = pair(cfg)
+    sgd = SGD(cfg.lr * 10, cfg.momentum, cfg.weight_decay)
+    X, Y = make_dataset(cfg, n=cfg.batch * 8)
+    x, y = X[:cfg.batch], Y[:cfg.batch]
+    g.forward(to_dev(x), train=True, step=0)
+    g.backward(to_dev(y), fused=sgd)
+    M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, 0)
     torch.cuda.synchronize()
-    assert_values_close(g, st, TOL)
+    load_oracle_state_into_gpu(g, st)          # identical state again; grad2 keeps step 0's values
+    pg, rg = g.prune_neurons(20.0)
+    po, ro = T.prune(st, 20.0)
+    assert pg == po and rg == ro and sum(ro) > 0
+    eg = g.evolve_topology(0.3, 0)
+    eo = T.evolve(st, 0.3, 0)
+    assert eg[1:] == eo
+    assert_topology_equal(g, st, f"{name} prune+evolve")
+    assert_values_bitexact(g, st, f"{name} prune+evolve")
+    x, y, tr = _kink_free(st, X[cfg.batch:], Y[cfg.batch:], cfg.batch, 1)
+    g.forward(to_dev(x), train=True, step=1)
+    g.backward(to_dev(y), fused=sgd)
+    M.step(st, M.backward(st, tr, y), sgd.lr, sgd.momentum, sgd.weight_decay)
+    torch.cuda.synchronize()
+    assert_values_close(g, st, TOL, f"{name} after prune+evolve")
     # the param view holds zeros in the pruned tail of each layer
     pv, _ = g.param_view()
     inf = g.info()
     pvh = pv.cpu().numpy()
     for l in range(2, cfg.n_layers + 1):
         o, n, c = inf["val_offset"][l - 1], inf["nnz"][l - 1], inf["cap"][l - 1]
-        assert np.all(pvh[o + n:o + c] == 0)
+        assert n < c or l == cfg.n_layers
+        assert np.all(pvh[o + n:o + c] == 0), (name, l)

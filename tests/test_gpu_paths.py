@@ -48,11 +48,11 @@ def _check_step(g, st, x, y, step, cfg, path_flag):
     g.backward(to_dev(y), fused=None)
     torch.cuda.synchronize()
     for l in range(2, cfg.n_layers):
-        assert rel_err(g.sparse_mlp_export_trace(0, l, B), tr.a[l - 1]) <= TOL, ("a", l)
+        assert rel_err(g.sparse_mlp_export_trace(0, l, B), tr.a[l - 1], tr.amag[l - 1]) <= TOL, ("a", l)
     gr = M.backward(st, tr, y)
     for Ly in st.layers:
-        assert rel_err(g.sparse_mlp_export_trace(2, Ly.l), gr.g[Ly.l - 2]) <= TOL, ("g", Ly.l)
-        assert rel_err(g.sparse_mlp_export_trace(3, Ly.l), gr.gb[Ly.l - 2]) <= TOL, ("gb", Ly.l)
+        assert rel_err(g.sparse_mlp_export_trace(2, Ly.l), gr.g[Ly.l - 2], gr.gmag[Ly.l - 2]) <= TOL, ("g", Ly.l)
+        assert rel_err(g.sparse_mlp_export_trace(3, Ly.l), gr.gb[Ly.l - 2], gr.gbmag[Ly.l - 2]) <= TOL, ("gb", Ly.l)
     return tr, gr
 
 
@@ -74,13 +74,15 @@ def test_binary_input_path_parity(B, chunk, fchunk, dropout, monkeypatch):
         _, gr = _check_step(g, st, x, y, s, cfg, 1.0)
         g.step(sgd)
         M.step(st, gr, sgd.lr, sgd.momentum, sgd.weight_decay)
+        torch.cuda.synchronize()
+        assert_values_close(g, st, TOL, f"binary path step {s}")
     # fused path (the 1-GPU bench path) on the last batch
     x, y = X[3 * B:], Y[3 * B:]
     g.forward(to_dev(x), train=True, step=3)
     g.backward(to_dev(y), fused=sgd)
     M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, 3)
     torch.cuda.synchronize()
-    assert_values_close(g, st, TOL * 3, "binary path")
+    assert_values_close(g, st, TOL, "binary path fused")
 
 
 def test_binary_path_falls_back_on_non_binary_input():
@@ -113,54 +115,45 @@ def test_real_input_kind_skips_the_bit_path():
         g.forward(to_dev(x), train=True, step=s_)
         assert g.sparse_mlp_export_trace(4, 0)[0] == -1.0
         for l in range(2, cfg.n_layers):
-            assert rel_err(g.sparse_mlp_export_trace(0, l, 64), tr.a[l - 1]) <= TOL, ("a", l)
+            assert rel_err(g.sparse_mlp_export_trace(0, l, 64), tr.a[l - 1], tr.amag[l - 1]) <= TOL, ("a", l)
         g.backward(to_dev(y), fused=sgd)
         M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, s_)
-    torch.cuda.synchronize()
-    assert_values_close(g, st, TOL * 2, "real input kind")
+        torch.cuda.synchronize()
+        assert_values_close(g, st, TOL, f"real input kind step {s_}")
 
 
-def test_binary_input_kind_bit_path_only():
-    """input_kind = SMLP_INPUT_BINARY: layer 2 runs only through the bit kernels (no fp32 launches
-    for it), same parity; a batch that breaks the promise raises SMLP_E_DATA at the next sync."""
+def test_binary_input_kind_checked_promise():
+    """input_kind = SMLP_INPUT_BINARY: binary batches take the bit path (same parity as the oracle);
+    a batch that breaks the promise is still trained correctly -- through the fp32 layer-2 kernels,
+    weights equal to the oracle's step on that batch, nothing corrupted -- and is
+    reported as SMLP_E_DATA at the next synchronising call."""
     from paper_2102_01732_b200 import SGD, SparseMLP, SparseMLPError
     torch = _torch()
     cfg = _binary_cfg(batch=64, dropout=0.3)
     st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed)
     g = SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed, 0, 64,
                   32, input_kind=2)
-    X, Y = _binary_data(128, cfg.sizes[0], seed=21)
+    X, Y = _binary_data(192, cfg.sizes[0], seed=21)
+    X[128 + 3, 7] = 0.5                              # the third batch breaks the promise
     sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay)
-    l0 = g.info()["launches"]
-    for s_ in range(2):
+    for s_ in range(3):
         x, y = X[s_ * 64:(s_ + 1) * 64], Y[s_ * 64:(s_ + 1) * 64]
         tr = M.forward(st, x, True, s_)
         assert sum(tr.ambiguous) == 0
         g.forward(to_dev(x), train=True, step=s_)
-        assert g.sparse_mlp_export_trace(4, 0)[0] == 1.0
+        assert g.sparse_mlp_export_trace(4, 0)[0] == (1.0 if s_ < 2 else 0.0)
         for l in range(2, cfg.n_layers):
-            assert rel_err(g.sparse_mlp_export_trace(0, l, 64), tr.a[l - 1]) <= TOL, ("a", l)
+            assert rel_err(g.sparse_mlp_export_trace(0, l, 64), tr.a[l - 1], tr.amag[l - 1]) <= TOL, ("a", s_, l)
         g.backward(to_dev(y), fused=sgd)
-        M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, s_)
-    g.sync()
-    assert_values_close(g, st, TOL * 2, "binary input kind")
-    # fewer launches than the auto path (no fp32 layer-2 kernels)
-    ga = SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed, 0, 64, 32)
-    a0 = ga.info()["launches"]
-    ga.forward(to_dev(X[:64]), train=True, step=0)
-    ga.backward(to_dev(Y[:64]), fused=sgd)
-    g2_0 = g.info()["launches"]
-    g.forward(to_dev(X[:64]), train=True, step=2)
-    g.backward(to_dev(Y[:64]), fused=sgd)
-    assert g.info()["launches"] - g2_0 < ga.info()["launches"] - a0
-    # the promise broken: flagged at the next synchronising call
-    xb = X[:64].copy()
-    xb[3, 7] = 0.5
-    g.forward(to_dev(xb), train=True, step=3)
-    g.backward(to_dev(Y[:64]), fused=sgd)
-    with pytest.raises(SparseMLPError):
+        M.step(st, M.backward(st, tr, y), sgd.lr, sgd.momentum, sgd.weight_decay)
+        torch.cuda.synchronize()
+        assert_values_close(g, st, TOL, f"binary input kind, step {s_}")
+    with pytest.raises(SparseMLPError, match="E_DATA"):
         g.sync()
-    torch.cuda.synchronize()
+    g.sync()                                         # reported once, then cleared
+    with pytest.raises(SparseMLPError, match="E_ARG"):
+        SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed, 0, 256,
+                  0, input_kind=2)                  # the bit path needs max_batch <= 128
 
 
 def test_binary_and_fp32_paths_agree_on_forward():
@@ -192,7 +185,7 @@ def test_generic_output_layer_parity():
     torch = _torch()
     cfg = get_config("C1", sizes=(120, 90, 70, 40), epsilon=6.0, dropout=0.2, batch=50)
     g, st = pair(cfg, max_batch=50, chunk_batch=16)
-    rng = np.random.default_rng(12)       # a batch with no kink-ambiguous pre-activation (R30)
+    rng = np.random.default_rng(12)       # a batch with no kink-ambiguous pre-activation (R32)
     X = rng.standard_normal((100, 120)).astype(np.float32)
     Y = rng.integers(0, 40, size=100).astype(np.int32)
     sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay)
@@ -202,19 +195,22 @@ def test_generic_output_layer_parity():
         assert sum(tr.ambiguous) == 0
         g.forward(to_dev(x), train=True, step=s)
         assert g.sparse_mlp_export_trace(4, 0)[0] == 0.0     # normal inputs: not binary
-        assert rel_err(g.sparse_mlp_export_trace(0, 4, 50), tr.z[-1]) <= TOL
+        assert rel_err(g.sparse_mlp_export_trace(0, 4, 50), tr.z[-1], tr.zmag[-1]) <= TOL
         g.backward(to_dev(y), fused=sgd)
         M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, s)
-    torch.cuda.synchronize()
-    assert_values_close(g, st, TOL * 2, "generic output layer")
+        torch.cuda.synchronize()
+        assert_values_close(g, st, TOL, f"generic output layer step {s}")
 
 
 # ----------------------------------------------------------------------------------------- C5 full size
-def _full_size_sampled_parity(name, B, widths):
+def _full_size_sampled_parity(name, B, widths, min_kept=256):
     """Full-size model in the bench launch configuration (max_batch = cfg.batch).  Checked: ER
-    topology and values bit-exact, every forward activation and logit of a B-row batch, and for
-    seeded samples of connections / neurons of every layer the gradient (unfused) and the Eq. 1
-    update (fused) against the oracle's cone evaluation (oracle/sampled.py)."""
+    topology and values bit-exact, every forward activation and logit of a B-row batch, every
+    exported delta_l element of the cone of the sampled neurons whose (b, j) does not depend on a
+    kink-ambiguous f' (R32), and for seeded samples of connections / neurons of every layer the
+    gradient (unfused) and the Eq. 1 update (fused) against the oracle's cone evaluation
+    (oracle/sampled.py).  Samples are drawn until >= min_kept untainted gradient entries, bias
+    gradients and delta elements per layer are compared; the per-layer counts are printed."""
     from oracle import sampled as S
     from paper_2102_01732_b200 import SGD
     from synth.data import c5_host_rows
@@ -231,34 +227,63 @@ def _full_size_sampled_parity(name, B, widths):
     g.forward(to_dev(x), train=True, step=0)
     assert g.sparse_mlp_export_trace(4, 0)[0] == 1.0
     for l in range(2, cfg.n_layers):
-        assert rel_err(g.sparse_mlp_export_trace(0, l, B), tr.a[l - 1]) <= TOL, ("a", l)
-    assert rel_err(g.sparse_mlp_export_trace(0, cfg.n_layers, B), tr.z[-1]) <= TOL
+        assert rel_err(g.sparse_mlp_export_trace(0, l, B), tr.a[l - 1], tr.amag[l - 1]) <= TOL, ("a", l)
+    assert rel_err(g.sparse_mlp_export_trace(0, cfg.n_layers, B), tr.z[-1], tr.zmag[-1]) <= TOL
     g.backward(to_dev(y), fused=None)
     torch.cuda.synchronize()
-    # seeded samples: 256 connections of every layer, 64 neurons of every layer (bias gradients)
+    L = cfg.n_layers
+    dexp = {l: g.sparse_mlp_export_trace(1, l, B) for l in range(2, L + 1)}
+    gexp = {Ly.l: g.sparse_mlp_export_trace(2, Ly.l) for Ly in st.layers}
+    gbexp = {l: g.sparse_mlp_export_trace(3, l) for l in range(2, L + 1)}
+    # seeded samples, drawn in rounds of 512 connections / 128 neurons per layer until every layer
+    # has >= min_kept untainted ones (all of them when a layer is smaller)
     rng = np.random.default_rng(2025)
-    ent = {Ly.l: np.sort(rng.choice(Ly.nnz, size=256, replace=False)) for Ly in st.layers}
-    neu = {l: np.sort(rng.choice(cfg.sizes[l - 1], size=min(64, cfg.sizes[l - 1]), replace=False))
-           for l in range(2, cfg.n_layers + 1)}
-    need = {l: set(neu[l].tolist()) for l in neu}
-    for Ly in st.layers:
-        need[Ly.l] |= set(Ly.col[ent[Ly.l]].tolist())
-    deltas, tainted = S.delta_columns(st, tr, y, need)
-    kept = 0
-    gsamp = {}
+    ent = {Ly.l: np.zeros(0, np.int64) for Ly in st.layers}
+    neu = {l: np.zeros(0, np.int64) for l in range(2, L + 1)}
+    for rnd in range(8):
+        for Ly in st.layers:
+            free = np.setdiff1d(np.arange(Ly.nnz), ent[Ly.l]) if Ly.nnz <= 4096 else None
+            new = (rng.choice(free, size=min(512, len(free)), replace=False) if free is not None
+                   else rng.choice(Ly.nnz, size=512, replace=False))
+            ent[Ly.l] = np.unique(np.concatenate([ent[Ly.l], new]))
+        for l in neu:
+            n = cfg.sizes[l - 1]
+            neu[l] = np.unique(np.concatenate([neu[l], rng.choice(n, size=min(128, n), replace=False)]))
+        need = {l: set(neu[l].tolist()) for l in neu}
+        for Ly in st.layers:
+            need[Ly.l] |= set(Ly.col[ent[Ly.l]].tolist())
+        deltas, tainted, dmags = S.delta_columns(st, tr, y, need)
+        gsamp, kept = {}, {}
+        for Ly in st.layers:
+            l = Ly.l
+            ok = np.array([not tainted[l][int(j)].any() for j in Ly.col[ent[l]]])
+            go, gm = S.grad_entries(st, tr, deltas, dmags, l, ent[l])
+            gsamp[l] = (go, gm, ok)
+            okn = np.array([not tainted[l][int(j)].any() for j in neu[l]])
+            gbo, gbm = S.bias_grad_columns(deltas, dmags, l, neu[l])
+            J = np.array(sorted(deltas[l]), np.int64)
+            T = np.stack([tainted[l][int(j)] for j in J], axis=1)
+            kept[l] = (int(ok.sum()), int(okn.sum()), int((~T).sum()))
+        if all(min(k) >= min(min_kept, Ly.nnz) for k, Ly in zip(kept.values(), st.layers)):
+            break
+    print(f"{name} kept per layer (gradient entries, bias gradients, delta elements):", kept)
     for Ly in st.layers:
         l = Ly.l
-        ok = np.array([not tainted[l][int(j)] for j in Ly.col[ent[l]]])
-        kept += int(ok.sum())
-        go = S.grad_entries(st, tr, deltas, l, ent[l])
-        gg = g.sparse_mlp_export_trace(2, l)[ent[l]]
-        assert rel_err(gg[ok], go[ok]) <= TOL, ("g", l, rel_err(gg[ok], go[ok]))
-        gsamp[l] = (go, ok)
-        okn = np.array([not tainted[l][int(j)] for j in neu[l]])
-        gbo = S.bias_grad_columns(deltas, l, neu[l])
-        gbg = g.sparse_mlp_export_trace(3, l)[neu[l]]
-        assert rel_err(gbg[okn], gbo[okn]) <= TOL, ("gb", l)
-    assert kept >= 0.75 * 256 * len(st.layers)   # the rest touch a kink-ambiguous element (R30)
+        assert min(kept[l]) >= min(min_kept, Ly.nnz), (l, kept[l])
+        go, gm, ok = gsamp[l]
+        gg = gexp[l][ent[l]]
+        assert rel_err(gg[ok], go[ok], gm[ok]) <= TOL, ("g", l, rel_err(gg[ok], go[ok], gm[ok]))
+        okn = np.array([not tainted[l][int(j)].any() for j in neu[l]])
+        gbo, gbm = S.bias_grad_columns(deltas, dmags, l, neu[l])
+        gbg = gbexp[l][neu[l]]
+        assert rel_err(gbg[okn], gbo[okn], gbm[okn]) <= TOL, ("gb", l)
+    for l in range(2, L + 1):
+        J = np.array(sorted(deltas[l]), np.int64)
+        D = np.stack([deltas[l][int(j)] for j in J], axis=1)
+        Dm = np.stack([dmags[l][int(j)] for j in J], axis=1)
+        T = np.stack([tainted[l][int(j)] for j in J], axis=1)
+        dg = dexp[l][:, J]
+        assert rel_err(dg[~T], D[~T], Dm[~T]) <= TOL, ("delta", l, rel_err(dg[~T], D[~T], Dm[~T]))
     # the fused Eq. 1 update in the bench configuration, on a second handle with the same init
     del g
     g2, _ = pair(cfg)
@@ -268,16 +293,19 @@ def _full_size_sampled_parity(name, B, widths):
     torch.cuda.synchronize()
     # expected update: the oracle's Eq. 1 (model.step) with the sampled gradients (zero elsewhere)
     G = M.Grads([np.zeros(Ly.nnz, np.float32) for Ly in st.layers],
-                [np.zeros(n, np.float32) for n in cfg.sizes[1:]], 0.0, [])
+                [np.zeros(n, np.float32) for n in cfg.sizes[1:]], 0.0, [],
+                [np.zeros(Ly.nnz) for Ly in st.layers], [np.zeros(n) for n in cfg.sizes[1:]])
     for Ly in st.layers:
         G.g[Ly.l - 2][ent[Ly.l]] = gsamp[Ly.l][0]
+        G.gmag[Ly.l - 2][ent[Ly.l]] = gsamp[Ly.l][1]
     M.step(st, G, sgd.lr, sgd.momentum, sgd.weight_decay)
     for Ly in st.layers:
         l = Ly.l
-        ok = gsamp[l][1]
+        ok = gsamp[l][2]
         e = g2.export_layer(l)
-        assert rel_err(e["w"][ent[l]][ok], Ly.w[ent[l]][ok]) <= TOL, ("w", l)
-        assert rel_err(e["v"][ent[l]][ok], Ly.v[ent[l]][ok]) <= TOL, ("v", l)
+        k = ent[l][ok]
+        assert rel_err(e["w"][k], Ly.w[k], Ly.wmag[k]) <= TOL, ("w", l)
+        assert rel_err(e["v"][k], Ly.v[k], Ly.vmag[k]) <= TOL, ("v", l)
 
 
 def test_c5_full_size_sampled_parity():
@@ -303,7 +331,7 @@ def test_width_scaling_t2_full_size_sampled_parity():
 
 
 # salt: data seed chosen (by the oracle alone) so that no pre-activation of the checked steps
-# sits within rounding of a kink (R30)
+# sits within rounding of a kink (R32)
 @pytest.mark.parametrize("chunk,fchunk,B,dropout,eps,salt",
                          [(8, 8, 29, 0.2, 40.0, 0), (16, 16, 64, 0.0, 40.0, 1), (32, 32, 77, 0.3, 40.0, 0),
                           (64, 64, 128, 0.0, 40.0, 0), (128, 128, 128, 0.2, 40.0, 0),
@@ -337,31 +365,43 @@ def test_long_rows_and_chunk_widths_parity(chunk, fchunk, B, dropout, eps, salt,
     if eps == 40.0:
         assert max(np.diff(st.layers[1].row_ptr)) > 64
     rng = np.random.default_rng([chunk, B, salt])
-    X = rng.standard_normal((3 * B, 30)).astype(np.float32)
-    Y = rng.integers(0, 10, size=3 * B).astype(np.int32)
+    X = rng.standard_normal((16 * B, 30)).astype(np.float32)
+    Y = rng.integers(0, 10, size=16 * B).astype(np.int32)
     sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay)
+    nxt = 0
     for s in range(2):
-        x, y = X[s * B:(s + 1) * B], Y[s * B:(s + 1) * B]
-        tr = M.forward(st, x, True, s)
-        if sum(tr.ambiguous):
-            pytest.skip("kink-ambiguous batch")
+        while True:           # the next candidate batch the oracle finds kink-free (R32)
+            assert nxt < 16, "no kink-free batch among the candidates"
+            x, y = X[nxt * B:(nxt + 1) * B], Y[nxt * B:(nxt + 1) * B]
+            nxt += 1
+            tr = M.forward(st, x, True, s)
+            if sum(tr.ambiguous) == 0:
+                break
         g.forward(to_dev(x), train=True, step=s)
         g.backward(to_dev(y), fused=None)
         torch.cuda.synchronize()
         for l in range(2, cfg.n_layers):
-            assert rel_err(g.sparse_mlp_export_trace(0, l, B), tr.a[l - 1]) <= TOL, ("a", l)
+            assert rel_err(g.sparse_mlp_export_trace(0, l, B), tr.a[l - 1], tr.amag[l - 1]) <= TOL, ("a", l)
         gr = M.backward(st, tr, y)
         for Ly in st.layers:
-            assert rel_err(g.sparse_mlp_export_trace(2, Ly.l), gr.g[Ly.l - 2]) <= TOL, ("g", Ly.l)
-            assert rel_err(g.sparse_mlp_export_trace(3, Ly.l), gr.gb[Ly.l - 2]) <= TOL, ("gb", Ly.l)
+            assert rel_err(g.sparse_mlp_export_trace(2, Ly.l), gr.g[Ly.l - 2], gr.gmag[Ly.l - 2]) <= TOL, ("g", Ly.l)
+            assert rel_err(g.sparse_mlp_export_trace(3, Ly.l), gr.gb[Ly.l - 2], gr.gbmag[Ly.l - 2]) <= TOL, ("gb", Ly.l)
         g.step(sgd)
         M.step(st, gr, sgd.lr, sgd.momentum, sgd.weight_decay)
-    x, y = X[2 * B:], Y[2 * B:]
+        torch.cuda.synchronize()
+        assert_values_close(g, st, TOL, f"long rows step {s}")
+    while True:
+        assert nxt < 16, "no kink-free batch among the candidates"
+        x, y = X[nxt * B:(nxt + 1) * B], Y[nxt * B:(nxt + 1) * B]
+        nxt += 1
+        tr = M.forward(st, x, True, 2)
+        if sum(tr.ambiguous) == 0:
+            break
     g.forward(to_dev(x), train=True, step=2)
     g.backward(to_dev(y), fused=sgd)
-    M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, 2)
+    M.step(st, M.backward(st, tr, y), sgd.lr, sgd.momentum, sgd.weight_decay)
     torch.cuda.synchronize()
-    assert_values_close(g, st, TOL * 3, "long rows fused")
+    assert_values_close(g, st, TOL, "long rows fused")
     assert_topology_equal(g, st)
 
 
@@ -447,7 +487,11 @@ def test_gradient_flow_parity(cfg_name):
     gr = M.backward(st, tr, Y)
     ref = M.gradient_flow(gr)
     assert f1 == f2
-    assert abs(f1 - ref) <= 3e-4 * ref, (f1, ref)
+    # R24: each GPU gradient value is within KAPPA_U * mag of the oracle's, so sum g^2 moves by
+    # at most sum 2 |g| KAPPA_U mag (first order); on top of that, 1e-4 relative
+    from oracle.compare import KAPPA_U
+    bound = sum(float(np.sum(2.0 * np.abs(gv.astype(np.float64)) * KAPPA_U * m)) for gv, m in zip(gr.g + gr.gb, gr.gmag + gr.gbmag))
+    assert abs(f1 - ref) <= 1e-4 * ref + bound, (f1, ref, bound)
 
 
 def test_post_training_prune_sweep_parity():
@@ -557,7 +601,8 @@ def test_retain_valid_updates_parity():
     assert_topology_equal(g, st)
     sgd = SGD(cfg.lr, cfg.momentum, cfg.weight_decay)
     ref = ODP.retain_valid_updates(keys_t, gr.g, st)
-    for (pos, gv), Ly, r in zip(stale.layers, st.layers, ref):
+    rmag = [m.astype(np.float64) for m in ODP.retain_valid_updates(keys_t, [x.astype(np.float32) for x in gr.gmag], st)]
+    for (pos, gv), Ly, r, rm in zip(stale.layers, st.layers, ref, rmag):
         k = g.retain_valid_updates(Ly.l, pos, gv)
         assert k == len(set(keys_t[Ly.l - 2].tolist()) & set(Ly.keys().tolist()))
         # pure data movement: bit-exact against the same mapping of the GPU's own stale values
@@ -565,11 +610,11 @@ def test_retain_valid_updates_parity():
         mapped = np.array([table.get(p, 0.0) for p in Ly.keys().tolist()], np.float32)
         got = g.sparse_mlp_export_trace(2, Ly.l)[:len(mapped)]
         assert np.array_equal(got.view(np.uint32), mapped.view(np.uint32)), Ly.l
-        assert rel_err(mapped, r) <= TOL                      # and the oracle's retained gradient
+        assert rel_err(mapped, r, rm) <= TOL                  # and the oracle's retained gradient
     kept = apply_stale_gradient(g, stale, sgd)                 # the full server step
     torch.cuda.synchronize()
     assert kept == [len(set(keys_t[L.l - 2].tolist()) & set(L.keys().tolist())) for L in st.layers]
-    M.step(st, M.Grads(ref, gr.gb, gr.loss, gr.deltas), sgd.lr, sgd.momentum, sgd.weight_decay)
+    M.step(st, M.Grads(ref, gr.gb, gr.loss, gr.deltas, rmag, gr.gbmag), sgd.lr, sgd.momentum, sgd.weight_decay)
     assert_values_close(g, st, TOL)
 
 

@@ -348,23 +348,28 @@ def test_sampled_backward_equals_full_backward():
     tr = M.forward(st, X, True, 1)
     gr = M.backward(st, tr, Y)
     need = {l: range(cfg.sizes[l - 1]) for l in range(2, st.L + 1)}
-    deltas, tainted = S.delta_columns(st, tr, Y, need)
+    deltas, tainted, dmags = S.delta_columns(st, tr, Y, need)
     for l in range(2, st.L + 1):
         D = np.stack([deltas[l][j] for j in range(cfg.sizes[l - 1])], axis=1)
         np.testing.assert_allclose(D, gr.deltas[l - 1], rtol=1e-6, atol=1e-9)
-        np.testing.assert_allclose(S.bias_grad_columns(deltas, l, np.arange(cfg.sizes[l - 1])), gr.gb[l - 2],
-                                   rtol=1e-6, atol=1e-9)
+        Dm = np.stack([dmags[l][j] for j in range(cfg.sizes[l - 1])], axis=1)
+        np.testing.assert_allclose(Dm, gr.dmag[l - 1], rtol=1e-9, atol=1e-15)
+        gb, gbm = S.bias_grad_columns(deltas, dmags, l, np.arange(cfg.sizes[l - 1]))
+        np.testing.assert_allclose(gb, gr.gb[l - 2], rtol=1e-6, atol=1e-9)
+        np.testing.assert_allclose(gbm, gr.gbmag[l - 2], rtol=1e-9, atol=1e-15)
         k = np.arange(st.layer(l).nnz)
-        np.testing.assert_allclose(S.grad_entries(st, tr, deltas, l, k), gr.g[l - 2], rtol=1e-6, atol=1e-9)
-    assert not any(any(t.values()) for t in tainted.values())   # no kink-ambiguous element here
+        g, gm = S.grad_entries(st, tr, deltas, dmags, l, k)
+        np.testing.assert_allclose(g, gr.g[l - 2], rtol=1e-6, atol=1e-9)
+        np.testing.assert_allclose(gm, gr.gmag[l - 2], rtol=1e-9, atol=1e-15)
+    assert not any(t.any() for tl in tainted.values() for t in tl.values())   # no kink-ambiguous element here
     # a sparse request only evaluates its cone and gives the same columns
-    d2, _ = S.delta_columns(st, tr, Y, {2: [3, 7]})
+    d2, _, _ = S.delta_columns(st, tr, Y, {2: [3, 7]})
     assert set(d2[2]) == {3, 7} and len(d2[3]) < cfg.sizes[2] + 1
     np.testing.assert_array_equal(d2[2][7], deltas[2][7])
 
 
 def test_kink_guard_ignores_exact_zero_preactivations():
-    """Binary inputs with no active input and zero bias give z = 0 exactly on every path (R30)."""
+    """Binary inputs with no active input and zero bias give z = 0 exactly on every path (R32)."""
     cfg = get_config("C1", sizes=(40, 30, 20, 2), epsilon=2.0, dropout=0.0, batch=8)
     st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, 0.0, cfg.init, 3)
     x = np.zeros((8, 40), np.float32)
@@ -395,3 +400,126 @@ def test_gradient_flow_pins():
     ref = sum(float(np.sum(np.square(dWs[k][Ly.rows(), Ly.col]))) for k, Ly in enumerate(st.layers))
     ref += sum(float(np.sum(np.square(b))) for b in dbs)
     assert abs(M.gradient_flow(gr) - ref) <= 1e-4 * ref
+
+
+def test_sparse_products_against_scipy_and_dense(monkeypatch):
+    """The oracle's plain-NumPy products (segmented sums over the support) against two independent
+    computations: a SciPy CSR product (SciPy only in oracle self-tests) and
+    the dense zero-filled matrix.  A tiny chunk size forces output segments to be
+    split across chunks, and empty rows / columns occur."""
+    import scipy.sparse as sp
+    monkeypatch.setattr(M, "_CHUNK_ELEMS", 37)
+    Ly = M.er_layer(53, 41, 0.8, "he_uniform", 9, 2)
+    assert np.any(np.diff(Ly.row_ptr) == 0) and len(np.unique(Ly.col)) < Ly.n_out
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((6, 53)).astype(np.float32)
+    d = rng.standard_normal((6, 41)).astype(np.float32)
+    W = sp.csr_matrix((Ly.w.astype(np.float64), Ly.col, Ly.row_ptr), shape=(53, 41))
+    D = Ly.dense()
+    z = M.spmm_fwd(a, Ly)
+    np.testing.assert_allclose(z, (W.T @ a.astype(np.float64).T).T, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(z, a.astype(np.float64) @ D, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(M.spmm_fwd(a, Ly, wabs=True), np.abs(a).astype(np.float64) @ np.abs(D),
+                               rtol=1e-12, atol=1e-12)
+    bk = M.spmm_bwd(d, Ly)
+    np.testing.assert_allclose(bk, (W @ d.astype(np.float64).T).T, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(bk, d.astype(np.float64) @ D.T, rtol=1e-12, atol=1e-12)
+    g = M.sddmm(a, d, Ly)
+    full = a.astype(np.float64).T @ d.astype(np.float64)
+    np.testing.assert_allclose(g, full[Ly.rows(), Ly.col], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("seed,dropout,alpha", [(1, 0.0, 0.6), (2, 0.3, 0.75), (3, 0.2, 0.05), (4, 0.0, 0.5)])
+def test_error_magnitudes_bound_an_fp32_implementation(seed, dropout, alpha):
+    """DESIGN.md R24 pin: the oracle's running error magnitudes bound the difference between the
+    fp64 oracle and an INDEPENDENT fp32 implementation of the same step (tests/dense_ref.py in
+    float32: dense masked matrices, BLAS sgemm summation order), element by element, for every
+    activation, logit, probability, delta, weight / bias gradient and -- after two Eq. 1 steps --
+    every weight, momentum and bias:  |fp32 - oracle| <= KAPPA_U * mag.  And the bound is not
+    vacuous: KAPPA_U * mag stays below 1e-4 relative wherever the value is not a cancellation."""
+    from oracle.compare import KAPPA_U, rel_err
+    cfg = get_config("C1", sizes=(70, 60, 50, 40, 3), epsilon=6.0, alpha=alpha, dropout=dropout, batch=32)
+    st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, seed)
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((64, 70)).astype(np.float32)
+    Y = rng.integers(0, 3, 64)
+    lr, mu, wd = 0.05, 0.9, 2e-4
+    Ws32 = [Ly.dense(np.float32) for Ly in st.layers]
+    bs32 = [b.copy() for b in st.b]
+    Vs32 = [np.zeros_like(W) for W in Ws32]
+    vb32 = [np.zeros_like(b) for b in bs32]
+    for s_ in range(2):
+        x, y = X[s_ * 32:(s_ + 1) * 32], Y[s_ * 32:(s_ + 1) * 32]
+        tr = M.forward(st, x, True, s_)
+        gr = M.backward(st, tr, y)
+        keeps = [tr.keep[k + 1] for k in range(len(st.layers) - 1)] + [None]
+        out = {}
+        _, p32, dW32, db32 = dense_ref.forward_backward(Ws32, bs32, x, y, alpha, "all_relu", keeps, dropout,
+                                                        np.float32, out)
+        if sum(tr.ambiguous) == 0:
+            for k in range(1, st.L - 1):
+                d = np.abs(out["a"][k].astype(np.float64) - tr.a[k])
+                assert np.all(d <= KAPPA_U * tr.amag[k]), ("a", s_, k + 1)
+            assert np.all(np.abs(p32 - tr.p64) <= KAPPA_U * tr.pmag + 2.0 ** -23 * tr.p64)
+            for k, Ly in enumerate(st.layers):
+                g32 = dW32[k][Ly.rows(), Ly.col].astype(np.float64)
+                assert np.all(np.abs(g32 - gr.g[k]) <= KAPPA_U * gr.gmag[k] + 2.0 ** -24 * np.abs(gr.g[k])), ("g", s_, k)
+                assert np.all(np.abs(db32[k] - gr.gb[k]) <= KAPPA_U * gr.gbmag[k] + 2.0 ** -24 * np.abs(gr.gb[k]))
+                if k >= 1:
+                    dd = np.abs(out["delta"][k + 1].astype(np.float64) - gr.deltas[k + 1])
+                    assert np.all(dd <= KAPPA_U * gr.dmag[k + 1] + 2.0 ** -24 * np.abs(gr.deltas[k + 1])), ("delta", k)
+            # not vacuous: where the activation is not a cancellation (|a| >= mag / 16), the error
+            # bound is far below the 1e-4 relative target
+            for k in range(1, st.L - 1):
+                big = np.abs(tr.a[k]) >= tr.amag[k] / 16
+                assert np.all(KAPPA_U * tr.amag[k][big] <= 1e-4 * np.abs(tr.a[k][big]))
+        M.step(st, gr, lr, mu, wd)
+        for k in range(len(Ws32)):
+            g = dW32[k] + wd * Ws32[k]
+            Vs32[k] = (np.float32(mu) * Vs32[k] - np.float32(lr) * g.astype(np.float32)).astype(np.float32)
+            Ws32[k] = ((Ws32[k] + Vs32[k]) * (Ws32[k] != 0)).astype(np.float32)
+            vb32[k] = (np.float32(mu) * vb32[k] - np.float32(lr) * db32[k]).astype(np.float32)
+            bs32[k] = (bs32[k] + vb32[k]).astype(np.float32)
+    for k, Ly in enumerate(st.layers):
+        w32 = Ws32[k][Ly.rows(), Ly.col]
+        v32 = Vs32[k][Ly.rows(), Ly.col]
+        assert np.all(np.abs(w32.astype(np.float64) - Ly.w) <= KAPPA_U * Ly.wmag), ("w", k)
+        assert np.all(np.abs(v32.astype(np.float64) - Ly.v) <= KAPPA_U * Ly.vmag), ("v", k)
+        assert np.all(np.abs(bs32[k].astype(np.float64) - st.b[k]) <= KAPPA_U * st.bmag[k]), ("b", k)
+        # and the comparison metric built on it passes the fp32 implementation
+        assert rel_err(w32, Ly.w, Ly.wmag) <= 1e-4 and rel_err(v32, Ly.v, Ly.vmag) <= 1e-4
+
+
+def test_sampled_taint_is_exactly_the_kink_dependence(monkeypatch):
+    """R32 pin for the per-(b, j) taint of oracle/sampled.py: (1) with the documented band the
+    per-column kink test reproduces the full forward's ambiguous count; (2) with a wide band
+    (many ambiguous elements), flipping the sign of every ambiguous pre-activation -- i.e. taking
+    the other branch of f' there -- changes only tainted deltas, and changes some."""
+    from oracle import sampled as S
+    cfg = get_config("C1", sizes=(60, 50, 40, 30, 3), epsilon=4.0, dropout=0.2, batch=17)
+    st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, 8)
+    X, Y = make_dataset(cfg, n=17)
+    tr = M.forward(st, X, True, 0)
+    for l in range(2, st.L):
+        cnt = int(S.kink_columns(st, tr, l, np.arange(cfg.sizes[l - 1])).sum())
+        assert cnt == tr.ambiguous[l - 1]
+    monkeypatch.setattr(S, "KINK_REL", 0.02)
+    need = {l: range(cfg.sizes[l - 1]) for l in range(2, st.L + 1)}
+    deltas, tainted, _ = S.delta_columns(st, tr, Y, need)
+    import copy
+    tr2 = copy.copy(tr)
+    tr2.z = list(tr.z)
+    for l in range(2, st.L):
+        amb = S.kink_columns(st, tr, l, np.arange(cfg.sizes[l - 1]))
+        assert amb.any()
+        z = tr.z[l - 1].copy()
+        z[amb] = np.where(z[amb] > 0, -z[amb], np.abs(z[amb]) + 1e-30)
+        tr2.z[l - 1] = z
+    d2, _, _ = S.delta_columns(st, tr2, Y, need)
+    changed_any = False
+    for l in range(2, st.L):
+        for j in range(cfg.sizes[l - 1]):
+            ch = deltas[l][j] != d2[l][j]
+            assert not np.any(ch & ~tainted[l][j]), (l, j)
+            changed_any |= bool(ch.any())
+    assert changed_any
