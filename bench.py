@@ -109,16 +109,31 @@ def load_data(cfg, rank, world, device):
             torch.from_numpy(np.ascontiguousarray(Y[lo:hi])).to(device))
 
 
-def cpu_baseline_job(cfg_name: str, batch: int, steps: int) -> dict:
-    """The oracle as it stands, on the host cores, over a bounded sample of the same workload."""
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_job(cfg_name: str, batch: int, steps: int, evolve: bool = False) -> dict:
+    """The oracle as it stands (its test instrumentation -- the R24 error magnitudes and the R32
+    kink count -- switched off), single-threaded on the host cores, over a bounded sample of the
+    same workload: `steps` training steps (fwd + bwd + Eq. 1) at batch `batch`, optionally followed
+    by one SET evolution of every sparse layer (timed separately)."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     os.environ.setdefault("MKL_NUM_THREADS", "1")
     import numpy as np
 
     from oracle import model as M
+    from oracle import topology as T
     from synth import get_config
     from synth.data import c5_host_rows, make_dataset
+    M.INSTRUMENT = False
     cfg = get_config(cfg_name)
     t0 = time.perf_counter()
     st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed)
@@ -130,31 +145,66 @@ def cpu_baseline_job(cfg_name: str, batch: int, steps: int) -> dict:
         sl = slice(s * batch, (s + 1) * batch)
         M.train_step(st, X[sl], Y[sl], cfg.lr, cfg.momentum, cfg.weight_decay, s)
     dt = time.perf_counter() - t0
+    t_ev = None
+    if evolve:
+        t1 = time.perf_counter()
+        T.evolve(st, cfg.zeta, 0)
+        t_ev = time.perf_counter() - t1
+    nz = sum(L.nnz for L in st.layers if not L.dense_capped)
     return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{steps} oracle training steps (fwd+bwd+Eq.1 update) of {cfg_name} at batch {batch} "
-                      f"(of {cfg.batch}); {dt:.1f} s timed, {t_init:.1f} s untimed ER init; NumPy/SciPy, "
-                      f"1 thread, os.cpu_count()={os.cpu_count()}"}
+            "sample": f"{steps} oracle training step(s) (fwd+bwd+Eq.1 update) of {cfg_name} at batch {batch} "
+                      f"(of {cfg.batch}): {dt:.1f} s timed"
+                      + (f"; one SET evolution of all sparse layers ({nz / 1e6:.1f}M connections): {t_ev:.1f} s"
+                         if t_ev is not None else "")
+                      + f"; {t_init:.1f} s untimed ER init; plain NumPy, 1 thread, test instrumentation off",
+            "cpu_model": _cpu_model(), "host_cpu_count": os.cpu_count(),
+            "evolve_s": None if t_ev is None else round(t_ev, 2), "step_s": round(dt / steps, 2)}
+
+
+def gathered_bytes(rec, sizes, nnz, cb, cbf):
+    """L2->SM gather bytes of one launch of a row kernel (SURVEY.md §8(d) second ceiling): one
+    chunk-wide fp32 row per connection -- the forward gathers a_{l-1} rows (CBf columns), the
+    backward delta_l rows (CB columns).  Narrow output layers stream instead (0)."""
+    l = rec["layer"]
+    if rec["kernel"] not in ("fwd", "bwd") or l < 2:
+        return 0.0
+    if l == len(sizes) and sizes[-1] <= 32:
+        return 0.0
+    w = cbf if rec["kernel"] == "fwd" else cb
+    return float(nnz[l - 1]) * w * 4.0
 
 
 # ------------------------------------------------------------------------------------------ reference arm
 def run_reference(args):
+    """The reference arm of this tier: the oracle as it stands on the host cores,
+    rank 0 only.  Same workload, metric and config as our arm; each step is a bounded sample of the
+    workload's minibatch (C5: 4 of the 128 rows, C3: all 5, others the full batch) so the whole
+    --steps K --warmup W run stays within a few minutes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from synth import get_config
     cfg = get_config(args.config)
-    sample_B = min(cfg.batch, 8) if (cfg.binary_input or cfg.name == "C3") else cfg.batch
+    sample_B = min(cfg.batch, 4) if cfg.binary_input else cfg.batch
     warm = max(0, min(args.warmup, 1))
     res = cpu_baseline_job(cfg.name, sample_B, args.steps + warm)
+    res["sample"] = (f"each of the {args.steps + warm} timed steps runs {sample_B} of the {cfg.batch} rows of the "
+                     f"minibatch; " + res["sample"])
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg.name, "global_batch": sample_B, "layer_sizes": list(cfg.sizes),
-                       "epsilon": cfg.epsilon},
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(cfg, args.gpus),
             "cpu_baseline": res,
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def config_dict(cfg, world: int) -> dict:
+    """The workload keys both arms report (BASELINE.json configs)."""
+    return {"workload": cfg.name, "stand_in_for": cfg.stand_in_for, "global_batch": cfg.batch * world,
+            "batch_per_rank": cfg.batch, "layer_sizes": list(cfg.sizes), "epsilon": cfg.epsilon,
+            "parallelism": f"dp{world}"}
 
 
 # ------------------------------------------------------------------------------------------ our arm
@@ -190,15 +240,6 @@ def main():
     device = torch.device("cuda", local)
     cfg = get_config(args.config)
     B = cfg.batch
-
-    # cpu_baseline (oracle, host cores) in a side process on rank 0, N = 1 only
-    cpu_fut = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import concurrent.futures as cf
-        import multiprocessing as mp
-        ex = cf.ProcessPoolExecutor(1, mp_context=mp.get_context("spawn"))
-        cpu_B = min(B, 8) if (cfg.binary_input or cfg.name == "C3") else B
-        cpu_fut = ex.submit(cpu_baseline_job, cfg.name, cpu_B, 2 if cfg.binary_input else 20)
 
     t0 = time.perf_counter()
     model = SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed,
@@ -337,6 +378,33 @@ def main():
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": f"{dom['kernel']} W^({dom['layer']})", "avg_launch_ms": round(avg_ms, 4),
                 "algorithmic_bytes_per_launch": dom["bytes_per_launch"], "peak_source": peak_src}
+    # second ceiling: L2 -> SM random-row gathers (profiles/gather_ceiling.json, measured on the box)
+    roof_g = None
+    gpath = os.path.join(ROOT, "profiles", "gather_ceiling.json")
+    if prof and os.path.exists(gpath):
+        try:
+            GC = json.load(open(gpath))
+            gpeak = float(GC["ceiling_GBps"])
+            per = []
+            step_gb = 0.0
+            for r in prof:
+                gb = gathered_bytes(r, cfg.sizes, nnz, info0["chunk_batch"], info0["fwd_chunk_batch"])
+                if gb <= 0:
+                    continue
+                avg = r["total_ms"] / r["launches"]
+                step_gb += gb * r["launches"] / profiled_steps
+                per.append({"kernel": f"{r['kernel']} W^({r['layer']})", "gathered_bytes_per_launch": gb,
+                            "avg_launch_ms": round(avg, 4), "achieved_GBps": round(gb / (avg * 1e-3) / 1e9, 1),
+                            "frac": round(gb / (avg * 1e-3) / 1e9 / gpeak, 4)})
+            if per:
+                ach = step_gb / (ms_per_step * 1e-3) / 1e9
+                roof_g = {"bound": "l2_gather", "peak": gpeak, "unit": "GB/s",
+                          "peak_source": "profiles/gather_ceiling.json (tools/gather_ceiling.py, sm clock median "
+                                         f"{GC.get('clocks', {}).get('sm_mhz_median')} MHz)",
+                          "gathered_bytes_per_step": step_gb, "achieved_step_GBps": round(ach, 1),
+                          "frac_step": round(ach / gpeak, 4), "kernels": per}
+        except Exception as e:  # reported, not fatal
+            roof_g = {"bound": "l2_gather", "error": str(e)}
     step_bytes = f1_bytes(cfg.sizes, nnz, B)
     step_roof = {"bytes_per_step_F1": step_bytes, "achieved_GBps": round(step_bytes / (ms_per_step * 1e-3) / 1e9, 1),
                  "frac": round(step_bytes / (ms_per_step * 1e-3) / 1e9 / peak, 4)}
@@ -419,10 +487,16 @@ def main():
                        "sparse_mlp_train_step_host_async (pinned host x, y -> device on a copy stream "
                        "overlapping the previous step, fwd, fused bwd, loss -> pinned host)")}
 
+    # cpu_baseline (the oracle on the host cores), rank 0 at N = 1 only, after every GPU-timed
+    # region: one full C5 step at the bench batch (B = 128) + one SET evolution; 20 steps otherwise
     cpu = None
-    if cpu_fut is not None:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import concurrent.futures as cf
+        import multiprocessing as mp
         try:
-            cpu = cpu_fut.result(timeout=900)
+            with cf.ProcessPoolExecutor(1, mp_context=mp.get_context("spawn")) as ex:
+                cpu = ex.submit(cpu_baseline_job, cfg.name, B, 1 if cfg.binary_input else 20,
+                                bool(cfg.binary_input)).result(timeout=1500)
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
 
@@ -430,17 +504,17 @@ def main():
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": cfg.name, "stand_in_for": cfg.stand_in_for, "global_batch": B * world,
+                "config": {**config_dict(cfg, world),
                            "step_path": "dp: unfused bwd + per-layer overlapped allreduce + Eq.1 kernel" if dp_path
                            else "1 GPU: sparse_mlp_backward with SGD (gradient, then the streaming Eq.1 pass "
                            "and mirror refresh inside the same call)",
-                           "batch_per_rank": B, "layer_sizes": list(cfg.sizes), "epsilon": cfg.epsilon,
                            "nnz": sum(nnz), "chunk_batch": info0["chunk_batch"],
                            "fwd_chunk_batch": info0["fwd_chunk_batch"],
-                           "parallelism": f"dp{world}", "l2_flush": "inputs larger than L2 (resident shard "
+                           "l2_flush": "inputs larger than L2 (resident shard "
                            f"{X.numel() * 4 / 1e9:.1f} GB; per-step traffic {step_bytes / 1e9:.2f} GB)",
                            "create_s": round(t_create, 2), "cuda_graph": graph_note},
-                "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roof, "step_roofline": step_roof, "roofline_l2_gather": roof_g,
+                "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk, "epoch": epoch, "profiled_steps": profiled_steps,
                 "ms_per_step_profiled": round(ms_prof, 4),
                 "kernels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in prof]}

@@ -12,6 +12,8 @@ and rounded once.
 from __future__ import annotations
 
 import math
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -122,6 +124,9 @@ class State:
 # --------------------------------------------------------------------------------------
 # Erdos-Renyi initialisation (Alg. 2)
 # --------------------------------------------------------------------------------------
+MAX_CANDIDATES = (1 << 31) - 1      # DESIGN.md R33 (same bound as oracle/topology.py)
+
+
 def er_count(n_in: int, n_out: int, epsilon: float) -> int:
     """M = min(n_in * n_out, floor(eps * (n_in + n_out))): the ER density
     eps(n_in+n_out)/(n_in n_out) of BASELINE.json north_star, capped at 1 (DESIGN reading 1)."""
@@ -173,6 +178,7 @@ def er_layer(n_in: int, n_out: int, epsilon: float, init: str, seed: int, l: int
         return Layer(l, n_in, n_out, row_ptr, col, w, np.zeros(total, F32), True)
     C = M + M // 8 + 1024
     while True:
+        C = min(C, MAX_CANDIDATES)
         m = np.arange(C, dtype=np.uint64)
         x0, x1, x2, x3 = philox.stream(seed, philox.PURPOSE_INIT, 0, l, 0, m)
         i, j = candidate_ij(x0, x1, n_in, n_out)
@@ -180,6 +186,8 @@ def er_layer(n_in: int, n_out: int, epsilon: float, init: str, seed: int, l: int
         _, first = np.unique(pos, return_index=True)      # first occurrence of every distinct pos
         if len(first) >= M:
             break
+        if C >= MAX_CANDIDATES:                           # R33: the stream prefix searched is bounded
+            raise ValueError("could not find enough distinct candidates (layer too saturated)")
         C *= 2
     acc = np.sort(first)[:M]                                # the first M distinct, in stream order
     w_acc = init_values(init, n_in, n_out, x2[acc], x3[acc])
@@ -216,6 +224,18 @@ def create(sizes, epsilon, activation="all_relu", alpha=0.5, dropout=0.0, init="
 # contiguous run of connection products.  No SciPy.
 # --------------------------------------------------------------------------------------
 _CHUNK_ELEMS = 1 << 24
+# Worker threads for the chunk loops (NumPy releases the GIL in its gathers / ufuncs / reduceat);
+# chunks write disjoint output rows, so the result does not depend on the thread count.  The
+# bench's cpu_baseline sets 1.
+THREADS = os.cpu_count() or 1
+_POOL = None
+
+
+def _pool():
+    global _POOL
+    if _POOL is None or _POOL._max_workers != THREADS:
+        _POOL = ThreadPoolExecutor(max_workers=THREADS)
+    return _POOL
 
 
 def _segment_sums(rows_of_terms: np.ndarray, seg_key: np.ndarray, out: np.ndarray) -> None:
@@ -227,16 +247,53 @@ def _segment_sums(rows_of_terms: np.ndarray, seg_key: np.ndarray, out: np.ndarra
     out[seg_key[starts]] += np.add.reduceat(rows_of_terms, starts, axis=0)
 
 
-def _chunks(n: int, B: int):
+def _chunks(n: int, B: int, key: Optional[np.ndarray] = None):
+    """[s0, s1) entry ranges of about _CHUNK_ELEMS / B entries; with a non-decreasing key, every
+    boundary falls between two different keys (no output row is split across chunks)."""
     step = max(1, _CHUNK_ELEMS // max(B, 1))
-    for s0 in range(0, n, step):
-        yield s0, min(n, s0 + step)
+    s0 = 0
+    while s0 < n:
+        s1 = min(n, s0 + step)
+        if key is not None and s1 < n:
+            s1 = int(np.searchsorted(key, key[s1 - 1], side="right"))
+        yield s0, s1
+        s0 = s1
+
+
+def _run_chunks(fn, chunks) -> None:
+    """fn(s0, s1) over the chunks, on THREADS workers (each chunk owns its output rows)."""
+    chunks = list(chunks)
+    if THREADS <= 1 or len(chunks) <= 1:
+        for c in chunks:
+            fn(*c)
+        return
+    for f in [_pool().submit(fn, *c) for c in chunks]:
+        f.result()
 
 
 def column_order(Ly: Layer) -> np.ndarray:
     """Permutation of the canonical entries sorting them by output neuron j (stable: i ascending
     within a column)."""
     return np.argsort(Ly.col, kind="stable")
+
+
+def _spmm_fwd_stack(aT: np.ndarray, ws, Ly: Layer, dtype) -> np.ndarray:
+    """zT [n_out x sum of column blocks]: aT [n_in x K B] holds K stacked column blocks of width B;
+    block k is multiplied by the weights ws[k] (values on the support of W^(l), canonical order)."""
+    K = len(ws)
+    Bk = aT.shape[1] // K
+    order = column_order(Ly)
+    rows, cols = Ly.rows()[order], Ly.col[order].astype(np.int64)
+    wo = [np.asarray(w, dtype)[order] for w in ws]
+    zT = np.zeros((Ly.n_out, aT.shape[1]), dtype=dtype)
+
+    def part(s0, s1):
+        t = aT[rows[s0:s1]].astype(dtype, copy=False)
+        for k in range(K):
+            t[:, k * Bk:(k + 1) * Bk] *= wo[k][s0:s1, None]
+        _segment_sums(t, cols[s0:s1], zT)
+    _run_chunks(part, _chunks(Ly.nnz, aT.shape[1], cols))
+    return zT
 
 
 def spmm_fwd(a: np.ndarray, Ly: Layer, wabs: bool = False, w: Optional[np.ndarray] = None) -> np.ndarray:
@@ -246,30 +303,17 @@ def spmm_fwd(a: np.ndarray, Ly: Layer, wabs: bool = False, w: Optional[np.ndarra
     aT = np.ascontiguousarray((np.abs(a) if wabs else a).astype(F64).T)      # [n_in x B]
     if w is None:
         w = (np.abs(Ly.w) if wabs else Ly.w).astype(F64)
-    order = column_order(Ly)
-    rows, cols = Ly.rows()[order], Ly.col[order].astype(np.int64)
-    zT = np.zeros((Ly.n_out, aT.shape[1]), dtype=F64)
-    for s0, s1 in _chunks(Ly.nnz, aT.shape[1]):
-        _segment_sums(aT[rows[s0:s1]] * w[order[s0:s1], None], cols[s0:s1], zT)
-    return zT.T
+    return _spmm_fwd_stack(aT, [w], Ly, F64).T
 
 
-def spmm_fwd_abs_pair(a1: np.ndarray, w1: np.ndarray, a2: np.ndarray, w2: np.ndarray, Ly: Layer):
-    """(a1 . W1, a2 . W2) on the support of W^(l) for non-negative magnitude operands, in float32
-    (magnitudes are error bounds, R24: relative accuracy ~1e-6 is ample), one pass over
-    the connections for both."""
-    B = a1.shape[0]
-    aT = np.ascontiguousarray(np.concatenate([a1, a2], axis=0).astype(F32).T)     # [n_in x 2B]
-    order = column_order(Ly)
-    rows, cols = Ly.rows()[order], Ly.col[order].astype(np.int64)
-    wa, wb = w1.astype(F32)[order], w2.astype(F32)[order]
-    zT = np.zeros((Ly.n_out, 2 * B), dtype=F32)
-    for s0, s1 in _chunks(Ly.nnz, 2 * B):
-        t = aT[rows[s0:s1]]
-        t[:, :B] *= wa[s0:s1, None]
-        t[:, B:] *= wb[s0:s1, None]
-        _segment_sums(t, cols[s0:s1], zT)
-    return zT[:, :B].T.astype(F64), zT[:, B:].T.astype(F64)
+def spmm_fwd_abs(blocks, Ly: Layer):
+    """[a_k . W_k for (a_k, W_k) in blocks] for non-negative magnitude operands (a_k [B x n_in],
+    W_k values on the support), in float32 -- magnitudes are error bounds (R24), relative
+    accuracy ~1e-6 is ample -- in one pass over the connections."""
+    B = blocks[0][0].shape[0]
+    aT = np.ascontiguousarray(np.concatenate([x for x, _ in blocks], axis=0).astype(F32).T)   # [n_in x K B]
+    zT = _spmm_fwd_stack(aT, [w for _, w in blocks], Ly, F32)
+    return [zT[:, k * B:(k + 1) * B].T.astype(F64) for k in range(len(blocks))]
 
 
 def spmm_bwd(delta: np.ndarray, Ly: Layer, w: Optional[np.ndarray] = None) -> np.ndarray:
@@ -279,9 +323,30 @@ def spmm_bwd(delta: np.ndarray, Ly: Layer, w: Optional[np.ndarray] = None) -> np
     w = Ly.w.astype(F64) if w is None else w
     rows, col = Ly.rows(), Ly.col.astype(np.int64)
     oT = np.zeros((Ly.n_in, dT.shape[1]), dtype=F64)
-    for s0, s1 in _chunks(Ly.nnz, dT.shape[1]):
+
+    def part(s0, s1):
         _segment_sums(dT[col[s0:s1]] * w[s0:s1, None], rows[s0:s1], oT)
+    _run_chunks(part, _chunks(Ly.nnz, dT.shape[1], rows))
     return oT.T
+
+
+def spmm_bwd_abs(blocks, Ly: Layer) -> np.ndarray:
+    """sum over (d_k, W_k) in blocks of d_k . W_k^T, for non-negative magnitude operands, float32
+    (see spmm_fwd_abs), one pass over the connections."""
+    B = blocks[0][0].shape[0]
+    K = len(blocks)
+    dT = np.ascontiguousarray(np.concatenate([d for d, _ in blocks], axis=0).astype(F32).T)   # [n_out x K B]
+    ws = [np.asarray(w, F32) for _, w in blocks]
+    rows, col = Ly.rows(), Ly.col.astype(np.int64)
+    oT = np.zeros((Ly.n_in, K * B), dtype=F32)
+
+    def part(s0, s1):
+        t = dT[col[s0:s1]]
+        for k in range(K):
+            t[:, k * B:(k + 1) * B] *= ws[k][s0:s1, None]
+        _segment_sums(t, rows[s0:s1], oT)
+    _run_chunks(part, _chunks(Ly.nnz, K * B, rows))
+    return sum(oT[:, k * B:(k + 1) * B].T.astype(F64) for k in range(K))
 
 
 def sddmm(a: np.ndarray, delta: np.ndarray, Ly: Layer) -> np.ndarray:
@@ -290,8 +355,10 @@ def sddmm(a: np.ndarray, delta: np.ndarray, Ly: Layer) -> np.ndarray:
     dT = np.ascontiguousarray(delta.astype(F64).T)
     rows, col = Ly.rows(), Ly.col.astype(np.int64)
     g = np.zeros(Ly.nnz, dtype=F64)
-    for s0, s1 in _chunks(Ly.nnz, aT.shape[1]):
+
+    def part(s0, s1):
         g[s0:s1] = (aT[rows[s0:s1]] * dT[col[s0:s1]]).sum(axis=1)
+    _run_chunks(part, _chunks(Ly.nnz, aT.shape[1]))
     return g
 
 
@@ -361,9 +428,9 @@ class Trace:
     pmag: Optional[np.ndarray] = None
 
 
-def _wmag(Ly: Layer) -> np.ndarray:
-    """|w| + the running error magnitude of w: the weights' contribution to a product's bound."""
-    return np.abs(Ly.w).astype(F64) + _m(Ly.wmag, Ly.w)
+# Test instrumentation (the R24 error magnitudes and the R32 kink count) is on by default; the
+# bench's cpu_baseline times the method's own arithmetic with it off (bench.py).
+INSTRUMENT = True
 
 
 def forward(st: State, x: np.ndarray, train: bool = True, step: int = 0, rank: Optional[int] = None) -> Trace:
@@ -373,8 +440,10 @@ def forward(st: State, x: np.ndarray, train: bool = True, step: int = 0, rank: O
     Alongside, the running error magnitudes of R24 (Higham, Accuracy and Stability of Numerical
     Algorithms, 2nd ed., §3.1-3.3: a sum of products computed in fp32 differs from its exact
     value by at most gamma times the same sum of absolute values; errors of the inputs propagate
-    through the absolute values of the weights):
-        zmag_l = (|a_{l-1}| + amag_{l-1}) . (|W^(l)| + wmag) + |b_l| + bmag_l,   amag_1 = 0 (x exact)
+    through the absolute values of what multiplies them; first order in u, so products of two
+    magnitudes are dropped):
+        zmag_l = |a_{l-1}| . |W^(l)| + amag_{l-1} . |W^(l)| + |a_{l-1}| . wmag + |b_l| + bmag_l,
+        amag_1 = 0 (x exact)
         amag_l = zmag_l * max(1, |slope_l|) * keep/(1-r)     (f_l is Lipschitz with that constant)
         pmag   = 2 p max_k zmag_L[:, k]                    (|dp_c| <= p_c (|dz_c| + sum_k p_k |dz_k|))"""
     rank = st.rank if rank is None else rank
@@ -391,10 +460,19 @@ def forward(st: State, x: np.ndarray, train: bool = True, step: int = 0, rank: O
     for l in range(2, L + 1):
         Ly = st.layer(l)
         z = spmm_fwd(a[-1], Ly) + st.b[l - 2].astype(F64)
-        aa = np.abs(a[-1]).astype(F64)
-        mag, zmag = spmm_fwd_abs_pair(aa, np.abs(Ly.w), aa + amags[-1], _wmag(Ly), Ly)
-        mag += np.abs(st.b[l - 2].astype(F64))
-        zmag += np.abs(st.b[l - 2].astype(F64)) + (0.0 if st.bmag is None else st.bmag[l - 2])
+        if INSTRUMENT:
+            aa = np.abs(a[-1]).astype(F64)
+            wa = np.abs(Ly.w)
+            blocks = [(aa, wa)]
+            if np.any(amags[-1]):
+                blocks.append((amags[-1], wa))
+            if Ly.wmag is not None:
+                blocks.append((aa, Ly.wmag))
+            res = spmm_fwd_abs(blocks, Ly)
+            mag = res[0] + np.abs(st.b[l - 2].astype(F64))
+            zmag = sum(res) + np.abs(st.b[l - 2].astype(F64)) + (0.0 if st.bmag is None else st.bmag[l - 2])
+        else:
+            mag = zmag = np.zeros_like(z)
         # pre-activations within fp32 summation error of the All-ReLU kink (hidden layers):
         # there the branch taken by an fp32 kernel may legitimately differ (R32, kink
         # guard).  mag == 0 means every term is an exact zero (e.g. no active binary input and a
@@ -454,11 +532,12 @@ def backward(st: State, tr: Trace, y: np.ndarray) -> Grads:
     only (SDDMM), gb_l = sum_b delta_l, delta_{l-1} = (delta_l W^(l)T) * f'_{l-1}(z_{l-1}) * keep/(1-r)
     for l >= 3.  delta_L = (p - onehot)/B.
 
-    Running error magnitudes (R24), as in `forward`, with f' exact away from the kink (R32):
+    Running error magnitudes (R24), first order as in `forward`, with f' exact away from the kink
+    (R32):
         dmag_L     = pmag / B
-        gmag_ij    = sum_b (|a_{l-1}| + amag_{l-1})[b, i] (|delta_l| + dmag_l)[b, j]
+        gmag_ij    = sum_b [(|a_{l-1}| + amag_{l-1})[b, i] |delta_l|[b, j] + |a_{l-1}|[b, i] dmag_l[b, j]]
         gbmag_j    = sum_b (|delta_l| + dmag_l)[b, j]
-        dmag_{l-1} = ((|delta_l| + dmag_l) . (|W^(l)| + wmag)^T) * |f'_{l-1}| * keep/(1-r)"""
+        dmag_{l-1} = (|delta_l| . (|W^(l)| + wmag)^T + dmag_l . |W^(l)|^T) * |f'_{l-1}| * keep/(1-r)"""
     if tr.version != st.version or not tr.train:
         raise RuntimeError("stale trace")
     L = st.L
@@ -478,14 +557,23 @@ def backward(st: State, tr: Trace, y: np.ndarray) -> Grads:
         Ly = st.layer(l)
         g[l - 2] = sddmm(tr.a[l - 2], delta, Ly).astype(F32)
         gb[l - 2] = delta.astype(F64).sum(axis=0).astype(F32)
-        afull = np.abs(tr.a[l - 2]).astype(F64) + (tr.amag[l - 2] if tr.amag is not None else 0.0)
-        dfull = np.abs(delta).astype(F64) + dmag
-        gmag[l - 2] = sddmm(afull, dfull, Ly)
-        gbmag[l - 2] = dfull.sum(axis=0)
+        dabs = np.abs(delta).astype(F64)
+        if INSTRUMENT:
+            aabs = np.abs(tr.a[l - 2]).astype(F64)
+            am = tr.amag[l - 2] if tr.amag is not None else np.zeros_like(aabs)
+            # stacking along the batch axis sums the two products: sum_b A1 D1 + sum_b A2 D2
+            gmag[l - 2] = sddmm(np.concatenate([aabs + am, aabs]), np.concatenate([dabs, dmag]), Ly)
+        else:
+            gmag[l - 2] = np.zeros(Ly.nnz)
+        gbmag[l - 2] = (dabs + dmag).sum(axis=0)
         if l >= 3:
             fp = activation_grad(tr.z[l - 2], l - 1, st.alpha, st.activation)
             d = spmm_bwd(delta, Ly) * fp
-            dmag = spmm_bwd(dfull, Ly, w=_wmag(Ly)) * np.abs(fp)
+            if INSTRUMENT:
+                wa = np.abs(Ly.w).astype(F64)
+                dmag = spmm_bwd_abs([(dabs, wa + _m(Ly.wmag, wa)), (dmag, wa)], Ly) * np.abs(fp)
+            else:
+                dmag = np.zeros_like(d)
             if tr.keep[l - 2] is not None:
                 d = d * tr.keep[l - 2] * scale
                 dmag = dmag * tr.keep[l - 2] * scale

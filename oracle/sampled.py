@@ -109,12 +109,15 @@ def delta_columns(st: State, tr: Trace, y, need: Dict[int, Iterable[int]]):
         Dn[:, K] = np.stack([deltas[l + 1][k] for k in K], axis=1).astype(F64)
         Tn = np.zeros((B, Ly.n_out), dtype=bool)
         Tn[:, K] = np.stack([tainted[l + 1][k] for k in K], axis=1)
-        Mn = np.zeros((B, Ly.n_out), dtype=F64)  # |delta_{l+1}| + dmag_{l+1} on the cone
-        Mn[:, K] = np.abs(Dn[:, K]) + np.stack([dmags[l + 1][k] for k in K], axis=1)
-        wm = np.abs(Ly.w).astype(F64) + (0.0 if Ly.wmag is None else Ly.wmag)
-        # [B x |J|] = delta_{l+1} W^(l+1)T on the cone, and its magnitude
+        Mn = np.zeros((B, Ly.n_out), dtype=F64)  # dmag_{l+1} on the cone
+        Mn[:, K] = np.stack([dmags[l + 1][k] for k in K], axis=1)
+        wa = np.abs(Ly.w).astype(F64)
+        wm = wa + (0.0 if Ly.wmag is None else Ly.wmag)
+        # [B x |J|] = delta_{l+1} W^(l+1)T on the cone, and its first-order magnitude
+        # |delta| . (|W| + wmag)^T + dmag . |W|^T  (model.backward)
         back = _segment_products(Ly.row_ptr, None, J, np.ascontiguousarray(Dn.T), Ly.col, Ly.w.astype(F64)).T
-        bmag = _segment_products(Ly.row_ptr, None, J, np.ascontiguousarray(Mn.T), Ly.col, wm).T
+        bmag = (_segment_products(Ly.row_ptr, None, J, np.ascontiguousarray(np.abs(Dn).T), Ly.col, wm).T
+                + _segment_products(Ly.row_ptr, None, J, np.ascontiguousarray(Mn.T), Ly.col, wa).T)
         fp = activation_grad(tr.z[l - 1][:, J], l, st.alpha, st.activation)
         d = back * fp
         dm = bmag * np.abs(fp)
@@ -136,15 +139,15 @@ def delta_columns(st: State, tr: Trace, y, need: Dict[int, Iterable[int]]):
 
 def grad_entries(st: State, tr: Trace, deltas, dmags, l: int, entries: np.ndarray):
     """g of the canonical entries `entries` of W^(l): sum_b a_{l-1}[b, i] delta_l[b, j] (fp64 -> f32),
-    and its running error magnitude sum_b (|a| + amag)(|delta| + dmag) (R24)."""
+    and its first-order running error magnitude sum_b (|a| + amag)|delta| + |a| dmag (R24)."""
     Ly = st.layer(l)
     rows = Ly.rows()[entries]
     cols = Ly.col[entries].astype(np.int64)
     a = tr.a[l - 2][:, rows].astype(F64)
     am = np.abs(a) + tr.amag[l - 2][:, rows]
     d = np.stack([deltas[l][int(j)] for j in cols], axis=1).astype(F64)
-    dm = np.abs(d) + np.stack([dmags[l][int(j)] for j in cols], axis=1)
-    return (a * d).sum(axis=0).astype(F32), (am * dm).sum(axis=0)
+    dm = np.stack([dmags[l][int(j)] for j in cols], axis=1)
+    return (a * d).sum(axis=0).astype(F32), (am * np.abs(d) + np.abs(a) * dm).sum(axis=0)
 
 
 def bias_grad_columns(deltas, dmags, l: int, cols: np.ndarray):

@@ -58,6 +58,12 @@ def select_removals(w: np.ndarray, zeta: float) -> Tuple[np.ndarray, int, int]:
     return flags, ks[0], ks[1]
 
 
+# The candidate streams (ER init, regrowth) are searched over at most 2^31 - 1 draws m (DESIGN.md
+# R33, the CUDA path's 32-bit candidate index): fewer than R distinct valid positions in that
+# prefix is an error on both sides.
+MAX_CANDIDATES = (1 << 31) - 1
+
+
 def regrow_candidates(st: State, Ly: Layer, e: int, R: int, pre_keys: np.ndarray):
     """Alg. 2 "Add randomly new weights in the equivalent amount" (DESIGN reading 8):
     the first R distinct candidates of the REGROW stream (c3 = e) that are outside the
@@ -69,6 +75,7 @@ def regrow_candidates(st: State, Ly: Layer, e: int, R: int, pre_keys: np.ndarray
     frac = free / n_pos
     C = int(R / frac * 1.25) + 1024
     while True:
+        C = min(C, MAX_CANDIDATES)
         m = np.arange(C, dtype=np.uint64)
         x0, x1, x2, x3 = philox.stream(st.seed, philox.PURPOSE_REGROW, 0, Ly.l, e, m)
         i, j = candidate_ij(x0, x1, Ly.n_in, Ly.n_out)
@@ -82,6 +89,8 @@ def regrow_candidates(st: State, Ly: Layer, e: int, R: int, pre_keys: np.ndarray
         if len(first) >= R:
             acc = mv[np.sort(first)[:R]]
             return pos[acc], acc, x2[acc], x3[acc]
+        if C >= MAX_CANDIDATES:
+            raise ValueError("could not find enough distinct candidates (layer too saturated)")
         C *= 2
 
 

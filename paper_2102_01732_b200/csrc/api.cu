@@ -359,19 +359,10 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
         h->has_allocator = true;
     }
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
-    if (const char* e = std::getenv("SMLP_MIRROR_SCATTER")) h->mirror_scatter = std::atoi(e) != 0;
-    if (const char* e = std::getenv("SMLP_L2HINT")) h->l2hint = std::atoi(e);
-    if (const char* e = std::getenv("SMLP_L2PERSIST")) h->l2persist = std::atoi(e);
-    if (const char* e = std::getenv("SMLP_FUSED_UPDATE")) h->fused_update = std::atoi(e) != 0;
-    if (const char* e = std::getenv("SMLP_OVERLAP_UPDATE")) h->overlap_update = std::atoi(e) != 0;
-    if (const char* e = std::getenv("SMLP_DEFER_MIRROR")) h->defer_mirror = std::atoi(e) != 0;
-    if (const char* e = std::getenv("SMLP_SHORT_ROWS")) h->short_rows = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_NARROW_SPARSE_BWD")) h->narrow_sparse_bwd = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_SHORT_MAX_FWD")) h->short_max_fwd = std::atoi(e);
     if (const char* e = std::getenv("SMLP_SHORT_MAX_BWD")) h->short_max_bwd = std::atoi(e);
     if (const char* e = std::getenv("SMLP_SHORT_MIN_ROWS")) h->short_min_rows = std::atoll(e);
-    if (const char* e = std::getenv("SMLP_SPLIT_GRAD")) h->split_grad = std::atoi(e) != 0;
-    if (const char* e = std::getenv("SMLP_UPDATE_SCATTER")) h->update_scatter = std::atoi(e) != 0;
     const int rc = build_handle(h, cfg);
     if (rc != SMLP_OK) {
         g_create_error = h->err;
@@ -383,7 +374,6 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
 }
 
 int sparse_mlp_destroy(smlp_handle* h) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!h) return SMLP_OK;
     cudaStreamSynchronize(h->stream);
     for (auto& r : h->prof_recs) {
@@ -408,8 +398,6 @@ int sparse_mlp_destroy(smlp_handle* h) {
         cudaStreamDestroy(h->aux_stream);
     }
     for (auto e : h->aux_ev)
-        if (e) cudaEventDestroy(e);
-    for (auto e : h->mirror_ev)
         if (e) cudaEventDestroy(e);
     cudaStreamSynchronize(h->stream);
     delete h;
@@ -455,7 +443,6 @@ int sparse_mlp_profile_read(smlp_handle* h, smlp_kernel_stat* out, int32_t cap, 
 }
 
 int sparse_mlp_params_updated(smlp_handle* h) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!h) return SMLP_E_ARG;
     for (auto& Ly : h->layers) SMLP_TRY(refresh_mirror_values(h, Ly));
     return SMLP_OK;
@@ -469,8 +456,6 @@ int sparse_mlp_set_step_counter(smlp_handle* h, const uint64_t* dev_counter) {
 
 int sparse_mlp_set_stream(smlp_handle* h, void* stream) {
     if (!h) return SMLP_E_ARG;
-    // deferred mirror refreshes join the stream they were left on before it is replaced
-    if (h->stream != (cudaStream_t)stream) SMLP_TRY(join_mirrors(h));
     h->stream = (cudaStream_t)stream;
     return SMLP_OK;
 }
@@ -486,28 +471,21 @@ int sparse_mlp_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int
 
 int sparse_mlp_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss,
                         const smlp_sgd* fused) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!h) return SMLP_E_ARG;
     if (!labels) return set_err(h, SMLP_E_ARG, "labels is NULL");
     if (!h->trace_valid || !h->trace_train || h->trace_version != h->version)
         return set_err(h, SMLP_E_STALE, "backward needs a train-mode forward on the current topology version");
     int rc;
-    if (fused && !h->fused_update) {
+    if (fused) {
         // measured faster than applying Eq. 1 inside the last chunk's backward: the
-        // backward only accumulates the gradient, then one streaming Eq. 1 pass over the whole
-        // view (grad_scale 1) and the mirror refresh
+        // backward only accumulates the gradient (the last chunk of a large model into grad2),
+        // then one streaming Eq. 1 pass over the whole view (grad_scale 1) and the mirror refresh
         smlp_sgd f = *fused;
         f.grad_scale = 1.f;
-        if (h->overlap_update) {
-            // each layer's Eq. 1 slice + mirror refresh start on the aux stream as soon as its
-            // gradient is final, overlapping the rest of the backward; the biases and the join last
-            rc = run_backward(h, labels, y_idx, loss, nullptr, &f, h->split_grad);
-        } else {
-            rc = run_backward(h, labels, y_idx, loss, nullptr, nullptr, h->split_grad);
-            if (rc == SMLP_OK) rc = run_step(h, &f);
-        }
+        rc = run_backward(h, labels, y_idx, loss, true);
+        if (rc == SMLP_OK) rc = run_step(h, &f);
     } else {
-        rc = run_backward(h, labels, y_idx, loss, fused);
+        rc = run_backward(h, labels, y_idx, loss, false);
     }
     if (rc == SMLP_OK) {
         h->grads_pending = fused == nullptr;
@@ -517,7 +495,6 @@ int sparse_mlp_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_
 }
 
 int sparse_mlp_step(smlp_handle* h, const smlp_sgd* sgd) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!h || !sgd) return SMLP_E_ARG;
     if (!h->grads_pending) return set_err(h, SMLP_E_STATE, "step without pending gradients");
     const int rc = run_step(h, sgd);
@@ -574,12 +551,11 @@ int sparse_mlp_train_step_host_async(smlp_handle* h, const float* x_host, const 
 }
 
 int sparse_mlp_join(smlp_handle* h) {
-    if (!h) return SMLP_E_ARG;
-    return join_mirrors(h);
+    // every call joins its side-stream work (mirror refreshes) before returning: nothing pending
+    return h ? SMLP_OK : SMLP_E_ARG;
 }
 
 int sparse_mlp_sync(smlp_handle* h) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!h) return SMLP_E_ARG;
     SMLP_CK(h, cudaStreamSynchronize(h->stream));
     return check_data_flag(h);
@@ -604,7 +580,6 @@ int sparse_mlp_view_layout(smlp_handle* h, int64_t* val_off, int64_t* cap, int64
 }
 
 int sparse_mlp_grad_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!h) return SMLP_E_ARG;
     if (dev) *dev = h->grad;
     if (count) *count = h->param_count;
@@ -613,7 +588,6 @@ int sparse_mlp_grad_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* 
 }
 
 int sparse_mlp_param_view(smlp_handle* h, float** dev, int64_t* count, uint64_t* version) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!h) return SMLP_E_ARG;
     if (dev) *dev = h->param;
     if (count) *count = h->param_count;
@@ -622,7 +596,6 @@ int sparse_mlp_param_view(smlp_handle* h, float** dev, int64_t* count, uint64_t*
 }
 
 int sparse_mlp_evolve_topology(smlp_handle* h, double zeta, uint64_t evolve_idx, int64_t* removed_per_layer) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!h) return SMLP_E_ARG;
     if (!(zeta > 0.0 && zeta < 1.0)) return set_err(h, SMLP_E_ARG, "zeta must be in (0, 1)");
     SMLP_TRY(check_data_flag(h));
@@ -631,7 +604,6 @@ int sparse_mlp_evolve_topology(smlp_handle* h, double zeta, uint64_t evolve_idx,
 
 int sparse_mlp_prune_neurons(smlp_handle* h, double percentile, int32_t flags, int64_t* pruned_per_layer,
                              int64_t* removed_conn) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!h) return SMLP_E_ARG;
     if (!(percentile >= 0.0 && percentile < 100.0)) return set_err(h, SMLP_E_ARG, "percentile must be in [0, 100)");
     SMLP_TRY(check_data_flag(h));
@@ -639,7 +611,6 @@ int sparse_mlp_prune_neurons(smlp_handle* h, double percentile, int32_t flags, i
 }
 
 int sparse_mlp_importance(smlp_handle* h, int32_t l, double* out, int32_t to_host) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!valid_layer(h, l, 2) || l == h->L) return h ? set_err(h, SMLP_E_SHAPE, "importance: hidden layer 2..L-1") : SMLP_E_ARG;
     if (!out) return set_err(h, SMLP_E_ARG, "out is NULL");
     const size_t n = (size_t)h->sizes[l - 1];
@@ -684,7 +655,6 @@ int sparse_mlp_info(smlp_handle* h, smlp_info* info) {
 
 int sparse_mlp_export_layer(smlp_handle* h, int32_t l, int32_t* row_ptr, int32_t* col_idx, float* val, float* mom,
                             int32_t to_host) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!valid_layer(h, l, 2)) return h ? set_err(h, SMLP_E_SHAPE, "export_layer: l must be in 2..L") : SMLP_E_ARG;
     const Layer& Ly = h->layers[(size_t)(l - 2)];
     const cudaMemcpyKind k = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
@@ -699,7 +669,6 @@ int sparse_mlp_export_layer(smlp_handle* h, int32_t l, int32_t* row_ptr, int32_t
 
 int sparse_mlp_import_layer(smlp_handle* h, int32_t l, int64_t nnz, const int32_t* row_ptr, const int32_t* col_idx,
                             const float* val, const float* mom) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!valid_layer(h, l, 2)) return h ? set_err(h, SMLP_E_SHAPE, "import_layer: l must be in 2..L") : SMLP_E_ARG;
     Layer& Ly = h->layers[(size_t)(l - 2)];
     if (!row_ptr || (nnz > 0 && (!col_idx || !val))) return set_err(h, SMLP_E_ARG, "import_layer: NULL array");
@@ -734,7 +703,6 @@ int sparse_mlp_import_layer(smlp_handle* h, int32_t l, int64_t nnz, const int32_
 }
 
 int sparse_mlp_export_bias(smlp_handle* h, int32_t l, float* bias, float* bias_mom) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!valid_layer(h, l, 2)) return h ? set_err(h, SMLP_E_SHAPE, "export_bias: l must be in 2..L") : SMLP_E_ARG;
     const Layer& Ly = h->layers[(size_t)(l - 2)];
     const size_t n = (size_t)Ly.n_out;
@@ -745,7 +713,6 @@ int sparse_mlp_export_bias(smlp_handle* h, int32_t l, float* bias, float* bias_m
 }
 
 int sparse_mlp_import_bias(smlp_handle* h, int32_t l, const float* bias, const float* bias_mom) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!valid_layer(h, l, 2)) return h ? set_err(h, SMLP_E_SHAPE, "import_bias: l must be in 2..L") : SMLP_E_ARG;
     const Layer& Ly = h->layers[(size_t)(l - 2)];
     const size_t n = (size_t)Ly.n_out;
@@ -756,7 +723,6 @@ int sparse_mlp_import_bias(smlp_handle* h, int32_t l, const float* bias, const f
 }
 
 int sparse_mlp_export_alive(smlp_handle* h, int32_t l, uint8_t* alive) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!valid_layer(h, l, 1) || !alive) return h ? set_err(h, SMLP_E_SHAPE, "export_alive: bad layer") : SMLP_E_ARG;
     SMLP_CK(h, cudaMemcpyAsync(alive, h->alive[l], (size_t)h->sizes[l - 1], cudaMemcpyDeviceToHost, h->stream));
     SMLP_CK(h, cudaStreamSynchronize(h->stream));
@@ -764,7 +730,6 @@ int sparse_mlp_export_alive(smlp_handle* h, int32_t l, uint8_t* alive) {
 }
 
 int sparse_mlp_import_alive(smlp_handle* h, int32_t l, const uint8_t* alive) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!valid_layer(h, l, 1) || !alive) return h ? set_err(h, SMLP_E_SHAPE, "import_alive: bad layer") : SMLP_E_ARG;
     const size_t n = (size_t)h->sizes[l - 1];
     std::vector<uint8_t> a(alive, alive + n);
@@ -782,7 +747,6 @@ int sparse_mlp_import_alive(smlp_handle* h, int32_t l, const uint8_t* alive) {
 }
 
 int sparse_mlp_export_trace(smlp_handle* h, int32_t kind, int32_t l, float* out) {
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!h || !out) return SMLP_E_ARG;
     if (kind == 0 || kind == 1) {
         const int CB = kind == 0 ? h->CBf : h->CB;   // act: forward layout, delta: backward layout

@@ -56,7 +56,6 @@ __global__ void __launch_bounds__(32) gf_final_kernel(const double* __restrict__
 }  // namespace smlp
 
 int sparse_mlp_gradient_flow(smlp_handle* h, double* out_host) {
-    if (h) SMLP_TRY(smlp::join_mirrors(h));   // deferred mirror refreshes (run_step)
     using namespace smlp;
     if (!h || !out_host) return SMLP_E_ARG;
     if (!h->grads_pending) return set_err(h, SMLP_E_STATE, "gradient_flow needs the gradient of an unfused backward");

@@ -151,8 +151,6 @@ struct smlp_handle {
     cudaStream_t copy_stream = nullptr;        // H2D of the next host batch, overlapping the current step
     cudaStream_t aux_stream = nullptr;         // mirror refreshes overlapping the Eq. 1 pass (run_step)
     cudaEvent_t aux_ev[2] = {nullptr, nullptr};
-    cudaEvent_t mirror_ev[SMLP_MAX_LAYERS + 1] = {nullptr};   // deferred mirror refresh of layer l (aux stream)
-    bool mirror_pending[SMLP_MAX_LAYERS + 1] = {false};
     cudaEvent_t ev_copied[2] = {nullptr, nullptr};
     cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
     int stage_idx = 0;
@@ -172,26 +170,12 @@ struct smlp_handle {
     std::vector<smlp::ProfRec> prof_recs;
     std::vector<cudaEvent_t> ev_pool;
     int num_sms = 148;
-    // tuning knobs (env, read at create; DESIGN.md §5 has the measurements)
-    int mirror_scatter = 0;         // SMLP_MIRROR_SCATTER: the in-backward Eq. 1 also scatters w into mval
-    int l2hint = 1;                 // SMLP_L2HINT: L2 eviction policies in the row kernels (on: +0.4%)
-    int l2persist = 0;              // SMLP_L2PERSIST (percent): persisting-L2 window on the gathered slabs
-    int fused_update = 0;           // SMLP_FUSED_UPDATE: Eq. 1 inside the last chunk's backward
-    int update_scatter = 0;         // SMLP_UPDATE_SCATTER: the Eq. 1 pass scatters w into mval (no mirror gather)
-    int split_grad = 1;             // SMLP_SPLIT_GRAD: fused path, last chunk's gradient to grad2 (no re-read)
+    // tuning knobs (env, read at create; each selects between kernels the parity tests cover)
     int narrow_sparse_bwd = 0;      // SMLP_NARROW_SPARSE_BWD: narrow row-streaming backward also for a sparse output layer
     int64_t short_min_rows = -1;    // SMLP_SHORT_MIN_ROWS: -1 = one 32-row unit per resident warp
     int short_max_fwd = 16;         // SMLP_SHORT_MAX_FWD / _BWD: average entries per row below which the
     int short_max_bwd = 8;          //   streaming kernels run (T2/T3 at ~10: forward -5%, backward +80%)
-    int short_rows = 1;             // SMLP_SHORT_ROWS: row-streaming forward for 128-column layers of < 8 entries per row
-    bool input_binary = false;      // SMLP_INPUT_BINARY: layer 2 only through the bit path
-    int defer_mirror = 0;           // SMLP_DEFER_MIRROR: join each layer's mirror refresh at its next use
-                                    // (C5: neutral, 5.82 vs 5.82 ms -- the overlapped forward slows by
-                                    // what the update region saves; off)
-    int overlap_update = 0;         // SMLP_OVERLAP_UPDATE: each layer's Eq. 1 pass + mirror refresh on the
-                                    // aux stream as soon as its gradient is final (overlaps the backward;
-                                    // C5: 6.040 -> 6.025 ms, the backward kernels slow down by what the
-                                    // update saves -- all of it is memory-bound)
+    bool input_binary = false;      // SMLP_INPUT_BINARY: inputs promised {0,1}; a broken promise is reported
     int64_t launches = 0;
     std::string err;
 };
@@ -312,11 +296,10 @@ int launch_grid(const smlp_handle* h, int64_t items, int threads);
 // step.cu
 int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, bool train,
                 uint64_t step, float* probs);
-int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss,
-                 const smlp_sgd* fused, const smlp_sgd* overlap_sgd = nullptr, bool split_last = false);
+// the gradient of the current trace into the grad view (split_last: a large model's last chunk
+// into grad2, added by the Eq. 1 pass that follows in the same call)
+int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, bool split_last);
 int run_step(smlp_handle* h, const smlp_sgd* sgd);
-int join_mirror(smlp_handle* h, int l);
-int join_mirrors(smlp_handle* h);   // every API call but forward runs this first (deferred mirror refreshes)
 int refresh_mirror_values(smlp_handle* h, Layer& Ly);
 
 // evolve.cu / prune.cu

@@ -14,7 +14,7 @@
 //                  gathered delta_l[j] it accumulates delta_{l-1}[i] += w_ij delta_l[j] (SpMM against
 //                  W^T) and the lane's partial of <a_{l-1}[i], delta_l[j]> (SDDMM), reduced per entry
 //                  in a fixed order through shared memory; the gradient accumulates over chunks in the
-//                  grad view (or, with SMLP_FUSED_UPDATE, Eq. 1 is applied on the last chunk)
+//                  grad view; the Eq. 1 pass (sgd_update4) follows in the same API call
 //   bits kernels   W^(2) when every input is 0 or 1: bit-packed input, exact sums of w / of delta
 //   narrow kernels output layers with n_L <= 32: streamed canonical rows instead of gathers
 //   bwd_finish     multi-segment rows: fixed-order sum of the delta partials + epilogue
@@ -681,13 +681,7 @@ __global__ void __launch_bounds__(512) softmax_ce_kernel(SoftmaxArgs A) {
             const float* dc = A.delta + ((int64_t)c * A.nL + j) * A.CB;
             for (int lb = 0; lb < A.CB; ++lb) g += dc[lb];
         }
-        if (A.fused) {
-            const float v = A.mu * A.bias_mom[j] - A.lr * g;
-            A.bias_mom[j] = v;
-            A.bias[j] = A.bias[j] + v;
-        } else {
-            A.bias_grad[j] = g;
-        }
+        A.bias_grad[j] = g;
     }
 }
 
@@ -793,15 +787,8 @@ __device__ __forceinline__ void bwd_epilogue(const BwdArgs& A, int64_t i, float4
     if (own && q == 0) {
         float tot = s;
         if (!A.first) tot += A.bgs[i];
-        if (!A.last) {
-            A.bgs[i] = tot;
-        } else if (A.fused) {
-            const float v = A.mu * A.bias_mom_prev[i] - A.lr * tot;
-            A.bias_mom_prev[i] = v;
-            A.bias_prev[i] = A.bias_prev[i] + v;
-        } else {
-            A.bias_grad_prev[i] = tot;
-        }
+        if (!A.last) A.bgs[i] = tot;
+        else A.bias_grad_prev[i] = tot;
     }
 }
 
@@ -832,24 +819,18 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
 // gradient of layer l-1 (a fixed 32-lane butterfly, then accumulated over chunks in order)
 struct BwdSide {            // per-row operands of the backward epilogue (loaded before the gathers)
     uint4 zb, kb;           // sign / keep bits of layer l-1, row i
-    float bgs, bmom, bval;  // lane 0: bias-grad accumulator, bias momentum and bias of neuron i
+    float bgs;              // lane 0: bias-grad accumulator of neuron i
 };
 template <bool DROP>
 __device__ __forceinline__ BwdSide bwd_side(const BwdArgs& A, int64_t i, int64_t moff, bool valid, int lane) {
     BwdSide t;
     t.zb = make_uint4(0, 0, 0, 0);
     t.kb = make_uint4(FULL, FULL, FULL, FULL);
-    t.bgs = t.bmom = t.bval = 0.f;
+    t.bgs = 0.f;
     if (!valid) return t;
     t.zb = A.zmask_prev[moff + i];
     if (DROP) t.kb = A.kmask_prev[moff + i];
-    if (lane == 0) {
-        if (!A.first) t.bgs = A.bgs[i];
-        if (A.last && A.fused) {
-            t.bmom = A.bias_mom_prev[i];
-            t.bval = A.bias_prev[i];
-        }
-    }
+    if (lane == 0 && !A.first) t.bgs = A.bgs[i];
     return t;
 }
 
@@ -918,15 +899,8 @@ __device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, c
     if (lane == 0) {
         float tot = s;
         if (!A.first) tot += sd.bgs;
-        if (!A.last) {
-            A.bgs[i] = tot;
-        } else if (A.fused) {
-            const float v = A.mu * sd.bmom - A.lr * tot;
-            A.bias_mom_prev[i] = v;
-            A.bias_prev[i] = sd.bval + v;
-        } else {
-            A.bias_grad_prev[i] = tot;
-        }
+        if (!A.last) A.bgs[i] = tot;
+        else A.bias_grad_prev[i] = tot;
     }
 }
 
@@ -946,7 +920,9 @@ __device__ __forceinline__ void bwd_slots(const float* __restrict__ d_out, const
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
         if (HAS_DPREV) fma4p(dacc, wv[u], dx[u]);
+#if !SMLP_EXP_NO_SDDMM
         red[(u * P + g) * S + q] = dot4p(ai, dx[u]);     // entry u P + g of this batch: lane-q partial
+#endif
     }
 }
 
@@ -962,9 +938,8 @@ __device__ __forceinline__ void bwd_batch(const float* __restrict__ d_out, const
     }
 }
 
-// GOLD: add the gradient accumulated by earlier chunks; UPD: last chunk of the fused path (Eq. 1
-// on (w, v) in place); DROP: dropout on layer l-1
-template <int CB, int CBF, bool HAS_DPREV, bool GOLD, bool UPD, bool DROP>
+// GOLD: add the gradient accumulated by earlier chunks; DROP: dropout on layer l-1
+template <int CB, int CBF, bool HAS_DPREV, bool GOLD, bool DROP>
 __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     using C = RowCfg<CB>;
     constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB, S = C::S, NR = C::NR;
@@ -1001,17 +976,15 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     for (int64_t s = s_lo; s < s_hi; ++s) {
         const int4 nn = s + 2 < s_hi ? A.seg[s + 2] : none;
         prefetch(nxt, buf ^ 1);
-        // operands consumed after the gathers: the lane's entries' weight / gradient / momentum,
-        // and the row's epilogue side data
+        // operands consumed after the gathers: the lane's entries' earlier-chunk gradient, and the
+        // row's epilogue side data
         const int n = cur.z - cur.y;
-        float w[NW], gold[NW], mold[NW];
+        float gold[NW];
 #pragma unroll
         for (int r = 0; r < NW; ++r) {
             const int k = cur.y + lane + 32 * r;
             const bool ok = lane + 32 * r < n;
-            w[r] = UPD && ok ? ld_hint(A.val + k, ps) : 0.f;
             gold[r] = GOLD && ok ? ld_hint(A.grad + k, ps) : 0.f;
-            mold[r] = UPD && ok ? ld_hint(A.mom + k, ps) : 0.f;
         }
         const BwdSide sd = bwd_side<DROP>(A, cur.x, fp.moff, HAS_DPREV && cur.w < 0, lane);
         cp_async_wait1();
@@ -1033,6 +1006,7 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
                                                  dacc, pg);
                 __syncwarp();
                 // window entry e = lane + 32 r of this round: fixed-order sum of its G lane partials
+#if !SMLP_EXP_NO_SDDMM
 #pragma unroll
                 for (int r = 0; r < NW; ++r) {
                     const int e = lane + 32 * r - b0 * EB;
@@ -1055,31 +1029,25 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
                         gsum[r] = t;
                     }
                 }
+#endif
                 __syncwarp();
             }
         }
-        // gradient accumulation / Eq. 1 on the lane's own entries (coalesced)
+        // gradient accumulation on the lane's own entries (coalesced)
 #pragma unroll
         for (int r = 0; r < NW; ++r) {
             const int e = lane + 32 * r;
-            if (e < n) {
-                const int k = cur.y + e;
-                const float gk = gsum[r] + gold[r];
-                if (!UPD) {
-                    st_hint(A.grad + k, gk, ps);
-                } else {
-                    const float v = A.mu * mold[r] - A.lr * (gk + A.wd * w[r]);
-                    st_hint(A.mom + k, v, ps);
-                    st_hint(A.val + k, w[r] + v, ps);
-                    if (A.mval_scatter) A.mval[__ldg(A.minv + k)] = w[r] + v;   // the forward's mirror copy
-                }
-            }
+            if (e < n) st_hint(A.grad + cur.y + e, gsum[r] + gold[r], ps);
         }
         if (HAS_DPREV) {
             if (cur.w < 0) {
                 float d[NR];
                 group_reduce_scatter<CB>(dacc, g, d);
+#if !SMLP_EXP_NO_EPI
                 bwd_rows_epilogue<CB>(A, cur.x, d, sd, fp.off >> 2, lane);
+#else
+                if (lane == 0 && d[0] == 12345.f) A.d_prev[cur.x] = 0.f;
+#endif
             } else {
                 dacc = group_allreduce<G>(dacc);
                 if (g == 0) st4(A.ws + (int64_t)cur.w * CB + q * 4, dacc);
@@ -1347,13 +1315,7 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_kernel(NarrowArg
             if (cj[r] >= 0) {             // lane owns entry k = beg + lane: accumulate / apply Eq. 1
                 const int64_t k = beg[r] + lane;
                 const float gk = gmine + gacc[r];
-                if (!A.last || !A.fused) {
-                    A.grad[k] = gk;
-                } else {
-                    const float vk = A.mu * A.mom[k] - A.lr * (gk + A.wd * w[r]);
-                    A.mom[k] = vk;
-                    A.val[k] = w[r] + vk;
-                }
+                A.grad[k] = gk;
             }
             if (A.d_prev) {
                 float o[VEC];
@@ -1373,15 +1335,8 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_kernel(NarrowArg
                 if (lane == 0) {
                     float tot = bsum;
                     if (!A.first) tot += A.bgs[i];
-                    if (!A.last) {
-                        A.bgs[i] = tot;
-                    } else if (A.fused) {
-                        const float vb = A.mu * A.bias_mom_prev[i] - A.lr * tot;
-                        A.bias_mom_prev[i] = vb;
-                        A.bias_prev[i] = A.bias_prev[i] + vb;
-                    } else {
-                        A.bias_grad_prev[i] = tot;
-                    }
+                    if (!A.last) A.bgs[i] = tot;
+                    else A.bias_grad_prev[i] = tot;
                 }
             }
         }
@@ -1484,27 +1439,14 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_rows_kernel(Narr
             if (jj < len) {
                 const int64_t k = beg + jj;
                 const float gk = g[jj] + gacc[jj];
-                if (!A.last || !A.fused) {
-                    st_f32(A.grad + k, gk, pol_s);
-                } else {
-                    const float vk = A.mu * ldrw_f32(A.mom + k, pol_s) - A.lr * (gk + A.wd * w[jj]);
-                    st_f32(A.mom + k, vk, pol_s);
-                    st_f32(A.val + k, w[jj] + vk, pol_s);
-                }
+                st_f32(A.grad + k, gk, pol_s);
             }
         }
         if (A.d_prev) {                           // bias gradient of layer L-1, accumulated over chunks
             float tot = bsum;
             if (!A.first) tot += A.bgs[i];
-            if (!A.last) {
-                A.bgs[i] = tot;
-            } else if (A.fused) {
-                const float vb = A.mu * A.bias_mom_prev[i] - A.lr * tot;
-                A.bias_mom_prev[i] = vb;
-                A.bias_prev[i] = A.bias_prev[i] + vb;
-            } else {
-                A.bias_grad_prev[i] = tot;
-            }
+            if (!A.last) A.bgs[i] = tot;
+            else A.bias_grad_prev[i] = tot;
         }
     }
 }
@@ -1740,26 +1682,15 @@ __global__ void __launch_bounds__(256) bwd_bits_rows_kernel(BitsArgs A) {
     }
 }
 
-// W^(2) gradient from mirror order to the canonical order (a gather; a scatter would cost a
-// sector read-fill): fused -> Eq. 1 on (w, v) in place, unfused -> the grad view
+// W^(2) gradient from mirror order to the canonical order of the grad view (a gather; a scatter
+// would cost a sector read-fill)
 __global__ void grad_from_mirror_kernel(const int32_t* __restrict__ nonbinary, const float* __restrict__ gm,
-                                        const int32_t* __restrict__ minv, float* __restrict__ w,
-                                        float* __restrict__ v, float* __restrict__ grad,
-                                        const LayerMeta* __restrict__ meta, int fused, float lr, float mu,
-                                        float wd) {
+                                        const int32_t* __restrict__ minv, float* __restrict__ grad,
+                                        const LayerMeta* __restrict__ meta) {
     if (*nonbinary) return;
     const int64_t n = meta->nnz;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const float gk = __ldg(gm + __ldg(minv + k));
-        if (!fused) {
-            grad[k] = gk;
-            continue;
-        }
-        const float wk = w[k];
-        const float vk = mu * v[k] - lr * (gk + wd * wk);
-        v[k] = vk;
-        w[k] = wk + vk;
-    }
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        grad[k] = __ldg(gm + __ldg(minv + k));
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1768,26 +1699,14 @@ __global__ void grad_from_mirror_kernel(const int32_t* __restrict__ nonbinary, c
 // Eq. 1 over one parameter slice (lam = weight decay, 0 for biases), 4 parameters per thread and
 // two float4 groups in flight per iteration.  g and v are streamed once (evict_first); w is kept
 // (evict_last): the mirror gather of the same layer reads it right after.
-// SCATTER: also write each updated w into its mirror slot mval[minv[k]] (k < the layer's device
-// nnz), replacing the separate mirror gather
-template <bool SCATTER, bool G2>
+// G2: the fused path's split last-chunk gradient is in g2 (the update adds g2 + g)
+template <bool G2>
 __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w, float* __restrict__ v,
                                                           const float* __restrict__ g, const float* __restrict__ g2,
                                                           int64_t n, float lr,
-                                                          float mu, float wd, int64_t decay_end, float gs,
-                                                          const int32_t* __restrict__ minv, float* __restrict__ mval,
-                                                          const LayerMeta* __restrict__ meta) {
+                                                          float mu, float wd, int64_t decay_end, float gs) {
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     const int64_t n4 = n >> 2;
-    const int64_t nnz = SCATTER ? meta->nnz : 0;
-    auto scatter = [&](int64_t k4, const float4& wn) {   // parameters 4 k4 .. 4 k4 + 3
-        if (!SCATTER || 4 * k4 >= nnz) return;
-        const int4 m = ldi4_hint(minv + 4 * k4, pf);
-        mval[m.x] = wn.x;
-        if (4 * k4 + 1 < nnz) mval[m.y] = wn.y;
-        if (4 * k4 + 2 < nnz) mval[m.z] = wn.z;
-        if (4 * k4 + 3 < nnz) mval[m.w] = wn.w;
-    };
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
     // weight decay on [0, decay_end) (the weight slices), none on the biases after it; decay_end
     // is a multiple of 32, so a float4 group never straddles it
@@ -1822,8 +1741,6 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
         st4_hint(w + 4 * k, wa, pl);
         st4_hint(v + 4 * k2, b, pf);
         st4_hint(w + 4 * k2, wb, pl);
-        scatter(k, wa);
-        scatter(k2, wb);
     }
     if (k < n4) {
         const float4 w0 = ld4_hint(w + 4 * k, pl), v0 = ld4_hint(v + 4 * k, pf), g0 = gload(k);
@@ -1831,7 +1748,6 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
         const float4 wa = make_float4(w0.x + a.x, w0.y + a.y, w0.z + a.z, w0.w + a.w);
         st4_hint(v + 4 * k, a, pf);
         st4_hint(w + 4 * k, wa, pl);
-        scatter(k, wa);
     }
     if (tid < n - 4 * n4) {   // tail (n % 4 parameters)
         const int64_t t = 4 * n4 + tid;
@@ -1840,7 +1756,6 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
         const float wk = w[t], vk = mu * v[t] - lr * (gs * gt + lam * wk);
         v[t] = vk;
         w[t] = wk + vk;
-        if (SCATTER && t < nnz) mval[minv[t]] = wk + vk;
     }
 }
 
@@ -1900,15 +1815,11 @@ __global__ void __launch_bounds__(256, 4) bwd_short_rows_kernel(BwdArgs A) {
         if (lane < GU) rec[32 + lane] = make_int4(A.zero_row, 0, (int)i0, 0);   // padding: zero delta row
         // the unit's rows' epilogue side data, lane t = row t (loaded once, shuffled at the finish)
         uint4 zb_l = make_uint4(0, 0, 0, 0), kb_l = make_uint4(FULL, FULL, FULL, FULL);
-        float bgs_l = 0.f, bmom_l = 0.f, bval_l = 0.f;
+        float bgs_l = 0.f;
         if (HAS_DPREV && lane < nrows) {
             zb_l = A.zmask_prev[i0 + lane];
             if (DROP) kb_l = A.kmask_prev[i0 + lane];
             if (!A.first) bgs_l = A.bgs[i0 + lane];
-            if (A.last && A.fused) {
-                bmom_l = A.bias_mom_prev[i0 + lane];
-                bval_l = A.bias_prev[i0 + lane];
-            }
         }
         int row = 0;
         int row_end = nrows > 1 ? __shfl_sync(FULL, rp_l, 1) : E1;
@@ -1923,8 +1834,6 @@ __global__ void __launch_bounds__(256, 4) bwd_short_rows_kernel(BwdArgs A) {
                                               __shfl_sync(FULL, kb_l.z, row), __shfl_sync(FULL, kb_l.w, row))
                                  : make_uint4(FULL, FULL, FULL, FULL);
                     sd.bgs = __shfl_sync(FULL, bgs_l, row);
-                    sd.bmom = __shfl_sync(FULL, bmom_l, row);
-                    sd.bval = __shfl_sync(FULL, bval_l, row);
                     const float d[NR] = {dacc.x, dacc.y, dacc.z, dacc.w};
                     bwd_rows_epilogue<CB>(A, i0 + row, d, sd, lane, lane);
                 }
@@ -2018,7 +1927,7 @@ int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
     if constexpr (CB == 128) {
         // layers of short rows (< 16 entries per mirror row on average): stream whole rows
         // (and enough 32-row units to give every resident warp one: a narrow layer keeps the row kernel)
-        if (h->short_rows && L.nnz < (int64_t)h->short_max_fwd * L.n_out &&
+        if (L.nnz < (int64_t)h->short_max_fwd * L.n_out &&
             L.n_out >= short_min_rows(h)) {
             const int64_t units = (L.n_out + SHORT_ROWS - 1) / SHORT_ROWS;
             fwd_short_rows_kernel<<<rows_grid(h, fwd_short_rows_kernel, units), WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
@@ -2039,10 +1948,10 @@ int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
 template <int CB, int CBF>
 int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev) {
     constexpr int P = 32 / (CB / 4);
-    const bool gold = !A.first && !A.no_gold, upd = A.last && A.fused, drop = A.dropout_prev != 0;
+    const bool gold = !A.first && !A.no_gold, drop = A.dropout_prev != 0;
     if constexpr (CB == 128 && CBF == 128) {
         // layers of short canonical rows (< 8 entries on average): stream whole rows
-        if (h->short_rows && !upd && L.nnz < (int64_t)h->short_max_bwd * L.n_in &&
+        if (L.nnz < (int64_t)h->short_max_bwd * L.n_in &&
             L.n_in >= short_min_rows(h)) {
             const int64_t units = (L.n_in + SHORT_ROWS - 1) / SHORT_ROWS;
 #define SMLP_BWD_SHORT(HD, GO, DR)                                                                          \
@@ -2061,25 +1970,19 @@ int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev)
 #undef SMLP_BWD_SHORT
         }
     }
-    const int mode = (has_dprev ? 8 : 0) | (gold ? 4 : 0) | (upd ? 2 : 0) | (drop ? 1 : 0);
-#define SMLP_BWD_ROWS(HD, GO, UP, DR)                                                                          \
-case (HD ? 8 : 0) | (GO ? 4 : 0) | (UP ? 2 : 0) | (DR ? 1 : 0):                                         \
-    bwd_rows_kernel<CB, CBF, HD, GO, UP, DR><<<rows_grid(h, bwd_rows_kernel<CB, CBF, HD, GO, UP, DR>, L.bseg_cap), \
-                                          WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);                      \
+    const int mode = (has_dprev ? 4 : 0) | (gold ? 2 : 0) | (drop ? 1 : 0);
+#define SMLP_BWD_ROWS(HD, GO, DR)                                                                             \
+case (HD ? 4 : 0) | (GO ? 2 : 0) | (DR ? 1 : 0):                                                            \
+    bwd_rows_kernel<CB, CBF, HD, GO, DR><<<rows_grid(h, bwd_rows_kernel<CB, CBF, HD, GO, DR>, L.bseg_cap),      \
+                                       WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);                          \
     break;
     switch (mode) {
-        SMLP_BWD_ROWS(true, false, false, false)
-        SMLP_BWD_ROWS(true, false, false, true)
-        SMLP_BWD_ROWS(true, false, true, false)
-        SMLP_BWD_ROWS(true, false, true, true)
-        SMLP_BWD_ROWS(true, true, false, false)
-        SMLP_BWD_ROWS(true, true, false, true)
-        SMLP_BWD_ROWS(true, true, true, false)
-        SMLP_BWD_ROWS(true, true, true, true)
-        SMLP_BWD_ROWS(false, false, false, false)
-        SMLP_BWD_ROWS(false, false, true, false)
-        SMLP_BWD_ROWS(false, true, false, false)
-        SMLP_BWD_ROWS(false, true, true, false)
+        SMLP_BWD_ROWS(true, false, false)
+        SMLP_BWD_ROWS(true, false, true)
+        SMLP_BWD_ROWS(true, true, false)
+        SMLP_BWD_ROWS(true, true, true)
+        SMLP_BWD_ROWS(false, false, false)
+        SMLP_BWD_ROWS(false, true, false)
         default: return set_err(h, SMLP_E_ARG, "bwd_rows_kernel: bad mode");
     }
 #undef SMLP_BWD_ROWS
@@ -2284,27 +2187,6 @@ NarrowArgs narrow_args(smlp_handle* h, Layer& Ly, int c, bool fwd) {
     return A;
 }
 
-// Optional persisting-L2 access window over the slab a row kernel gathers from (knob
-// SMLP_L2PERSIST = hit ratio in percent; 0 = off).  Stream attribute, set around the launch.
-static void l2_window(smlp_handle* h, const void* base, size_t bytes) {
-    if (h->l2persist <= 0) return;
-    static bool limit_set = false;
-    if (!limit_set) {
-        int maxp = 0;
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device);
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
-        limit_set = true;
-    }
-    cudaStreamAttrValue v{};
-    v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
-    v.accessPolicyWindow.num_bytes = bytes;
-    v.accessPolicyWindow.hitRatio = bytes ? (float)h->l2persist / 100.f : 0.f;
-    v.accessPolicyWindow.hitProp = bytes ? cudaAccessPropertyPersisting : cudaAccessPropertyNormal;
-    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &v);
-    if (!bytes) cudaCtxResetPersistingL2Cache();
-}
-
 int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, bool train, uint64_t step,
                 float* probs) {
     const int CB = h->CBf;    // the forward tensors' chunk width
@@ -2322,7 +2204,6 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
     const bool drop = train && h->dropout > 0.f;
     if (h->xbits) {   // binary-input layer 2, all chunks in one pass (returns at once if not binary)
         Layer& L2 = h->layers[0];
-        SMLP_TRY(join_mirror(h, 2));
         BitsArgs A = bits_args(h, L2, nchunks);
         A.dropout_on = drop ? 1 : 0;
         A.step_lo = (uint32_t)step;
@@ -2340,7 +2221,6 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             const int Bc = std::min(CB, B - c * CB);
             const double nnz = (double)Ly.nnz;
             if (Ly.narrow) continue;   // after the chunk loop, several chunks per pass
-            SMLP_TRY(join_mirror(h, l));
             FwdArgs A{};
             A.a_prev = h->act[l - 1] + (int64_t)c * nin * CB;
             A.a_out = h->act[l] + (int64_t)c * nout * CB;
@@ -2369,11 +2249,9 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
             A.b0 = c * CB;
             A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
             A.zero_row = (int)((int64_t)(h->max_chunks_f - c) * nin);
-            A.l2hint = h->l2hint;
+            A.l2hint = 1;
             prof_start(h, K_FWD, l, 12.0 * nnz / nchunks + 4.0 * Bc * (double)(nin + nout), 2.0 * nnz * Bc);
-            l2_window(h, A.a_prev, (size_t)nin * CB * sizeof(float));
             SMLP_TRY(dispatch_fwd(h, A, Ly));
-            l2_window(h, nullptr, 0);
             prof_stop(h);
         }
     }
@@ -2407,7 +2285,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
 // Eq. 1 over the parameter slice [lo, hi) on `stream`: one resident wave (8 CTAs of 256 per SM),
 // two float4 groups per thread and iteration
 static int launch_update(smlp_handle* h, cudaStream_t stream, int64_t lo, int64_t hi, bool decay, const smlp_sgd* sgd,
-                         const Layer* mirror = nullptr, bool g2 = false) {
+                         bool g2 = false) {
     if (hi <= lo) return SMLP_OK;
     constexpr int threads = 256;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((hi - lo + 4 * threads - 1) / (4 * threads),
@@ -2421,18 +2299,10 @@ static int launch_update(smlp_handle* h, cudaStream_t stream, int64_t lo, int64_
     const float* gb = g2 ? h->grad2 + lo : nullptr;
     const float lr = sgd->lr, mu = sgd->momentum, wd = sgd->weight_decay, gs = sgd->grad_scale;
     const int64_t n = hi - lo;
-    if (mirror && g2)
-        sgd_update4_kernel<true, true><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs,
-                                                                     mirror->minv, mirror->mval, mirror->meta);
-    else if (mirror)
-        sgd_update4_kernel<true, false><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs,
-                                                                      mirror->minv, mirror->mval, mirror->meta);
-    else if (g2)
-        sgd_update4_kernel<false, true><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs,
-                                                                      nullptr, nullptr, nullptr);
+    if (g2)
+        sgd_update4_kernel<true><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs);
     else
-        sgd_update4_kernel<false, false><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs,
-                                                                       nullptr, nullptr, nullptr);
+        sgd_update4_kernel<false><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs);
     SMLP_CK_LAUNCH(h, "sgd_update4_kernel");
     return SMLP_OK;
 }
@@ -2444,22 +2314,6 @@ static int ensure_aux(smlp_handle* h) {
     return SMLP_OK;
 }
 
-// W^(l)'s gradient is final: its Eq. 1 slice and its mirror refresh go to the aux stream, behind
-// everything the main stream has enqueued so far (the backward of the layers below continues)
-static int overlap_layer_update(smlp_handle* h, Layer& Ly, const smlp_sgd* sgd) {
-    SMLP_TRY(ensure_aux(h));
-    SMLP_CK(h, cudaEventRecord(h->aux_ev[0], h->stream));
-    SMLP_CK(h, cudaStreamWaitEvent(h->aux_stream, h->aux_ev[0], 0));
-    SMLP_TRY(launch_update(h, h->aux_stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd, nullptr, Ly.split));
-    Ly.split = false;
-    if (!Ly.narrow) {   // narrow layers never read the mirror copy
-        mirror_values_kernel<<<launch_grid(h, (Ly.cap + 3) / 4, 256), 256, 0, h->aux_stream>>>(Ly.val, Ly.mperm,
-                                                                                               Ly.meta, Ly.mval);
-        SMLP_CK_LAUNCH(h, "mirror_values_kernel");
-    }
-    return SMLP_OK;
-}
-
 // W^(l)'s gradient (and b_{l-1}'s) is final: record the layer event (sparse_mlp_wait_layer lets a
 // communication stream start that layer's allreduce while the backward continues)
 static int layer_done(smlp_handle* h, int l) {
@@ -2468,15 +2322,11 @@ static int layer_done(smlp_handle* h, int l) {
     return SMLP_OK;
 }
 
-int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, const smlp_sgd* fused,
-                 const smlp_sgd* overlap_sgd, bool split_last) {
+int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, bool split_last) {
     const int CB = h->CB;
     const int B = h->trace_B;
     const int nchunks = (B + CB - 1) / CB;
     const int L = h->L;
-    const bool is_fused = fused != nullptr;
-    const float lr = is_fused ? fused->lr : 0.f, mu = is_fused ? fused->momentum : 0.f,
-                wd = is_fused ? fused->weight_decay : 0.f;
     {
         Layer& Lo = h->layers[L - 2];
         SoftmaxArgs S{};
@@ -2494,9 +2344,6 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
         S.nchunks = nchunks;
         S.CB = CB;
         S.CBf = h->CBf;
-        S.fused = is_fused ? 1 : 0;
-        S.lr = lr;
-        S.mu = mu;
         prof_start(h, K_SOFTMAX, L, 8.0 * (double)B * (double)S.nL, 0.0);
         softmax_ce_kernel<<<1, 512, 0, h->stream>>>(S);
         SMLP_CK_LAUNCH(h, "softmax_ce_kernel");
@@ -2504,7 +2351,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
     }
     // chunk-major, chunks in reverse: the forward ended on the last chunk, and layer l of chunk c
     // gathers the delta_l slab layer l+1 of chunk c just wrote (L2-resident).  Gradients
-    // accumulate over the chunks in this fixed order; the last one applies Eq. 1.
+    // accumulate over the chunks in this fixed order.
     for (int c = nchunks - 1; c >= 0; --c) {
         const bool first = c == nchunks - 1, last = c == 0;
         for (int l = L; l >= 2; --l) {
@@ -2533,16 +2380,10 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
                 A.dropout_prev = dropout_prev;
                 A.first = first;
                 A.last = last;
-                A.fused = is_fused ? 1 : 0;
-                A.lr = lr;
-                A.mu = mu;
-                A.wd = wd;
-                prof_start(h, K_BWD, l, (is_fused ? 20.0 : 12.0) * nnz / nchunks + act_bytes,
-                           (has_dprev ? 4.0 : 2.0) * nnz * Bc);
+                prof_start(h, K_BWD, l, 12.0 * nnz / nchunks + act_bytes, (has_dprev ? 4.0 : 2.0) * nnz * Bc);
                 SMLP_TRY(dispatch_narrow(h, A, Ly, false, CB));
                 prof_stop(h);
                 if (last) SMLP_TRY(layer_done(h, l));
-                if (last && overlap_sgd) SMLP_TRY(overlap_layer_update(h, Ly, overlap_sgd));
                 continue;
             }
             BwdArgs A{};
@@ -2561,8 +2402,6 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.val = Ly.val;
             A.mom = Ly.mom;
             A.grad = Ly.grad;
-            A.mval = Ly.mval;
-            A.minv = Ly.minv;
             A.ws = Ly.bws;
             A.bgs = Ly.bgs;
             A.bias_prev = Lp ? Lp->bias : nullptr;
@@ -2573,38 +2412,22 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
             A.keep_scale_prev = keep_scale;
             A.first = first;
             A.last = last;
-            A.fused = is_fused ? 1 : 0;
-            A.lr = lr;
-            A.mu = mu;
-            A.wd = wd;
             A.skip_if_binary = (l == 2 && h->xbits) ? h->d_nonbinary : nullptr;
             // the last of several chunks writes its gradient to grad2 instead of adding the earlier
             // chunks' sum (read back from grad); the Eq. 1 pass that follows adds the two
             // (W^(2) with the bit path keeps one buffer: its gradient may come from the bit kernels)
             Ly.split = false;
-            if (split_last && !fused && last && !first && h->grad2 && !(l == 2 && h->xbits)) {
+            if (split_last && last && !first && h->grad2 && !(l == 2 && h->xbits)) {
                 A.grad = h->grad2 + Ly.val_off;
                 A.no_gold = 1;
                 Ly.split = true;
             }
             A.zero_row = (int)((int64_t)(h->max_chunks - c) * nout);
-            A.l2hint = h->l2hint;
-            A.mval_scatter = (h->mirror_scatter && !(l == 2 && h->xbits)) ? 1 : 0;
-            prof_start(h, K_BWD, l, (is_fused ? 20.0 : 12.0) * nnz / nchunks + act_bytes,
-                       (has_dprev ? 4.0 : 2.0) * nnz * Bc);
-            l2_window(h, A.d_out, (size_t)nout * CB * sizeof(float));
+            A.l2hint = 1;
+            prof_start(h, K_BWD, l, 12.0 * nnz / nchunks + act_bytes, (has_dprev ? 4.0 : 2.0) * nnz * Bc);
             SMLP_TRY(dispatch_bwd(h, A, Ly, has_dprev));
-            l2_window(h, nullptr, 0);
             prof_stop(h);
-            // the forward reads the weights in mirror order: refresh that copy by a gather
-            // right after the update, while the canonical values are still L2-resident
-            if (is_fused && last && !(l == 2 && h->xbits) && !A.mval_scatter) {
-                prof_start(h, K_MIRROR, l, 12.0 * nnz, 0.0);
-                SMLP_TRY(refresh_mirror_values(h, Ly));
-                prof_stop(h);
-            }
             if (last) SMLP_TRY(layer_done(h, l));
-            if (last && overlap_sgd && !(l == 2 && h->xbits)) SMLP_TRY(overlap_layer_update(h, Ly, overlap_sgd));
         }
     }
     if (h->xbits) {   // binary-input layer 2 (returns at once if not binary)
@@ -2614,25 +2437,12 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
         prof_start(h, K_BWD_BITS, 2, 8.0 * nnz + 4.0 * B * (double)(L2.n_in + L2.n_out), 2.0 * nnz * B);   // src, g
         SMLP_TRY(dispatch_bits(h, A, L2, false));
         prof_stop(h);
-        prof_start(h, K_LAYER_UPDATE, 2, (is_fused ? 24.0 : 12.0) * nnz, 0.0);
-        grad_from_mirror_kernel<<<launch_grid(h, L2.cap, 256), 256, 0, h->stream>>>(
-            h->d_nonbinary, h->gmirror2, L2.minv, L2.val, L2.mom, L2.grad, L2.meta, is_fused ? 1 : 0, lr, mu, wd);
+        prof_start(h, K_LAYER_UPDATE, 2, 12.0 * nnz, 0.0);
+        grad_from_mirror_kernel<<<launch_grid(h, L2.cap, 256), 256, 0, h->stream>>>(h->d_nonbinary, h->gmirror2,
+                                                                                    L2.minv, L2.grad, L2.meta);
         SMLP_CK_LAUNCH(h, "grad_from_mirror_kernel");
         prof_stop(h);
-        if (is_fused) {
-            prof_start(h, K_MIRROR, 2, 12.0 * nnz, 0.0);
-            SMLP_TRY(refresh_mirror_values(h, L2));
-            prof_stop(h);
-        }
         SMLP_TRY(layer_done(h, 2));
-        if (overlap_sgd) SMLP_TRY(overlap_layer_update(h, L2, overlap_sgd));
-    }
-    if (overlap_sgd) {   // the biases (no weight decay), then join the aux stream
-        prof_start(h, K_SGD, 0, 20.0 * (double)(h->param_count - h->bias_base), 0.0);
-        SMLP_TRY(launch_update(h, h->stream, h->bias_base, h->param_count, false, overlap_sgd));
-        SMLP_CK(h, cudaEventRecord(h->aux_ev[1], h->aux_stream));
-        SMLP_CK(h, cudaStreamWaitEvent(h->stream, h->aux_ev[1], 0));
-        prof_stop(h);
     }
     return SMLP_OK;
 }
@@ -2675,26 +2485,14 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
     for (auto& Ly : h->layers) {
         const bool g2 = Ly.split;
         Ly.split = false;
-        if (h->update_scatter && !Ly.narrow) {                     // the update writes the mirror copy too
-            SMLP_TRY(launch_update(h, h->stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd, &Ly, g2));
-            continue;
-        }
-        SMLP_TRY(launch_update(h, h->stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd, nullptr, g2));
+        SMLP_TRY(launch_update(h, h->stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd, g2));
         if (Ly.narrow) continue;                                   // narrow layers never read the mirror copy
         SMLP_CK(h, cudaEventRecord(h->aux_ev[0], h->stream));
         SMLP_CK(h, cudaStreamWaitEvent(h->aux_stream, h->aux_ev[0], 0));
         mirror_values_kernel<<<launch_grid(h, (Ly.cap + 3) / 4, 256), 256, 0, h->aux_stream>>>(Ly.val, Ly.mperm, Ly.meta,
                                                                                      Ly.mval);
         SMLP_CK_LAUNCH(h, "mirror_values_kernel");
-        if (h->defer_mirror) {
-            // joined lazily: the next forward waits for layer l's copy right before layer l
-            // (join_mirrors for every other consumer), so the refresh overlaps its first layers
-            if (!h->mirror_ev[Ly.l]) SMLP_CK(h, cudaEventCreateWithFlags(&h->mirror_ev[Ly.l], cudaEventDisableTiming));
-            SMLP_CK(h, cudaEventRecord(h->mirror_ev[Ly.l], h->aux_stream));
-            h->mirror_pending[Ly.l] = true;
-        } else {
-            side = true;
-        }
+        side = true;
     }
     SMLP_TRY(update(h->bias_base, n, false));                      // biases: no weight decay
     if (side) {
@@ -2702,18 +2500,6 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
         SMLP_CK(h, cudaStreamWaitEvent(h->stream, h->aux_ev[1], 0));
     }
     prof_stop(h);
-    return SMLP_OK;
-}
-
-// the handle's stream waits for layer l's pending mirror refresh (deferred by run_step)
-int join_mirror(smlp_handle* h, int l) {
-    if (!h->mirror_pending[l]) return SMLP_OK;
-    SMLP_CK(h, cudaStreamWaitEvent(h->stream, h->mirror_ev[l], 0));
-    h->mirror_pending[l] = false;
-    return SMLP_OK;
-}
-int join_mirrors(smlp_handle* h) {
-    for (int l = 2; l <= h->L; ++l) SMLP_TRY(join_mirror(h, l));
     return SMLP_OK;
 }
 

@@ -100,7 +100,6 @@ __global__ void removal_from_keys_kernel(const uint64_t* __restrict__ sorted_key
 
 int sparse_mlp_union_average_layer(smlp_handle* h, int32_t l, int32_t K, const uint64_t* pos_all,
                                    const float* val_all, int64_t total, int64_t target, int64_t* kept) {
-    if (h) SMLP_TRY(smlp::join_mirrors(h));   // deferred mirror refreshes (run_step)
     using namespace smlp;
     if (!h || l < 2 || l > h->L || K < 1 || total < 0 || target < 0 || (total > 0 && (!pos_all || !val_all)))
         return SMLP_E_ARG;
@@ -178,7 +177,6 @@ int sparse_mlp_union_average_layer(smlp_handle* h, int32_t l, int32_t K, const u
 }
 
 int sparse_mlp_export_positions(smlp_handle* h, int32_t l, uint64_t* pos_dev, float* val_dev) {
-    if (h) SMLP_TRY(smlp::join_mirrors(h));   // deferred mirror refreshes (run_step)
     using namespace smlp;
     if (!h || l < 2 || l > h->L) return SMLP_E_ARG;
     Layer& Ly = h->layers[l - 2];
@@ -219,7 +217,6 @@ __global__ void retain_kernel(const int32_t* __restrict__ rowid, const int32_t* 
 
 int sparse_mlp_retain_valid_updates(smlp_handle* h, int32_t l, const uint64_t* stale_pos, const float* stale_g,
                                     int64_t n_stale, int64_t* retained) {
-    if (h) SMLP_TRY(smlp::join_mirrors(h));   // deferred mirror refreshes (run_step)
     using namespace smlp;
     if (!h || l < 2 || l > h->L || n_stale < 0 || (n_stale > 0 && (!stale_pos || !stale_g))) return SMLP_E_ARG;
     Layer& Ly = h->layers[l - 2];
@@ -242,7 +239,6 @@ int sparse_mlp_retain_valid_updates(smlp_handle* h, int32_t l, const uint64_t* s
 
 int sparse_mlp_params_averaged(smlp_handle* h, int32_t K, int32_t biases_only) {
     using namespace smlp;
-    if (h) SMLP_TRY(join_mirrors(h));   // deferred mirror refreshes (run_step)
     if (!h) return SMLP_E_ARG;
     if (K < 1) return set_err(h, SMLP_E_ARG, "K must be >= 1");
     const int64_t lo = biases_only ? h->bias_base : 0;

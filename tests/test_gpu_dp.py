@@ -62,7 +62,8 @@ def _worker(rank, K, port, mode, q):
         from paper_2102_01732_b200 import SGD, SparseMLP
         from paper_2102_01732_b200 import dp as D
         from synth import get_config, make_dataset
-        from tests.gpu_helpers import TOL, assert_topology_equal, assert_values_close, to_dev
+        from tests.gpu_helpers import (TOL, assert_topology_equal, assert_values_close, load_oracle_state_into_gpu,
+                                       to_dev)
         D.init_process_group(backend="gloo")
         assert dist.get_world_size() == K and dist.get_rank() == rank
         cfg = get_config("C1", dropout=0.2)
@@ -89,6 +90,7 @@ def _worker(rank, K, port, mode, q):
             assert_values_close(g, st, TOL, f"rank {rank} step {s}")
             p, _ = g.param_view()
             assert D.replicas_identical(p), f"replicas differ after step {s}"
+            load_oracle_state_into_gpu(g, st)        # the next step from identical inputs (per-step parity)
         # ---- Eq. 2 averaging after divergent local steps (phase 2 without a per-step collective)
         states = [st.copy() for _ in range(K)]
         batches, nxt = _kink_free_batches(st, X, Y, B, K, 3, nxt)
@@ -100,6 +102,9 @@ def _worker(rank, K, port, mode, q):
         g.backward(to_dev(y.astype(np.int32)), fused=sgd)
         torch.cuda.synchronize()
         assert_values_close(g, states[rank], TOL, f"rank {rank} local step")
+        for k in range(K):                       # Eq. 2 compared op by op: every replica's exact
+            if k != rank:                        # pre-average state is the oracle's own
+                states[k].reset_error()
         ODP.average(states)
         D.average_model_(g)
         torch.cuda.synchronize()

@@ -15,7 +15,7 @@ import pytest
 from oracle import model as M
 from oracle.compare import rel_err
 from synth import get_config, make_dataset
-from tests.gpu_helpers import TOL, assert_topology_equal, assert_values_close, pair, to_dev
+from tests.gpu_helpers import TOL, assert_topology_equal, assert_values_close, check_and_resync, pair, to_dev
 
 pytestmark = pytest.mark.gpu
 
@@ -75,7 +75,7 @@ def test_binary_input_path_parity(B, chunk, fchunk, dropout, monkeypatch):
         g.step(sgd)
         M.step(st, gr, sgd.lr, sgd.momentum, sgd.weight_decay)
         torch.cuda.synchronize()
-        assert_values_close(g, st, TOL, f"binary path step {s}")
+        check_and_resync(g, st, f"binary path step {s}")
     # fused path (the 1-GPU bench path) on the last batch
     x, y = X[3 * B:], Y[3 * B:]
     g.forward(to_dev(x), train=True, step=3)
@@ -119,7 +119,7 @@ def test_real_input_kind_skips_the_bit_path():
         g.backward(to_dev(y), fused=sgd)
         M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, s_)
         torch.cuda.synchronize()
-        assert_values_close(g, st, TOL, f"real input kind step {s_}")
+        check_and_resync(g, st, f"real input kind step {s_}")
 
 
 def test_binary_input_kind_checked_promise():
@@ -147,7 +147,7 @@ def test_binary_input_kind_checked_promise():
         g.backward(to_dev(y), fused=sgd)
         M.step(st, M.backward(st, tr, y), sgd.lr, sgd.momentum, sgd.weight_decay)
         torch.cuda.synchronize()
-        assert_values_close(g, st, TOL, f"binary input kind, step {s_}")
+        check_and_resync(g, st, f"binary input kind, step {s_}")
     with pytest.raises(SparseMLPError, match="E_DATA"):
         g.sync()
     g.sync()                                         # reported once, then cleared
@@ -199,10 +199,17 @@ def test_generic_output_layer_parity():
         g.backward(to_dev(y), fused=sgd)
         M.train_step(st, x, y, sgd.lr, sgd.momentum, sgd.weight_decay, s)
         torch.cuda.synchronize()
-        assert_values_close(g, st, TOL, f"generic output layer step {s}")
+        check_and_resync(g, st, f"generic output layer step {s}")
 
 
 # ----------------------------------------------------------------------------------------- C5 full size
+def _kept_ok(k, Ly, cfg, B, min_kept):
+    """>= min_kept untainted gradient entries, bias gradients and delta elements of the layer, or
+    all there are when the layer has fewer (e.g. the 2 output neurons)."""
+    n = cfg.sizes[Ly.l - 1]
+    return k[0] >= min(min_kept, Ly.nnz) and k[1] >= min(min_kept, n) and k[2] >= min(min_kept, B * n)
+
+
 def _full_size_sampled_parity(name, B, widths, min_kept=256):
     """Full-size model in the bench launch configuration (max_batch = cfg.batch).  Checked: ER
     topology and values bit-exact, every forward activation and logit of a B-row batch, every
@@ -264,12 +271,12 @@ def _full_size_sampled_parity(name, B, widths, min_kept=256):
             J = np.array(sorted(deltas[l]), np.int64)
             T = np.stack([tainted[l][int(j)] for j in J], axis=1)
             kept[l] = (int(ok.sum()), int(okn.sum()), int((~T).sum()))
-        if all(min(k) >= min(min_kept, Ly.nnz) for k, Ly in zip(kept.values(), st.layers)):
+        if all(_kept_ok(kept[Ly.l], Ly, cfg, B, min_kept) for Ly in st.layers):
             break
     print(f"{name} kept per layer (gradient entries, bias gradients, delta elements):", kept)
     for Ly in st.layers:
         l = Ly.l
-        assert min(kept[l]) >= min(min_kept, Ly.nnz), (l, kept[l])
+        assert _kept_ok(kept[l], Ly, cfg, B, min_kept), (l, kept[l])
         go, gm, ok = gsamp[l]
         gg = gexp[l][ent[l]]
         assert rel_err(gg[ok], go[ok], gm[ok]) <= TOL, ("g", l, rel_err(gg[ok], go[ok], gm[ok]))
@@ -389,7 +396,7 @@ def test_long_rows_and_chunk_widths_parity(chunk, fchunk, B, dropout, eps, salt,
         g.step(sgd)
         M.step(st, gr, sgd.lr, sgd.momentum, sgd.weight_decay)
         torch.cuda.synchronize()
-        assert_values_close(g, st, TOL, f"long rows step {s}")
+        check_and_resync(g, st, f"long rows step {s}")
     while True:
         assert nxt < 16, "no kink-free batch among the candidates"
         x, y = X[nxt * B:(nxt + 1) * B], Y[nxt * B:(nxt + 1) * B]

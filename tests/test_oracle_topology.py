@@ -233,3 +233,20 @@ def test_prune_uses_snapshot_of_all_layers():
         ids = np.flatnonzero(pre.alive[h - 1])
         t = T.percentile_threshold(np.sort(I[h][ids]), 20.0)
         assert set(np.flatnonzero(st.alive[h - 1] == 0)) == set(ids[I[h][ids] < t])
+
+
+def test_candidate_stream_bound_fails_like_the_cuda_path(monkeypatch):
+    """R33: the candidate stream is searched over at most MAX_CANDIDATES draws (2^31 - 1 on both
+    sides, the CUDA path's 32-bit candidate index); with fewer distinct valid positions in that
+    prefix than needed, ER init and regrowth raise instead of drawing on (the library returns
+    SMLP_E_ARG "could not find enough distinct candidates").  Exercised with a small bound."""
+    from oracle import model as M
+    from oracle import topology as T
+    monkeypatch.setattr(M, "MAX_CANDIDATES", 50)
+    with pytest.raises(ValueError, match="distinct candidates"):
+        M.er_layer(30, 30, 3.0, "he_uniform", 1, 2)            # M = 180 distinct needed in 50 draws
+    monkeypatch.setattr(M, "MAX_CANDIDATES", (1 << 31) - 1)
+    st = M.create((40, 40, 3), 4.0, "all_relu", 0.5, 0.0, "he_uniform", 2)
+    monkeypatch.setattr(T, "MAX_CANDIDATES", 10)
+    with pytest.raises(ValueError, match="distinct candidates"):
+        T.evolve(st, 0.3, 0)
