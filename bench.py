@@ -280,7 +280,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    use_graph = args.graph in ("on", "auto") and world == 1 and not dp_path
+    use_graph = args.graph in ("on", "auto")
     graph_note = None
     if use_graph:
         # C1-C4 steps last ~0.1-0.3 ms: replay G captured steps per CUDA graph; the
@@ -290,7 +290,10 @@ def main():
         idx_win = torch.zeros(G * B, dtype=torch.int32, device=device)
         counter = torch.zeros(1, dtype=torch.int64, device=device)
         model.sparse_mlp_set_step_counter(counter)
-        sgd_g = SGD(cfg.lr, cfg.momentum, cfg.weight_decay)
+        # the DP path replays with the post-warmup learning rate K eta (R20: the warmup is a
+        # schedule of the same kernels)
+        lr_g = scaled_lr(cfg.lr, world, warm_steps, warm_steps) if dp_path else cfg.lr
+        sgd_g = SGD(lr_g, cfg.momentum, cfg.weight_decay, 1.0 / world if dp_path else 1.0)
         cap_stream = torch.cuda.Stream(device=device)
         cap_stream.wait_stream(torch.cuda.current_stream())
         graph = torch.cuda.CUDAGraph()
@@ -300,7 +303,12 @@ def main():
                 for k in range(G):
                     iw = idx_win[k * B:(k + 1) * B]
                     model.forward(X, x_idx=iw, train=True, step=0)
-                    model.backward(Y, y_idx=iw, loss=loss, fused=sgd_g)
+                    if not dp_path:
+                        model.backward(Y, y_idx=iw, loss=loss, fused=sgd_g)
+                    else:   # unfused backward, bucketed allreduce on the side stream, Eq. 1 (1/K)
+                        model.backward(Y, y_idx=iw, loss=loss, fused=None)
+                        overlap() if world > 1 else overlap(reduce=lambda t: None)
+                        model.step(sgd_g)
                     counter.add_(1)
                 model.join()                                 # the library's side-stream work rejoins the capture
         torch.cuda.current_stream().wait_stream(cap_stream)

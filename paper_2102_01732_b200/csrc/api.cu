@@ -163,6 +163,9 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
         off += round_up(Ly.n_out, 32);
     }
     h->param_count = off;
+    // programmatic dependent launch for the launch-bound small models only (measured
+    // C4 / C3 -2..5%, C5 +12% per step)
+    h->pdl = off <= SMALL_MODEL_PARAMS ? 1 : 0;
     h->param = zalloc<float>(h, (size_t)off, &rc);
     h->mom = zalloc<float>(h, (size_t)off, &rc);
     h->grad = zalloc<float>(h, (size_t)off, &rc);

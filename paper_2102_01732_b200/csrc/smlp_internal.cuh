@@ -170,6 +170,7 @@ struct smlp_handle {
     std::vector<smlp::ProfRec> prof_recs;
     std::vector<cudaEvent_t> ev_pool;
     int num_sms = 148;
+    int pdl = 0;                    // launch the step's kernels with programmatic serialization
     // tuning knobs (env, read at create; each selects between kernels the parity tests cover)
     int narrow_sparse_bwd = 0;      // SMLP_NARROW_SPARSE_BWD: narrow row-streaming backward also for a sparse output layer
     int64_t short_min_rows = -1;    // SMLP_SHORT_MIN_ROWS: -1 = one 32-row unit per resident warp
@@ -203,6 +204,53 @@ int check_cuda(smlp_handle* h, cudaError_t e, const char* what);
         int _rc = (call);          \
         if (_rc != SMLP_OK) return _rc; \
     } while (0)
+
+// ------------------------------------------------------------------------------------------
+// Programmatic dependent launch ("launch chain"): for small models (h->pdl) the
+// step's kernels are launched with the programmatic-serialization attribute, so kernel n+1's
+// launch and CTA rasterisation overlap kernel n's tail; every such kernel starts with
+// SMLP_PDL_ENTRY -- griddepcontrol.wait blocks until the previous grid has COMPLETED and its
+// writes are visible (so no kernel reads a predecessor's output early), then launch_dependents
+// lets the next grid start launching.  Without the attribute both are no-ops.
+// ------------------------------------------------------------------------------------------
+#define SMLP_PDL_ENTRY()                                          \
+    do {                                                          \
+        asm volatile("griddepcontrol.wait;" ::: "memory");        \
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    } while (0)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(int pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t stream,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+// Device bounds checks ("bounds-checked build"): compiled in only by the A/B build
+// tools/ab_build.py bounds -DSMLP_BOUNDS_CHECK=1 (compute-sanitizer is closed on the GPU pool), which
+// the GPU parity tests then run against with SMLP_LIB; a violated bound prints and traps.
+#ifdef SMLP_BOUNDS_CHECK
+#define SMLP_BOUND(cond, what)                                                             \
+    do {                                                                                   \
+        if (!(cond)) {                                                                     \
+            printf("smlp bounds check failed: %s (%s:%d)\n", what, __FILE__, __LINE__);   \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define SMLP_BOUND(cond, what) \
+    do {                       \
+    } while (0)
+#endif
 
 // per-kernel CUDA-event timing (no-ops unless h->prof)
 void prof_start(smlp_handle* h, int kind, int layer, double bytes, double flops);

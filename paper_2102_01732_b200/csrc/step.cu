@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(1024) stage_input_kernel(const float* __restri
                                                            int B, int nchunks, int CB, int64_t n1,
                                                            float* __restrict__ act1, uint32_t* __restrict__ xbits,
                                                            int32_t* __restrict__ nonbinary, int vec) {
+    SMLP_PDL_ENTRY();
     __shared__ float tile[32][129];
     const int64_t f0 = (int64_t)blockIdx.x * 128;
     const int b0 = blockIdx.y * 32;
@@ -262,6 +263,7 @@ __device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4
 
 template <int CB>
 __global__ void __launch_bounds__(256) fwd_finish_kernel(FwdArgs A) {
+    SMLP_PDL_ENTRY();
     constexpr int G = CB / 4, P = 32 / G;
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
@@ -496,6 +498,7 @@ __device__ __forceinline__ void stage_window(int2* win, const int (&ix)[NW], con
 
 template <int CB>
 __global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(FwdArgs A) {
+    SMLP_PDL_ENTRY();
     using C = RowCfg<CB, true>;
     constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB;
     __shared__ int2 win_all[WARPS_PER_BLOCK][C::WIN];
@@ -523,6 +526,10 @@ __global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(F
         load_window<NW>(A.msrc, A.mval, nxt.y, nxt.z, lane, ix_n, w_n);   // indices one ahead
         const float bj = cur.w < 0 ? __ldg(A.bias + cur.x) : 0.f;         // consumed after the gathers
         const int n = cur.z - cur.y;
+        SMLP_BOUND(0 <= cur.y && cur.y <= cur.z && cur.z <= A.meta->nnz && n <= SEG_NNZ, "fwd segment");
+#pragma unroll
+        for (int r = 0; r < NW; ++r)
+            SMLP_BOUND(lane + 32 * r >= n || (unsigned)ix[r] < (unsigned)A.zero_row, "fwd gathered row");
         __syncwarp();
         stage_window<NW>(win, ix, w, n, lane, A.zero_row);
         __syncwarp();
@@ -555,6 +562,7 @@ __global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(F
 // sum per row as the row kernel, so the result is identical.
 constexpr int SHORT_ROWS = 32;
 __global__ void __launch_bounds__(256, 4) fwd_short_rows_kernel(FwdArgs A) {
+    SMLP_PDL_ENTRY();
     constexpr int CB = 128, GU = 4;                 // gathers in flight per warp (4 x 16 B, 64 regs)
     __shared__ int2 rec_all[WARPS_PER_BLOCK][32 + GU];
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;
@@ -588,6 +596,7 @@ __global__ void __launch_bounds__(256, 4) fwd_short_rows_kernel(FwdArgs A) {
             __syncwarp();
             rec[lane] = lane < n ? make_int2(ld_hint_i(A.msrc + blk + lane, ps), __float_as_int(ld_hint(A.mval + blk + lane, ps)))
                                  : make_int2(A.zero_row, 0);
+            SMLP_BOUND((unsigned)rec[lane].x <= (unsigned)A.zero_row, "fwd short gathered row");
             __syncwarp();
             for (int v0 = 0; v0 < n; v0 += GU) {
                 float4 x[GU];
@@ -637,6 +646,7 @@ struct SoftmaxArgs {
 };
 
 __global__ void __launch_bounds__(512) softmax_ce_kernel(SoftmaxArgs A) {
+    SMLP_PDL_ENTRY();
     __shared__ double red[512];
     const int tid = threadIdx.x;
     double lsum = 0.0;
@@ -687,6 +697,7 @@ __global__ void __launch_bounds__(512) softmax_ce_kernel(SoftmaxArgs A) {
 
 __global__ void softmax_probs_kernel(const float* __restrict__ logits, float* __restrict__ probs, int64_t nL, int B,
                                      int CB) {
+    SMLP_PDL_ENTRY();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     const int c = b / CB, lb = b % CB;
@@ -795,6 +806,7 @@ __device__ __forceinline__ void bwd_epilogue(const BwdArgs& A, int64_t i, float4
 
 template <int CB, int CBF>
 __global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
+    SMLP_PDL_ENTRY();
     constexpr int G = CB / 4, P = 32 / G;
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
@@ -941,6 +953,7 @@ __device__ __forceinline__ void bwd_batch(const float* __restrict__ d_out, const
 // GOLD: add the gradient accumulated by earlier chunks; DROP: dropout on layer l-1
 template <int CB, int CBF, bool HAS_DPREV, bool GOLD, bool DROP>
 __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
+    SMLP_PDL_ENTRY();
     using C = RowCfg<CB>;
     constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB, S = C::S, NR = C::NR;
     constexpr int RB = NB < 2 ? NB : 2;              // batches per reduction round
@@ -990,6 +1003,10 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
         cp_async_wait1();
         __syncwarp();
         window_pad(win[buf], n, lane, A.zero_row);
+        SMLP_BOUND(0 <= cur.y && cur.y <= cur.z && cur.z <= A.meta->nnz && n <= SEG_NNZ, "bwd segment");
+#pragma unroll
+        for (int r = 0; r < SEG_NNZ / 32; ++r)
+            SMLP_BOUND((unsigned)win[buf][lane + 32 * r].x <= (unsigned)A.zero_row, "bwd gathered row");
         __syncwarp();
         const float4 ai = ais[buf][q];
         float4 dacc = f4zero();
@@ -1146,6 +1163,7 @@ __device__ __forceinline__ void narrow_row(const NarrowArgs& A, bool dense, int6
 // whatever CB, so the logits do not depend on it.
 template <int CB, int CBF, int NOUT>
 __global__ void __launch_bounds__(NARROW_WARPS * 32) fwd_narrow_kernel(NarrowArgs A) {
+    SMLP_PDL_ENTRY();
     constexpr int VEC = CB >= 32 ? CB / 32 : 1;
     constexpr int RU = VEC == 4 ? 4 : 8;
     __shared__ float red[NOUT * CB];
@@ -1215,6 +1233,7 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) fwd_narrow_kernel(NarrowArg
 // then an xor tree) + b_L, stored at column b % CBF of forward chunk b / CBF
 template <int CB, int CBF, int NOUT>
 __global__ void __launch_bounds__(32) fwd_narrow_finish_kernel(NarrowArgs A, int nparts) {
+    SMLP_PDL_ENTRY();
     const int e = blockIdx.x, lane = threadIdx.x;
     if (e % CB >= A.ncols) return;
     // lane b sums parts b, b + 32, ... in order; the loads of 8 parts are issued together (one
@@ -1240,6 +1259,7 @@ __global__ void __launch_bounds__(32) fwd_narrow_finish_kernel(NarrowArgs A, int
 
 template <int CB, int CBF, int NOUT>
 __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_kernel(NarrowArgs A) {
+    SMLP_PDL_ENTRY();
     constexpr int VEC = CB >= 32 ? CB / 32 : 1;
     constexpr int RU = VEC == 4 ? 2 : (VEC == 2 ? 4 : 8);
     const int lane = threadIdx.x & 31;
@@ -1352,6 +1372,7 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_kernel(NarrowArg
 // row is output jj.  ~10 warp instructions per row instead of ~200 with one row per warp.
 template <int CB, int CBF, int NOUT>
 __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_rows_kernel(NarrowArgs A) {
+    SMLP_PDL_ENTRY();
     constexpr int CS = CB < 32 ? CB : 32;     // columns per slice
     constexpr int NS = CB / CS;
     static_assert(CBF % CS == 0, "a slice lies inside one forward chunk");
@@ -1501,6 +1522,7 @@ constexpr int BITS_ROWS = 32;
 
 template <int CB, bool DROP>
 __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
+    SMLP_PDL_ENTRY();
     constexpr int G = CB / 4;                       // lanes per chunk
     __shared__ float2 rec[WARPS_PER_BLOCK][32][XBITS_WORDS];
     if (*A.nonbinary) {
@@ -1626,6 +1648,7 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
 // grad_from_mirror_kernel.
 template <int CB>
 __global__ void __launch_bounds__(256) bwd_bits_rows_kernel(BitsArgs A) {
+    SMLP_PDL_ENTRY();
     __shared__ __align__(16) float dsm_all[WARPS_PER_BLOCK][2][32 * XBITS_WORDS];
     if (*A.nonbinary) return;
     const int lane = threadIdx.x & 31;
@@ -1687,6 +1710,7 @@ __global__ void __launch_bounds__(256) bwd_bits_rows_kernel(BitsArgs A) {
 __global__ void grad_from_mirror_kernel(const int32_t* __restrict__ nonbinary, const float* __restrict__ gm,
                                         const int32_t* __restrict__ minv, float* __restrict__ grad,
                                         const LayerMeta* __restrict__ meta) {
+    SMLP_PDL_ENTRY();
     if (*nonbinary) return;
     const int64_t n = meta->nnz;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
@@ -1705,6 +1729,7 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
                                                           const float* __restrict__ g, const float* __restrict__ g2,
                                                           int64_t n, float lr,
                                                           float mu, float wd, int64_t decay_end, float gs) {
+    SMLP_PDL_ENTRY();
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     const int64_t n4 = n >> 2;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
@@ -1768,6 +1793,7 @@ struct MirrorSet {
     float* mval[SMLP_MAX_LAYERS];
 };
 __global__ void __launch_bounds__(256) mirror_values_multi_kernel(const __grid_constant__ MirrorSet M) {
+    SMLP_PDL_ENTRY();
     const int l = blockIdx.y;
     const int64_t n = M.meta[l]->nnz;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
@@ -1777,6 +1803,7 @@ __global__ void __launch_bounds__(256) mirror_values_multi_kernel(const __grid_c
 // mirror copy mval[t] = val[mperm[t]], 4 consecutive t per thread (4 independent gathers in flight)
 __global__ void __launch_bounds__(256) mirror_values_kernel(const float* __restrict__ val, const int32_t* __restrict__ mperm,
                                                             const LayerMeta* __restrict__ meta, float* __restrict__ mval) {
+    SMLP_PDL_ENTRY();
     const uint64_t pf = policy_evict_first();
     const int64_t n = meta->nnz, n4 = n >> 2;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
@@ -1798,6 +1825,7 @@ __global__ void __launch_bounds__(256) mirror_values_kernel(const float* __restr
 // variant keeps the row kernel).
 template <bool HAS_DPREV, bool GOLD, bool DROP>
 __global__ void __launch_bounds__(256, 4) bwd_short_rows_kernel(BwdArgs A) {
+    SMLP_PDL_ENTRY();
     constexpr int CB = 128, GU = 4, NR = RowCfg<CB>::NR;
     __shared__ int4 rec_all[WARPS_PER_BLOCK][32 + GU];
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;
@@ -1852,6 +1880,7 @@ __global__ void __launch_bounds__(256, 4) bwd_short_rows_kernel(BwdArgs A) {
             } else {
                 rec[lane] = make_int4(A.zero_row, 0, (int)i0, 0);
             }
+            SMLP_BOUND((unsigned)rec[lane].x <= (unsigned)A.zero_row, "bwd short gathered row");
             const float gold_l = GOLD && lane < n ? ld_hint(A.grad + blk + lane, ps) : 0.f;
             __syncwarp();
             float gval = 0.f;                              // lane t: the SDDMM gradient of entry t
@@ -1930,16 +1959,16 @@ int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
         if (L.nnz < (int64_t)h->short_max_fwd * L.n_out &&
             L.n_out >= short_min_rows(h)) {
             const int64_t units = (L.n_out + SHORT_ROWS - 1) / SHORT_ROWS;
-            fwd_short_rows_kernel<<<rows_grid(h, fwd_short_rows_kernel, units), WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+            launch_pdl(h->pdl, fwd_short_rows_kernel, rows_grid(h, fwd_short_rows_kernel, units), WARPS_PER_BLOCK * 32, h->stream, A);
             SMLP_CK_LAUNCH(h, "fwd_short_rows_kernel");
             return SMLP_OK;
         }
     }
-    fwd_rows_kernel<CB><<<rows_grid(h, fwd_rows_kernel<CB>, L.fseg_cap), WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+    launch_pdl(h->pdl, fwd_rows_kernel<CB>, rows_grid(h, fwd_rows_kernel<CB>, L.fseg_cap), WARPS_PER_BLOCK * 32, h->stream, A);
     SMLP_CK_LAUNCH(h, "fwd_rows_kernel");
     if (L.fslot_cap > 0) {
         const int g2 = persistent_grid(h, std::max<int64_t>(1, L.fslot_cap / 2), P);
-        fwd_finish_kernel<CB><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        launch_pdl(h->pdl, fwd_finish_kernel<CB>, g2, WARPS_PER_BLOCK * 32, h->stream, A);
         SMLP_CK_LAUNCH(h, "fwd_finish_kernel");
     }
     return SMLP_OK;
@@ -1956,8 +1985,7 @@ int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev)
             const int64_t units = (L.n_in + SHORT_ROWS - 1) / SHORT_ROWS;
 #define SMLP_BWD_SHORT(HD, GO, DR)                                                                          \
     if (has_dprev == HD && gold == GO && drop == DR) {                                                    \
-        bwd_short_rows_kernel<HD, GO, DR><<<rows_grid(h, bwd_short_rows_kernel<HD, GO, DR>, units),             \
-                                            WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);                       \
+        launch_pdl(h->pdl, bwd_short_rows_kernel<HD, GO, DR>, rows_grid(h, bwd_short_rows_kernel<HD, GO, DR>, units), WARPS_PER_BLOCK * 32, h->stream, A); \
         SMLP_CK_LAUNCH(h, "bwd_short_rows_kernel");                                                       \
         return SMLP_OK;                                                                                   \
     }
@@ -1973,8 +2001,7 @@ int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev)
     const int mode = (has_dprev ? 4 : 0) | (gold ? 2 : 0) | (drop ? 1 : 0);
 #define SMLP_BWD_ROWS(HD, GO, DR)                                                                             \
 case (HD ? 4 : 0) | (GO ? 2 : 0) | (DR ? 1 : 0):                                                            \
-    bwd_rows_kernel<CB, CBF, HD, GO, DR><<<rows_grid(h, bwd_rows_kernel<CB, CBF, HD, GO, DR>, L.bseg_cap),      \
-                                       WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);                          \
+    launch_pdl(h->pdl, bwd_rows_kernel<CB, CBF, HD, GO, DR>, rows_grid(h, bwd_rows_kernel<CB, CBF, HD, GO, DR>, L.bseg_cap), WARPS_PER_BLOCK * 32, h->stream, A); \
     break;
     switch (mode) {
         SMLP_BWD_ROWS(true, false, false)
@@ -1989,7 +2016,7 @@ case (HD ? 4 : 0) | (GO ? 2 : 0) | (DR ? 1 : 0):                                
     SMLP_CK_LAUNCH(h, "bwd_rows_kernel");
     if (has_dprev && L.bslot_cap > 0) {
         const int g2 = persistent_grid(h, std::max<int64_t>(1, L.bslot_cap / 2), P);
-        bwd_finish_kernel<CB, CBF><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        launch_pdl(h->pdl, bwd_finish_kernel<CB, CBF>, g2, WARPS_PER_BLOCK * 32, h->stream, A);
         SMLP_CK_LAUNCH(h, "bwd_finish_kernel");
     }
     return SMLP_OK;
@@ -2033,17 +2060,16 @@ int launch_narrow_n(smlp_handle* h, const NarrowArgs& A, const Layer& L, bool fw
         return set_err(h, SMLP_E_ARG, "narrow output layer too wide for chunk_batch");
     } else {
         if (fwd) {
-            fwd_narrow_kernel<CB, CBF, NOUT><<<L.ngrid, NARROW_WARPS * 32, 0, h->stream>>>(A);
+            launch_pdl(h->pdl, fwd_narrow_kernel<CB, CBF, NOUT>, L.ngrid, NARROW_WARPS * 32, h->stream, A);
             SMLP_CK_LAUNCH(h, "fwd_narrow_kernel");
-            fwd_narrow_finish_kernel<CB, CBF, NOUT><<<A.n_out * CB, 32, 0, h->stream>>>(A, L.ngrid);
+            launch_pdl(h->pdl, fwd_narrow_finish_kernel<CB, CBF, NOUT>, A.n_out * CB, 32, h->stream, A, L.ngrid);
             SMLP_CK_LAUNCH(h, "fwd_narrow_finish_kernel");
         } else {
             if constexpr (NOUT <= 16) {
                 if (L.dense) {
                     const int64_t tiles = (A.n_in + 31) / 32;
                     const int64_t blocks = std::min<int64_t>((tiles + NARROW_WARPS - 1) / NARROW_WARPS, (int64_t)h->num_sms * 4);
-                    bwd_narrow_rows_kernel<CB, CBF, NOUT>
-                        <<<(int)std::max<int64_t>(1, blocks), NARROW_WARPS * 32, 0, h->stream>>>(A);
+                    launch_pdl(h->pdl, bwd_narrow_rows_kernel<CB, CBF, NOUT>, (int)std::max<int64_t>(1, blocks), NARROW_WARPS * 32, h->stream, A);
                     SMLP_CK_LAUNCH(h, "bwd_narrow_rows_kernel");
                     return SMLP_OK;
                 }
@@ -2052,7 +2078,7 @@ int launch_narrow_n(smlp_handle* h, const NarrowArgs& A, const Layer& L, bool fw
             constexpr int RU = VEC == 4 ? 2 : (VEC == 2 ? 4 : 8);
             const int64_t warps = (A.n_in + RU - 1) / RU;
             const int64_t blocks = std::min<int64_t>((warps + NARROW_WARPS - 1) / NARROW_WARPS, (int64_t)h->num_sms * 3);
-            bwd_narrow_kernel<CB, CBF, NOUT><<<(int)std::max<int64_t>(1, blocks), NARROW_WARPS * 32, 0, h->stream>>>(A);
+            launch_pdl(h->pdl, bwd_narrow_kernel<CB, CBF, NOUT>, (int)std::max<int64_t>(1, blocks), NARROW_WARPS * 32, h->stream, A);
             SMLP_CK_LAUNCH(h, "bwd_narrow_kernel");
         }
         return SMLP_OK;
@@ -2098,13 +2124,13 @@ uint32_t drop_threshold(float rate) {
 
 int refresh_mirror_values(smlp_handle* h, Layer& Ly) {
     if (Ly.cap == 0) return SMLP_OK;
-    mirror_values_kernel<<<launch_grid(h, (Ly.cap + 3) / 4, 256), 256, 0, h->stream>>>(Ly.val, Ly.mperm, Ly.meta, Ly.mval);
+    launch_pdl(h->pdl, mirror_values_kernel, launch_grid(h, (Ly.cap + 3) / 4, 256), 256, h->stream, Ly.val, Ly.mperm, Ly.meta, Ly.mval);
     SMLP_CK_LAUNCH(h, "mirror_values_kernel");
     return SMLP_OK;
 }
 
 int run_probs(smlp_handle* h, int B, float* probs) {
-    softmax_probs_kernel<<<(B + 127) / 128, 128, 0, h->stream>>>(h->act[h->L], probs, h->sizes[h->L - 1], B, h->CBf);
+    launch_pdl(h->pdl, softmax_probs_kernel, (B + 127) / 128, 128, h->stream, h->act[h->L], probs, h->sizes[h->L - 1], B, h->CBf);
     SMLP_CK_LAUNCH(h, "softmax_probs_kernel");
     return SMLP_OK;
 }
@@ -2144,17 +2170,15 @@ int launch_bits(smlp_handle* h, const BitsArgs& A, const Layer& L2, bool fwd) {
     if (fwd) {
         // units are grid-strided: one resident wave (blocks/SM from the occupancy calculator)
         if (A.dropout_on)
-            fwd_bits_kernel<CB, true><<<rows_grid(h, fwd_bits_kernel<CB, true>, units), WARPS_PER_BLOCK * 32, 0,
-                                        h->stream>>>(A);
+            launch_pdl(h->pdl, fwd_bits_kernel<CB, true>, rows_grid(h, fwd_bits_kernel<CB, true>, units), WARPS_PER_BLOCK * 32, h->stream, A);
         else
-            fwd_bits_kernel<CB, false><<<rows_grid(h, fwd_bits_kernel<CB, false>, units), WARPS_PER_BLOCK * 32, 0,
-                                         h->stream>>>(A);
+            launch_pdl(h->pdl, fwd_bits_kernel<CB, false>, rows_grid(h, fwd_bits_kernel<CB, false>, units), WARPS_PER_BLOCK * 32, h->stream, A);
         SMLP_CK_LAUNCH(h, "fwd_bits_kernel");
     } else {
         const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((L2.n_out + 8 * WARPS_PER_BLOCK - 1) /
                                                                      (8 * WARPS_PER_BLOCK),
                                                                  (int64_t)h->num_sms * 8));
-        bwd_bits_rows_kernel<CB><<<g2, WARPS_PER_BLOCK * 32, 0, h->stream>>>(A);
+        launch_pdl(h->pdl, bwd_bits_rows_kernel<CB>, g2, WARPS_PER_BLOCK * 32, h->stream, A);
         SMLP_CK_LAUNCH(h, "bwd_bits_rows_kernel");
     }
     return SMLP_OK;
@@ -2196,8 +2220,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
         const int vec = (h->sizes[0] % 4 == 0) && ((uintptr_t)x % 16 == 0);
         prof_start(h, K_STAGE, 1, 8.0 * (double)B * (double)h->sizes[0], 0.0);
         if (h->xbits) SMLP_CK(h, cudaMemsetAsync(h->d_nonbinary, 0, sizeof(int32_t), h->stream));
-        stage_input_kernel<<<grid, dim3(32, 32), 0, h->stream>>>(x, x_idx, B, nchunks, CB, h->sizes[0], h->act[1],
-                                                                 h->xbits, h->d_nonbinary, vec);
+        launch_pdl(h->pdl, stage_input_kernel, grid, dim3(32, 32), h->stream, x, x_idx, B, nchunks, CB, h->sizes[0], h->act[1], h->xbits, h->d_nonbinary, vec);
         SMLP_CK_LAUNCH(h, "stage_input_kernel");
         prof_stop(h);
     }
@@ -2300,9 +2323,9 @@ static int launch_update(smlp_handle* h, cudaStream_t stream, int64_t lo, int64_
     const float lr = sgd->lr, mu = sgd->momentum, wd = sgd->weight_decay, gs = sgd->grad_scale;
     const int64_t n = hi - lo;
     if (g2)
-        sgd_update4_kernel<true><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs);
+        launch_pdl(h->pdl, sgd_update4_kernel<true>, grid, threads, stream, w, v, g, gb, n, lr, mu, wd, decay_end, gs);
     else
-        sgd_update4_kernel<false><<<grid, threads, 0, stream>>>(w, v, g, gb, n, lr, mu, wd, decay_end, gs);
+        launch_pdl(h->pdl, sgd_update4_kernel<false>, grid, threads, stream, w, v, g, gb, n, lr, mu, wd, decay_end, gs);
     SMLP_CK_LAUNCH(h, "sgd_update4_kernel");
     return SMLP_OK;
 }
@@ -2345,7 +2368,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
         S.CB = CB;
         S.CBf = h->CBf;
         prof_start(h, K_SOFTMAX, L, 8.0 * (double)B * (double)S.nL, 0.0);
-        softmax_ce_kernel<<<1, 512, 0, h->stream>>>(S);
+        launch_pdl(h->pdl, softmax_ce_kernel, 1, 512, h->stream, S);
         SMLP_CK_LAUNCH(h, "softmax_ce_kernel");
         prof_stop(h);
     }
@@ -2438,8 +2461,7 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
         SMLP_TRY(dispatch_bits(h, A, L2, false));
         prof_stop(h);
         prof_start(h, K_LAYER_UPDATE, 2, 12.0 * nnz, 0.0);
-        grad_from_mirror_kernel<<<launch_grid(h, L2.cap, 256), 256, 0, h->stream>>>(h->d_nonbinary, h->gmirror2,
-                                                                                    L2.minv, L2.grad, L2.meta);
+        launch_pdl(h->pdl, grad_from_mirror_kernel, launch_grid(h, L2.cap, 256), 256, h->stream, h->d_nonbinary, h->gmirror2, L2.minv, L2.grad, L2.meta);
         SMLP_CK_LAUNCH(h, "grad_from_mirror_kernel");
         prof_stop(h);
         SMLP_TRY(layer_done(h, 2));
@@ -2472,7 +2494,7 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
         if (nl > 0) {
             const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((cmax + 255) / 256, h->num_sms * 4)),
                             (unsigned)nl);
-            mirror_values_multi_kernel<<<grid, 256, 0, h->stream>>>(M);
+            launch_pdl(h->pdl, mirror_values_multi_kernel, grid, 256, h->stream, M);
             SMLP_CK_LAUNCH(h, "mirror_values_multi_kernel");
         }
         prof_stop(h);

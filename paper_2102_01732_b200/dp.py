@@ -112,18 +112,48 @@ def dp_train_step(model, X, Y, idx, step: int, lr: float, momentum: float, weigh
 
 class OverlappedAllreduce:
     """X1 with the communication overlapped on the backward: after an UNFUSED
-    backward is enqueued, each layer's slice of the grad view is SUM-allreduced on a side stream as
-    soon as the library's per-layer event says that gradient is final -- the output layer first,
-    while the backward of the layers below is still running -- then the bias block; the caller's
-    stream waits for all of them before the Eq. 1 update.  Every rank issues the same collectives
-    in the same order (same topology and layout), so the reduction is the plain value allreduce."""
+    backward is enqueued, the grad view is SUM-allreduced bucket by bucket on a side stream, each
+    bucket as soon as the library's per-layer event says its last layer's gradient is final -- the
+    output layer first, while the backward of the layers below is still running.  A bucket is a
+    run of consecutive weight layers W^(L), W^(L-1), ... (contiguous in the view) of at least
+    `bucket_bytes`; the bucket holding W^(2) also takes the bias block b_2..b_L, which is final once
+    W^(2)'s backward ran (and is contiguous with it when that bucket spans every layer).  Small
+    models (C4's 0.22 MB view) thus make ONE collective per step -- latency, not bandwidth, is
+    their cost -- and C5 one per layer (215 MB: the overlap pays).  The caller's stream waits for
+    all of them before the Eq. 1 update.  Every rank issues the same collectives in the same order
+    (same topology and layout), so the reduction is the plain value allreduce.  Everything is
+    stream-ordered (events, no host sync), so the step can be captured in a CUDA graph, NCCL
+    collectives included."""
 
-    def __init__(self, model, group=None):
+    def __init__(self, model, group=None, bucket_bytes: int = 4 << 20):
         import torch
         self.m = model
         self.group = group
         self.stream = torch.cuda.Stream(device=model.device) if torch.cuda.is_available() else None
         self.layout, self.bias_base = model.view_layout()
+        self.buckets = self.plan(self.layout, self.bias_base, model.L, bucket_bytes)
+
+    @staticmethod
+    def plan(layout, bias_base: int, L: int, bucket_bytes: int):
+        """[(wait_layer, lo, hi)]: slices [lo, hi) of the grad view in issue order; a slice is
+        final once layer wait_layer's backward has run (host-only arithmetic on the layout)."""
+        out, l = [], L
+        while l >= 2:
+            top = l
+            off, cap = layout[l - 2]
+            hi = off + cap
+            lo, nbytes = off, 4 * cap
+            while nbytes < bucket_bytes and l > 2:     # extend downwards (contiguous in the view)
+                l -= 1
+                off, cap = layout[l - 2]
+                lo, nbytes = off, nbytes + 4 * cap
+            if l == 2 and top == L:                       # every layer: one slice through the biases
+                out.append((2, lo, None))
+                return out
+            out.append((l, lo, hi))
+            l -= 1
+        out.append((2, bias_base, None))                  # b_2..b_L
+        return out
 
     def __call__(self, reduce=None):
         """reduce(tensor_slice) -> work handle (default: torch.distributed.all_reduce SUM, async)."""
@@ -135,14 +165,12 @@ class OverlappedAllreduce:
         g, _ = self.m.grad_view()
         works = []
         main = torch.cuda.current_stream()
-        # no blanket wait on the main stream: each slice waits only for its own layer's event, so
+        # no blanket wait on the main stream: each bucket waits only for its own layer's event, so
         # the collectives overlap the rest of the backward
         with torch.cuda.stream(self.stream):
-            for l in range(self.m.L, 1, -1):                 # W^(L) is final first
+            for l, lo, hi in self.buckets:
                 self.m.wait_layer(l, self.stream)
-                off, cap = self.layout[l - 2]
-                works.append(reduce(g[off:off + cap]))
-            works.append(reduce(g[self.bias_base:]))         # b_2..b_L: final once W^(2)'s backward ran
+                works.append(reduce(g[lo:hi]))
         for w in works:
             if w is not None:
                 w.wait()                                     # the current stream waits for the collective

@@ -120,3 +120,33 @@ def test_dp_plumbing_world_size_2_gloo():
         # differ by one rounding: fp32 gloo SUM vs the oracle's fp64 sum rounded once)
         assert out[r]["dp_err"] < 1e-6
         assert out[r]["dp_identical"] is True
+
+
+@pytest.mark.parametrize("bucket_bytes", [1, 4 << 20, 100 << 20, 1 << 40])
+def test_overlapped_allreduce_buckets_cover_the_view_once(bucket_bytes):
+    """OverlappedAllreduce.plan (host logic): the buckets are disjoint slices covering the whole
+    grad view [0, param_count) exactly once, issued output layer first; a bucket waits for the
+    lowest layer it holds; every bucket but the one reaching W^(2) holds >= bucket_bytes."""
+    from paper_2102_01732_b200.dp import OverlappedAllreduce
+    for caps in ([10304, 20000, 20000, 2016], [11310720, 20000000, 20000000, 1000000], [9000, 5000, 5000, 800]):
+        L = len(caps) + 1
+        layout, off = [], 0
+        for c in caps:
+            layout.append((off, c))
+            off += (c + 31) // 32 * 32
+        bias_base, total = off, off + 1000
+        plan = OverlappedAllreduce.plan(layout, bias_base, L, bucket_bytes)
+        cover = np.zeros(total, np.int32)
+        for l, lo, hi in plan:
+            cover[lo:(total if hi is None else hi)] += 1
+        assert cover.max() == 1                           # disjoint
+        for off_l, c in layout:                           # every value of every layer, once
+            assert cover[off_l:off_l + c].min() == 1
+        assert cover[bias_base:].min() == 1               # and the bias block
+        waits = [l for l, _, _ in plan]
+        assert waits == sorted(waits, reverse=True) and waits[-1] == 2
+        for l, lo, hi in plan[:-1]:
+            if l > 2 and hi is not None:
+                assert 4 * (hi - lo) >= bucket_bytes
+        if bucket_bytes >= 4 * total:
+            assert plan == [(2, 0, None)]                # one collective of the whole view

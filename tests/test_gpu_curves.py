@@ -43,8 +43,11 @@ def _oracle_curve(cfg, st, X, Y, epochs):
 
 
 @pytest.mark.parametrize("name,n", [("C1", None), ("C2", 2_560), ("C3", 160), ("C4", 12_800)])
-def test_loss_curves_5_epochs(name, n):
+def test_loss_curves_5_epochs(name, n, monkeypatch):
     import torch
+    # loss curves compare losses only: the oracle's R24 error magnitudes (per-step parity
+    # instrumentation) are switched off; over thousands of steps they only grow
+    monkeypatch.setattr(M, "INSTRUMENT", False)
     from paper_2102_01732_b200.trainer import Trainer
     cfg = get_config(name) if n is None else get_config(name, n_samples=n)
     X, Y = make_dataset(cfg, n=cfg.n_samples)

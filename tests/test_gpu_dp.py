@@ -66,12 +66,12 @@ def _worker(rank, K, port, mode, q):
                                        to_dev)
         D.init_process_group(backend="gloo")
         assert dist.get_world_size() == K and dist.get_rank() == rank
-        cfg = get_config("C1", dropout=0.2)
+        cfg = get_config("C1", dropout=0.2, n_samples=8000)
         B = cfg.batch
         g = SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed,
                       rank, B)
         st = M.create(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init, cfg.model_seed)
-        X, Y = make_dataset(cfg, n=2000)
+        X, Y = make_dataset(cfg, n=8000)        # candidate pool: (3 + 1) x K kink-free batches
         ov = D.OverlappedAllreduce(g) if mode == "overlap" else None
         nxt = 0
         # ---- synchronous steps (WASSP phase 1)
@@ -93,6 +93,8 @@ def _worker(rank, K, port, mode, q):
             load_oracle_state_into_gpu(g, st)        # the next step from identical inputs (per-step parity)
         # ---- Eq. 2 averaging after divergent local steps (phase 2 without a per-step collective)
         states = [st.copy() for _ in range(K)]
+        for k in range(K):                       # replica k draws the dropout stream of rank k
+            states[k].rank = k
         batches, nxt = _kink_free_batches(st, X, Y, B, K, 3, nxt)
         sgd = SGD(cfg.lr * 10, cfg.momentum, cfg.weight_decay)
         for k in range(K):
@@ -167,6 +169,83 @@ def test_dp_k_ranks_on_one_gpu_match_the_oracle(K, mode):
     out = dict(q.get(timeout=600) for _ in range(K))
     for p in ps:
         p.join(timeout=120)
-    for r in range(K):
-        assert "error" not in out[r], out[r].get("error")
-        assert out[r]["ok"]
+    errs = {r: out[r]["error"] for r in range(K) if "error" in out[r]}
+    # a rank whose peer failed first only reports the closed connection: show the root cause first
+    root = sorted(errs.items(), key=lambda kv: "Connection closed" in kv[1])
+    assert not errs, "\n".join(f"rank {r}: {e}" for r, e in root)
+    assert all(out[r]["ok"] for r in range(K))
+
+
+def _graph_worker(port, q):
+    """One NCCL rank (world size 1: the collective is a real NCCL launch) -- the DP step (forward,
+    unfused backward, bucketed OverlappedAllreduce on its side stream, Eq. 1 with 1/K) captured in
+    ONE CUDA graph with its NCCL collectives, replayed, and compared bit for bit with the same
+    steps run eagerly on a second replica."""
+    try:
+        import torch
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+        torch.cuda.set_device(0)
+        from paper_2102_01732_b200 import SGD, SparseMLP
+        from paper_2102_01732_b200 import dp as D
+        from synth import get_config, make_dataset
+        dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+        cfg = get_config("C1", dropout=0.2)
+        B = cfg.batch
+        X, Y = make_dataset(cfg, n=4 * B)
+        Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y.astype(np.int32)).cuda()
+        idx = torch.arange(4 * B, dtype=torch.int32, device="cuda")
+        sgd = SGD(cfg.lr * 5, cfg.momentum, cfg.weight_decay, 1.0)
+        mk = lambda: SparseMLP(cfg.sizes, cfg.epsilon, cfg.activation, cfg.alpha, cfg.dropout, cfg.init,
+                               cfg.model_seed, 0, B)
+        ge, gg = mk(), mk()
+        ove, ovg = D.OverlappedAllreduce(ge), D.OverlappedAllreduce(gg)
+        assert len(ovg.buckets) == 1                      # C1's 0.08 MB view: one collective per step
+
+        def step(g, ov, iw, s):
+            g.forward(Xd, x_idx=iw, train=True, step=s)
+            g.backward(Yd, y_idx=iw, fused=None)
+            ov()
+            g.step(sgd)
+
+        for s in range(2):                                # eager warm-up of both (NCCL communicator up)
+            step(ge, ove, idx[s * B:(s + 1) * B], s)
+            step(gg, ovg, idx[s * B:(s + 1) * B], s)
+        torch.cuda.synchronize()
+        win = torch.zeros(B, dtype=torch.int32, device="cuda")
+        counter = torch.zeros(1, dtype=torch.int64, device="cuda")
+        gg.sparse_mlp_set_step_counter(counter)
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(graph, stream=cs):
+                step(gg, ovg, win, 0)
+                gg.join()
+        torch.cuda.current_stream().wait_stream(cs)
+        for s in range(2, 4):
+            win.copy_(idx[s * B:(s + 1) * B])
+            counter.fill_(s)
+            graph.replay()
+            step(ge, ove, idx[s * B:(s + 1) * B], s)
+        torch.cuda.synchronize()
+        gg.sparse_mlp_set_step_counter(None)
+        pe, _ = ge.param_view()
+        pg, _ = gg.param_view()
+        assert torch.equal(pe.view(torch.int32), pg.view(torch.int32)), "graph replay differs from eager"
+        q.put({"ok": True})
+        dist.destroy_process_group()
+    except BaseException as e:  # surfaced by the parent
+        import traceback
+        q.put({"error": traceback.format_exc() + repr(e)})
+
+
+def test_dp_step_with_nccl_collectives_in_a_cuda_graph():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_graph_worker, args=(_free_port(), q))
+    p.start()
+    out = q.get(timeout=600)
+    p.join(timeout=120)
+    assert "error" not in out, out.get("error")

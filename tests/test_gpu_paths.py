@@ -438,9 +438,10 @@ def test_pipelined_host_step_matches_sync():
 
 
 def test_overlapped_dp_path_matches_fused_on_one_rank():
-    """The K > 1 step structure on one GPU: unfused backward, per-layer grad slices released by the
-    library's layer events to a side stream (identity 'allreduce'), Eq. 1 update kernel + mirror
-    refresh -- the same trajectory as the fused 1-GPU step (up to the update's rounding)."""
+    """The K > 1 step structure on one GPU: unfused backward, per-layer grad slices (output layer
+    first, then the bias block) released by the library's layer events to a side stream (identity
+    'allreduce'), Eq. 1 update kernel + mirror refresh -- the same trajectory as the fused 1-GPU
+    step (up to the update's rounding)."""
     from paper_2102_01732_b200 import SGD, SparseMLPError
     from paper_2102_01732_b200.dp import OverlappedAllreduce
     torch = _torch()
@@ -451,7 +452,8 @@ def test_overlapped_dp_path_matches_fused_on_one_rank():
     with pytest.raises(SparseMLPError, match="E_STATE"):
         g2.wait_layer(2, side)                            # no backward recorded yet
     X, Y = _binary_data(3 * 64, cfg.sizes[0], seed=5)
-    ov = OverlappedAllreduce(g2)
+    ov = OverlappedAllreduce(g2, bucket_bytes=1)          # one bucket per layer (then the biases)
+    assert len(OverlappedAllreduce(g2).buckets) == 1        # default: a small view is one collective
     layout, bb = g2.view_layout()
     assert layout[0][0] == 0 and all(o2 >= o1 + c1 for (o1, c1), (o2, _) in zip(layout, layout[1:]))
     seen = []
@@ -465,7 +467,7 @@ def test_overlapped_dp_path_matches_fused_on_one_rank():
         ov(reduce=lambda t: seen.append(t.numel()))
         g2.step(sgd)
     torch.cuda.synchronize()
-    assert seen[:cfg.n_layers - 1] == [c for _, c in reversed(layout)]   # output layer first
+    assert seen[:cfg.n_layers] == [c for _, c in reversed(layout)] + [g2.info()["param_count"] - bb]
     for l in range(2, cfg.n_layers + 1):
         a, b = g1.export_layer(l), g2.export_layer(l)
         assert np.array_equal(a["col"], b["col"])

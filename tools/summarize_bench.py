@@ -1,6 +1,9 @@
 """Print a compact per-kernel summary of bench.py JSON lines (one file per argument)."""
 import json
+import signal
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)   # quiet under `| head`
 
 for path in sys.argv[1:]:
     try:
