@@ -74,6 +74,11 @@ static void prof_record(smlp_handle* h, cudaEvent_t e) {
 }
 
 void prof_start(smlp_handle* h, int kind, int layer, double bytes, double flops) {
+    if (h->rec) {            // recording a persistent step: its launch is timed as one record
+        h->rec_bytes += bytes;
+        h->rec_flops += flops;
+        return;
+    }
     if (!h->prof) return;
     ProfRec r{kind, layer, nullptr, nullptr, bytes, flops};
     for (cudaEvent_t* e : {&r.a, &r.b}) {
@@ -89,7 +94,7 @@ void prof_start(smlp_handle* h, int kind, int layer, double bytes, double flops)
 }
 
 void prof_stop(smlp_handle* h) {
-    if (!h->prof || h->prof_recs.empty()) return;
+    if (h->rec || !h->prof || h->prof_recs.empty()) return;
     prof_record(h, h->prof_recs.back().b);
 }
 
@@ -166,6 +171,13 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
     // programmatic dependent launch for the launch-bound small models only (measured
     // C4 / C3 -2..5%, C5 +12% per step)
     h->pdl = off <= SMALL_MODEL_PARAMS ? 1 : 0;
+    h->gbar = zalloc<unsigned>(h, 2 + (size_t)h->num_sms, &rc);   // barrier [count, gen] + per-SM slot counters
+    // persistent step: built and bit-identical to the per-kernel path, but measured
+    // 1.4-1.9x slower than the CUDA-graph replay of the per-kernel step on C1-C4, so it is opt-in:
+    // SMLP_PERSIST=1 (small models whose forward and backward tensors share one chunk width)
+    h->persist = 0;
+    if (const char* e = std::getenv("SMLP_PERSIST"))
+        h->persist = (std::atoi(e) != 0 && off <= SMALL_MODEL_PARAMS && h->CB == h->CBf && h->CB >= 8) ? 1 : 0;
     h->param = zalloc<float>(h, (size_t)off, &rc);
     h->mom = zalloc<float>(h, (size_t)off, &rc);
     h->grad = zalloc<float>(h, (size_t)off, &rc);
@@ -485,10 +497,9 @@ int sparse_mlp_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_
         // then one streaming Eq. 1 pass over the whole view (grad_scale 1) and the mirror refresh
         smlp_sgd f = *fused;
         f.grad_scale = 1.f;
-        rc = run_backward(h, labels, y_idx, loss, true);
-        if (rc == SMLP_OK) rc = run_step(h, &f);
+        rc = run_backward_step(h, labels, y_idx, loss, &f);
     } else {
-        rc = run_backward(h, labels, y_idx, loss, false);
+        rc = run_backward_step(h, labels, y_idx, loss, nullptr);
     }
     if (rc == SMLP_OK) {
         h->grads_pending = fused == nullptr;

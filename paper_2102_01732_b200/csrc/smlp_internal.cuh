@@ -96,7 +96,8 @@ struct Alloc {
 };
 
 enum KernelKind { K_STAGE = 0, K_FWD = 1, K_FWD_FINISH = 2, K_SOFTMAX = 3, K_BWD = 4, K_BWD_FINISH = 5, K_SGD = 6,
-                  K_FWD_BITS = 7, K_BWD_BITS = 8, K_LAYER_UPDATE = 9, K_MIRROR = 10 };
+                  K_FWD_BITS = 7, K_BWD_BITS = 8, K_LAYER_UPDATE = 9, K_MIRROR = 10, K_PERSIST_FWD = 11,
+                  K_PERSIST_BWD = 12 };
 
 struct ProfRec {
     int kind, layer;
@@ -171,6 +172,10 @@ struct smlp_handle {
     std::vector<cudaEvent_t> ev_pool;
     int num_sms = 148;
     int pdl = 0;                    // launch the step's kernels with programmatic serialization
+    int persist = 0;                // small models: every forward / backward call is one persistent launch
+    void* rec = nullptr;            // persistent step: the phase recorder while a call records (step.cu)
+    unsigned* gbar = nullptr;       // persistent step: grid barrier [count, generation], then per-SM slot counters
+    double rec_bytes = 0.0, rec_flops = 0.0;   // ... and the algorithmic bytes / flops of its phases
     // tuning knobs (env, read at create; each selects between kernels the parity tests cover)
     int narrow_sparse_bwd = 0;      // SMLP_NARROW_SPARSE_BWD: narrow row-streaming backward also for a sparse output layer
     int64_t short_min_rows = -1;    // SMLP_SHORT_MIN_ROWS: -1 = one 32-row unit per resident warp
@@ -347,6 +352,8 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
 // the gradient of the current trace into the grad view (split_last: a large model's last chunk
 // into grad2, added by the Eq. 1 pass that follows in the same call)
 int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, bool split_last);
+// backward (+ the fused Eq. 1 pass when fused != null); one persistent launch for small models
+int run_backward_step(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, const smlp_sgd* fused);
 int run_step(smlp_handle* h, const smlp_sgd* sgd);
 int refresh_mirror_values(smlp_handle* h, Layer& Ly);
 

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 
 #include "smlp_internal.cuh"
 
@@ -125,36 +126,56 @@ __device__ __forceinline__ int4 ldi4_hint(const int32_t* p, uint64_t pol) {
 __device__ __forceinline__ uint64_t gather_policy(int hint) { return hint ? policy_evict_last() : policy_evict_normal(); }
 __device__ __forceinline__ uint64_t stream_policy(int hint) { return hint ? policy_evict_first() : policy_evict_normal(); }
 
+// Virtual grid of a kernel body ("persistent step"): every kernel of the step is a
+// __device__ body run by 256-thread blocks with explicit block coordinates, called once by its
+// own __global__ wrapper (vg = blockIdx / gridDim) or, for small models, by the persistent step
+// kernel for each of the phase's virtual blocks in turn; shared memory comes from the caller.
+struct VGrid {
+    int bx, by, gx;
+};
+__device__ __forceinline__ VGrid hw_grid() { return VGrid{(int)blockIdx.x, (int)blockIdx.y, (int)gridDim.x}; }
+
 // ------------------------------------------------------------------------------------------
 // a1: input staging (transpose + optional row gather), zero padding of columns b >= B
 // ------------------------------------------------------------------------------------------
-// 32 batch rows x 128 features per 1024-thread block: float4 loads along the features (scalar
-// when n_1 or x is not 16-B aligned), a shared-memory transpose (feature 4t + k stored at column
-// 32k + t: conflict-free both ways), then per feature one coalesced row of the chunk layout and
-// one 32-bit word of the bit-packed input
-__global__ void __launch_bounds__(1024) stage_input_kernel(const float* __restrict__ x, const int32_t* __restrict__ x_idx,
-                                                           int B, int nchunks, int CB, int64_t n1,
-                                                           float* __restrict__ act1, uint32_t* __restrict__ xbits,
-                                                           int32_t* __restrict__ nonbinary, int vec) {
-    SMLP_PDL_ENTRY();
-    __shared__ float tile[32][129];
-    const int64_t f0 = (int64_t)blockIdx.x * 128;
-    const int b0 = blockIdx.y * 32;
-    const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 32
-    {
+// 32 batch rows x 128 features per block of 256 threads (8 warps x 4 sub-rows = 32 batch rows):
+// float4 loads along the features (scalar when n_1 or x is not 16-B aligned), a shared-memory
+// transpose (feature 4t + k stored at column 32k + t: conflict-free both ways), then per feature
+// one coalesced row of the chunk layout and one 32-bit word of the bit-packed input
+struct StageArgs {
+    const float* x;
+    const int32_t* x_idx;
+    int B, nchunks, CB;
+    int64_t n1;
+    float* act1;
+    uint32_t* xbits;
+    int32_t* nonbinary;
+    int vec;
+};
+struct StageSmem {
+    float tile[32][129];
+};
+__device__ __forceinline__ void stage_input_body(const StageArgs& S, const VGrid vg, StageSmem& sm) {
+    auto& tile = sm.tile;
+    const int64_t f0 = (int64_t)vg.bx * 128;
+    const int b0 = vg.by * 32;
+    const int tx = threadIdx.x & 31;
+#pragma unroll
+    for (int sub = 0; sub < 4; ++sub) {
+        const int ty = sub * 8 + (threadIdx.x >> 5);
         const int b = b0 + ty;
         const int64_t f = f0 + 4 * tx;
         float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (b < B) {
-            const int64_t row = x_idx ? (int64_t)__ldg(x_idx + b) : (int64_t)b;
-            const float* p = x + row * n1 + f;
-            if (vec && f + 3 < n1) {
+        if (b < S.B) {
+            const int64_t row = S.x_idx ? (int64_t)__ldg(S.x_idx + b) : (int64_t)b;
+            const float* p = S.x + row * S.n1 + f;
+            if (S.vec && f + 3 < S.n1) {
                 const float4 t = ldg4(p);
                 v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
             } else {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    if (f + k < n1) v[k] = __ldg(p + k);
+                    if (f + k < S.n1) v[k] = __ldg(p + k);
             }
         }
 #pragma unroll
@@ -163,25 +184,34 @@ __global__ void __launch_bounds__(1024) stage_input_kernel(const float* __restri
     __syncthreads();
     const int b = b0 + tx;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int fl = ty + 32 * r;                       // warp-uniform local feature
-        const int64_t f = f0 + fl;
-        const float v = tile[tx][32 * (fl & 3) + (fl >> 2)];
-        if (f < n1 && b < nchunks * CB) {
-            const int c = b / CB, lb = b % CB;
-            act1[((int64_t)c * n1 + f) * CB + lb] = v;
-        }
-        if (xbits) {
-            // the warp holds feature f over batch b0..b0+31: one 32-bit word of the bit-packed
-            // input (bit b%32 = x[b][f] != 0) for the exact binary-input path of layer 2
-            const unsigned word = __ballot_sync(FULL, v != 0.f);
-            const bool nb = __any_sync(FULL, v != 0.f && v != 1.f);
-            if (tx == 0 && f < n1) {
-                xbits[f * XBITS_WORDS + blockIdx.y] = word;
-                if (nb) atomicOr(nonbinary, 1);
+    for (int sub = 0; sub < 4; ++sub) {
+        const int ty = sub * 8 + (threadIdx.x >> 5);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int fl = ty + 32 * r;                       // warp-uniform local feature
+            const int64_t f = f0 + fl;
+            const float v = tile[tx][32 * (fl & 3) + (fl >> 2)];
+            if (f < S.n1 && b < S.nchunks * S.CB) {
+                const int c = b / S.CB, lb = b % S.CB;
+                S.act1[((int64_t)c * S.n1 + f) * S.CB + lb] = v;
+            }
+            if (S.xbits) {
+                // the warp holds feature f over batch b0..b0+31: one 32-bit word of the bit-packed
+                // input (bit b%32 = x[b][f] != 0) for the exact binary-input path of layer 2
+                const unsigned word = __ballot_sync(FULL, v != 0.f);
+                const bool nb = __any_sync(FULL, v != 0.f && v != 1.f);
+                if (tx == 0 && f < S.n1) {
+                    S.xbits[f * XBITS_WORDS + vg.by] = word;
+                    if (nb) atomicOr(S.nonbinary, 1);
+                }
             }
         }
     }
+}
+__global__ void __launch_bounds__(256) stage_input_kernel(StageArgs S) {
+    SMLP_PDL_ENTRY();
+    __shared__ StageSmem sm;
+    stage_input_body(S, hw_grid(), sm);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -262,13 +292,12 @@ __device__ __forceinline__ void fwd_epilogue(const FwdArgs& A, int64_t j, float4
 
 
 template <int CB>
-__global__ void __launch_bounds__(256) fwd_finish_kernel(FwdArgs A) {
-    SMLP_PDL_ENTRY();
+__device__ __forceinline__ void fwd_finish_body(const FwdArgs& A, const VGrid vg) {
     constexpr int G = CB / 4, P = 32 / G;
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int warp = (vg.bx * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (vg.gx * blockDim.x) >> 5;
     const int nm = A.meta->n_fmulti;
     const uint32_t step_lo = A.step_ptr ? (uint32_t)(*A.step_ptr) : A.step_lo;
     for (int r0 = warp * P; r0 < nm; r0 += nwarps * P) {
@@ -282,6 +311,11 @@ __global__ void __launch_bounds__(256) fwd_finish_kernel(FwdArgs A) {
         }
         fwd_epilogue<CB>(A, m.x, acc, active, lane, step_lo);
     }
+}
+template <int CB>
+__global__ void __launch_bounds__(256) fwd_finish_kernel(FwdArgs A) {
+    SMLP_PDL_ENTRY();
+    fwd_finish_body<CB>(A, hw_grid());
 }
 
 // ------------------------------------------------------------------------------------------
@@ -497,18 +531,21 @@ __device__ __forceinline__ void stage_window(int2* win, const int (&ix)[NW], con
 }
 
 template <int CB>
-__global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(FwdArgs A) {
-    SMLP_PDL_ENTRY();
+struct FwdRowsSmem {
+    int2 win_all[WARPS_PER_BLOCK][RowCfg<CB, true>::WIN];
+};
+template <int CB>
+__device__ __forceinline__ void fwd_rows_body(const FwdArgs& A, const VGrid vg, FwdRowsSmem<CB>& sm) {
     using C = RowCfg<CB, true>;
     constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB;
-    __shared__ int2 win_all[WARPS_PER_BLOCK][C::WIN];
+    auto& win_all = sm.win_all;
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
     int2* win = win_all[threadIdx.x >> 5];
     for (int e = SEG_NNZ + lane; e < C::WIN; e += 32) win[e] = make_int2(A.zero_row, 0);   // never-used tail
     const uint64_t pg = gather_policy(A.l2hint);
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t warp = ((int64_t)vg.bx * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)vg.gx * blockDim.x) >> 5;
     const int64_t nseg = A.meta->n_fseg;
     const int64_t s_lo = warp * nseg / nwarps, s_hi = (warp + 1) * nseg / nwarps;
     if (s_lo >= s_hi) return;
@@ -551,6 +588,12 @@ __global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(F
             w[r] = w_n[r];
         }
     }
+}
+template <int CB>
+__global__ void __launch_bounds__(256, RowCfg<CB, true>::MINB) fwd_rows_kernel(FwdArgs A) {
+    SMLP_PDL_ENTRY();
+    __shared__ FwdRowsSmem<CB> sm;
+    fwd_rows_body<CB>(A, hw_grid(), sm);
 }
 
 // Short-row forward (128-column chunks, rows averaging < 16 entries: Table 4's eps <= 5 layers).
@@ -645,14 +688,18 @@ struct SoftmaxArgs {
     float lr, mu;
 };
 
-__global__ void __launch_bounds__(512) softmax_ce_kernel(SoftmaxArgs A) {
-    SMLP_PDL_ENTRY();
-    __shared__ double red[512];
-    const int tid = threadIdx.x;
+// One block of 256 threads standing in for the 512 virtual threads of the loss tree: thread t
+// takes batch columns b = t, t + 512, ... (virtual thread t) and b = t + 256, t + 768, ...
+// (virtual thread t + 256); red[t] = their two fp64 sums is the 512-tree's first level, the rest
+// of the tree follows in the same fixed order.
+struct SoftmaxSmem {
+    double red[256];
+};
+__device__ __forceinline__ double softmax_ce_cols(const SoftmaxArgs& A, int v) {
     double lsum = 0.0;
     const int total = A.nchunks * A.CB;
     const float invB = 1.0f / (float)A.B;
-    for (int b = tid; b < total; b += blockDim.x) {
+    for (int b = v; b < total; b += 512) {
         const int c = b / A.CB, lb = b % A.CB;
         const float* zc = A.logits + (int64_t)(b / A.CBf) * A.nL * A.CBf + b % A.CBf;
         float* dc = A.delta + (int64_t)c * A.nL * A.CB + lb;
@@ -677,15 +724,21 @@ __global__ void __launch_bounds__(512) softmax_ce_kernel(SoftmaxArgs A) {
             dc[j * A.CB] = (p - (j == y ? 1.f : 0.f)) * invB;
         }
     }
-    red[tid] = lsum;
+    return lsum;
+}
+__device__ __forceinline__ void softmax_ce_body(const SoftmaxArgs& A, SoftmaxSmem& sm) {
+    double* red = sm.red;
+    const int tid = threadIdx.x;
+    const double l0 = softmax_ce_cols(A, tid), l1 = softmax_ce_cols(A, tid + 256);
+    red[tid] = l0 + l1;
     __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    for (int s = 128; s > 0; s >>= 1) {
         if (tid < s) red[tid] += red[tid + s];
         __syncthreads();
     }
     if (tid == 0 && A.loss) *A.loss = (float)(red[0] / (double)A.B);
     // output-layer bias gradient gb_L = sum_b delta_L[b, :]
-    for (int64_t j = tid; j < A.nL; j += blockDim.x) {
+    for (int64_t j = tid; j < A.nL; j += 256) {
         float g = 0.f;
         for (int c = 0; c < A.nchunks; ++c) {
             const float* dc = A.delta + ((int64_t)c * A.nL + j) * A.CB;
@@ -693,6 +746,11 @@ __global__ void __launch_bounds__(512) softmax_ce_kernel(SoftmaxArgs A) {
         }
         A.bias_grad[j] = g;
     }
+}
+__global__ void __launch_bounds__(256) softmax_ce_kernel(SoftmaxArgs A) {
+    SMLP_PDL_ENTRY();
+    __shared__ SoftmaxSmem sm;
+    softmax_ce_body(A, sm);
 }
 
 __global__ void softmax_probs_kernel(const float* __restrict__ logits, float* __restrict__ probs, int64_t nL, int B,
@@ -805,13 +863,12 @@ __device__ __forceinline__ void bwd_epilogue(const BwdArgs& A, int64_t i, float4
 
 
 template <int CB, int CBF>
-__global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
-    SMLP_PDL_ENTRY();
+__device__ __forceinline__ void bwd_finish_body(const BwdArgs& A, const VGrid vg) {
     constexpr int G = CB / 4, P = 32 / G;
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int warp = (vg.bx * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (vg.gx * blockDim.x) >> 5;
     const int nm = A.meta->n_bmulti;
     for (int r0 = warp * P; r0 < nm; r0 += nwarps * P) {
         const int r = r0 + g;
@@ -824,6 +881,11 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
         }
         bwd_epilogue<CB, CBF>(A, m.x, acc, active, lane);
     }
+}
+template <int CB, int CBF>
+__global__ void __launch_bounds__(256) bwd_finish_kernel(BwdArgs A) {
+    SMLP_PDL_ENTRY();
+    bwd_finish_body<CB, CBF>(A, hw_grid());
 }
 
 // backward epilogue of one complete input row i (d = sum_j w_ij delta_l[j], identical in every
@@ -951,23 +1013,29 @@ __device__ __forceinline__ void bwd_batch(const float* __restrict__ d_out, const
 }
 
 // GOLD: add the gradient accumulated by earlier chunks; DROP: dropout on layer l-1
+template <int CB>
+struct BwdRowsSmem {
+    static constexpr int RB = RowCfg<CB>::NB < 2 ? RowCfg<CB>::NB : 2;   // batches per reduction round
+    int2 win_all[WARPS_PER_BLOCK][2][SEG_NNZ];
+    __align__(16) float4 ai_all[WARPS_PER_BLOCK][2][RowCfg<CB>::G];
+    __align__(16) float red_all[WARPS_PER_BLOCK][RB * RowCfg<CB>::EB * RowCfg<CB>::S];
+};
 template <int CB, int CBF, bool HAS_DPREV, bool GOLD, bool DROP>
-__global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
-    SMLP_PDL_ENTRY();
+__device__ __forceinline__ void bwd_rows_body(const BwdArgs& A, const VGrid vg, BwdRowsSmem<CB>& sm) {
     using C = RowCfg<CB>;
     constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB, S = C::S, NR = C::NR;
-    constexpr int RB = NB < 2 ? NB : 2;              // batches per reduction round
-    __shared__ int2 win_all[WARPS_PER_BLOCK][2][SEG_NNZ];
-    __shared__ __align__(16) float4 ai_all[WARPS_PER_BLOCK][2][G];
-    __shared__ __align__(16) float red_all[WARPS_PER_BLOCK][RB * EB * S];
+    constexpr int RB = BwdRowsSmem<CB>::RB;
+    auto& win_all = sm.win_all;
+    auto& ai_all = sm.ai_all;
+    auto& red_all = sm.red_all;
     if (A.skip_if_binary && *A.skip_if_binary == 0) return;
     const int lane = threadIdx.x & 31, g = lane / G, q = lane % G;
     const int wib = threadIdx.x >> 5;
     int2 (*win)[SEG_NNZ] = win_all[wib];
     float4 (*ais)[G] = ai_all[wib];
     float* red = red_all[wib];
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t warp = ((int64_t)vg.bx * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)vg.gx * blockDim.x) >> 5;
     const int64_t nseg = A.meta->n_bseg;
     const int64_t s_lo = warp * nseg / nwarps, s_hi = (warp + 1) * nseg / nwarps;
     if (s_lo >= s_hi) return;
@@ -1077,6 +1145,12 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     }
 }
 
+template <int CB, int CBF, bool HAS_DPREV, bool GOLD, bool DROP>
+__global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
+    SMLP_PDL_ENTRY();
+    __shared__ BwdRowsSmem<CB> sm;
+    bwd_rows_body<CB, CBF, HAS_DPREV, GOLD, DROP>(A, hw_grid(), sm);
+}
 
 // ------------------------------------------------------------------------------------------
 // narrow output layer (l = L, n_L <= NARROW_MAX): both passes walk the canonical CSR rows i of
@@ -1161,16 +1235,19 @@ __device__ __forceinline__ void narrow_row(const NarrowArgs& A, bool dense, int6
 // present): one pass over the rows and weights for all of them; column b of the launch is column
 // b % CBF of chunk b / CBF (FwdPos).  Each column's sum runs over the same rows in the same order
 // whatever CB, so the logits do not depend on it.
+template <int CB, int NOUT>
+struct FwdNarrowSmem {
+    float red[NOUT * CB];
+};
 template <int CB, int CBF, int NOUT>
-__global__ void __launch_bounds__(NARROW_WARPS * 32) fwd_narrow_kernel(NarrowArgs A) {
-    SMLP_PDL_ENTRY();
+__device__ __forceinline__ void fwd_narrow_body(const NarrowArgs& A, const VGrid vg, FwdNarrowSmem<CB, NOUT>& sm) {
     constexpr int VEC = CB >= 32 ? CB / 32 : 1;
     constexpr int RU = VEC == 4 ? 4 : 8;
-    __shared__ float red[NOUT * CB];
+    float* red = sm.red;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool colok = lane * VEC < A.ncols;
     const FwdPos<CB, CBF> fp(colok ? lane * VEC : 0, A.n_in);
-    const int64_t r0 = (A.n_in * blockIdx.x) / gridDim.x, r1 = (A.n_in * (blockIdx.x + 1)) / gridDim.x;
+    const int64_t r0 = (A.n_in * vg.bx) / vg.gx, r1 = (A.n_in * (vg.bx + 1)) / vg.gx;
     const bool dense = (int64_t)A.meta->nnz == A.n_in * (int64_t)A.n_out;   // graph-stable (device count)
     float acc[NOUT][VEC];
 #pragma unroll
@@ -1226,15 +1303,19 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) fwd_narrow_kernel(NarrowArg
         }
         __syncthreads();
     }
-    for (int e = threadIdx.x; e < NOUT * CB; e += blockDim.x) A.ws[(int64_t)blockIdx.x * NOUT * CB + e] = red[e];
+    for (int e = threadIdx.x; e < NOUT * CB; e += blockDim.x) A.ws[(int64_t)vg.bx * NOUT * CB + e] = red[e];
+}
+template <int CB, int CBF, int NOUT>
+__global__ void __launch_bounds__(NARROW_WARPS * 32) fwd_narrow_kernel(NarrowArgs A) {
+    SMLP_PDL_ENTRY();
+    __shared__ FwdNarrowSmem<CB, NOUT> sm;
+    fwd_narrow_body<CB, CBF, NOUT>(A, hw_grid(), sm);
 }
 
 // one warp per logit element e = jj * CB + b: fixed-order sum of the CTA partials (lane-strided,
 // then an xor tree) + b_L, stored at column b % CBF of forward chunk b / CBF
 template <int CB, int CBF, int NOUT>
-__global__ void __launch_bounds__(32) fwd_narrow_finish_kernel(NarrowArgs A, int nparts) {
-    SMLP_PDL_ENTRY();
-    const int e = blockIdx.x, lane = threadIdx.x;
+__device__ __forceinline__ void fwd_narrow_finish_body(const NarrowArgs& A, int nparts, int e, int lane) {
     if (e % CB >= A.ncols) return;
     // lane b sums parts b, b + 32, ... in order; the loads of 8 parts are issued together (one
     // latency per 8 parts instead of one per part)
@@ -1255,6 +1336,11 @@ __global__ void __launch_bounds__(32) fwd_narrow_finish_kernel(NarrowArgs A, int
         const int jj = e / CB, b = e % CB;
         A.a_out[((int64_t)(b / CBF) * A.n_out + jj) * CBF + b % CBF] = s + __ldg(A.bias + jj);
     }
+}
+template <int CB, int CBF, int NOUT>
+__global__ void __launch_bounds__(32) fwd_narrow_finish_kernel(NarrowArgs A, int nparts) {
+    SMLP_PDL_ENTRY();
+    fwd_narrow_finish_body<CB, CBF, NOUT>(A, nparts, blockIdx.x, threadIdx.x);
 }
 
 template <int CB, int CBF, int NOUT>
@@ -1370,16 +1456,23 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_kernel(NarrowArg
 // delta_L (n_L x CB) is broadcast from shared memory.  Rows of a dense-capped layer are either
 // complete (j = 0..n_L-1 in order) or empty (outgoing row of a pruned neuron), so entry jj of a
 // row is output jj.  ~10 warp instructions per row instead of ~200 with one row per warp.
+template <int CB, int NOUT>
+struct BwdNarrowRowsSmem {
+    static constexpr int CS = CB < 32 ? CB : 32;     // columns per slice
+    static constexpr int TS = CS + 1;                // odd smem row stride: lane-per-row access is conflict-free
+    float dLs[NOUT][CB];
+    float tile[NARROW_WARPS][32][TS];
+};
 template <int CB, int CBF, int NOUT>
-__global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_rows_kernel(NarrowArgs A) {
-    SMLP_PDL_ENTRY();
+__device__ __forceinline__ void bwd_narrow_rows_body(const NarrowArgs& A, const VGrid vg,
+                                                     BwdNarrowRowsSmem<CB, NOUT>& sm) {
     constexpr int CS = CB < 32 ? CB : 32;     // columns per slice
     constexpr int NS = CB / CS;
     static_assert(CBF % CS == 0, "a slice lies inside one forward chunk");
     constexpr int TS = CS + 1;                // odd smem row stride: lane-per-row access is conflict-free
     constexpr int C4 = CS / 4;                // float4 per row slice
-    __shared__ float dLs[NOUT][CB];
-    __shared__ float tile[NARROW_WARPS][32][TS];
+    auto& dLs = sm.dLs;
+    auto& tile = sm.tile;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     for (int e = threadIdx.x; e < NOUT * CB; e += blockDim.x)
         dLs[e / CB][e % CB] = (e / CB < A.n_out) ? __ldg(A.d_out + e) : 0.f;
@@ -1388,7 +1481,7 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_rows_kernel(Narr
     const bool dense = (int64_t)A.meta->nnz == A.n_in * (int64_t)A.n_out;
     const int64_t ntiles = (A.n_in + 31) / 32;
     float* tl = &tile[wib][0][0];
-    for (int64_t t = (int64_t)blockIdx.x * NARROW_WARPS + wib; t < ntiles; t += (int64_t)gridDim.x * NARROW_WARPS) {
+    for (int64_t t = (int64_t)vg.bx * NARROW_WARPS + wib; t < ntiles; t += (int64_t)vg.gx * NARROW_WARPS) {
         const int64_t r0 = t * 32, i = r0 + lane;
         const bool valid = i < A.n_in;
         int beg = 0, len = 0;
@@ -1471,6 +1564,12 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_rows_kernel(Narr
         }
     }
 }
+template <int CB, int CBF, int NOUT>
+__global__ void __launch_bounds__(NARROW_WARPS * 32) bwd_narrow_rows_kernel(NarrowArgs A) {
+    SMLP_PDL_ENTRY();
+    __shared__ BwdNarrowRowsSmem<CB, NOUT> sm;
+    bwd_narrow_rows_body<CB, CBF, NOUT>(A, hw_grid(), sm);
+}
 
 // ------------------------------------------------------------------------------------------
 // binary-input path of the first weight layer W^(2) (C5's inputs are {0,1}, stored fp32).
@@ -1520,13 +1619,15 @@ struct BitsArgs {
 // then reads, per entry, the one pair holding its 4 columns' bits (broadcast, conflict-free).
 constexpr int BITS_ROWS = 32;
 
+struct FwdBitsSmem {
+    float2 rec[WARPS_PER_BLOCK][32][XBITS_WORDS];
+};
 template <int CB, bool DROP>
-__global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
-    SMLP_PDL_ENTRY();
+__device__ __forceinline__ void fwd_bits_body(const BitsArgs& A, const VGrid vg, FwdBitsSmem& sm) {
     constexpr int G = CB / 4;                       // lanes per chunk
-    __shared__ float2 rec[WARPS_PER_BLOCK][32][XBITS_WORDS];
+    auto& rec = sm.rec;
     if (*A.nonbinary) {
-        if (A.err && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.err, 2);   // promise broken
+        if (A.err && vg.bx == 0 && threadIdx.x == 0) atomicOr(A.err, 2);   // promise broken
         return;
     }
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1534,8 +1635,8 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
     const bool colok = g < A.nchunks;
     const int wsel = lane >> 3, sh = (lane * 4) & 31;
     const uint32_t step_lo = A.step_ptr ? (uint32_t)(*A.step_ptr) : A.step_lo;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t warp = ((int64_t)vg.bx * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)vg.gx * blockDim.x) >> 5;
     const int64_t nunits = (A.n_out + BITS_ROWS - 1) / BITS_ROWS;
     const uint4* xb4 = reinterpret_cast<const uint4*>(A.xbits);
     const float2* myrec = &rec[wib][0][wsel];
@@ -1636,6 +1737,12 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
         while (row < nrows) finish_row();
     }
 }
+template <int CB, bool DROP>
+__global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
+    SMLP_PDL_ENTRY();
+    __shared__ FwdBitsSmem sm;
+    fwd_bits_body<CB, DROP>(A, hw_grid(), sm);
+}
 
 
 // Backward of the binary-input layer, one lane per mirror entry (i -> j): since x[b, i] is 0 or 1,
@@ -1646,15 +1753,16 @@ __global__ void __launch_bounds__(256) fwd_bits_kernel(BitsArgs A) {
 // of 128 bit tests.  Rows are contiguous per warp; the next row's delta and entries are
 // prefetched.  Output: the gradient in mirror order (gmirror), moved to the canonical order by
 // grad_from_mirror_kernel.
+struct BwdBitsSmem {
+    __align__(16) float dsm_all[WARPS_PER_BLOCK][2][32 * XBITS_WORDS];
+};
 template <int CB>
-__global__ void __launch_bounds__(256) bwd_bits_rows_kernel(BitsArgs A) {
-    SMLP_PDL_ENTRY();
-    __shared__ __align__(16) float dsm_all[WARPS_PER_BLOCK][2][32 * XBITS_WORDS];
+__device__ __forceinline__ void bwd_bits_rows_body(const BitsArgs& A, const VGrid vg, BwdBitsSmem& sm) {
     if (*A.nonbinary) return;
     const int lane = threadIdx.x & 31;
-    float (*dsm)[32 * XBITS_WORDS] = dsm_all[threadIdx.x >> 5];
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    float (*dsm)[32 * XBITS_WORDS] = sm.dsm_all[threadIdx.x >> 5];
+    const int64_t warp = ((int64_t)vg.bx * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)vg.gx * blockDim.x) >> 5;
     const int64_t r_lo = warp * A.n_out / nwarps, r_hi = (warp + 1) * A.n_out / nwarps;
     if (r_lo >= r_hi) return;
     const uint4* xb4 = reinterpret_cast<const uint4*>(A.xbits);
@@ -1705,16 +1813,31 @@ __global__ void __launch_bounds__(256) bwd_bits_rows_kernel(BitsArgs A) {
     }
 }
 
+template <int CB>
+__global__ void __launch_bounds__(256) bwd_bits_rows_kernel(BitsArgs A) {
+    SMLP_PDL_ENTRY();
+    __shared__ BwdBitsSmem sm;
+    bwd_bits_rows_body<CB>(A, hw_grid(), sm);
+}
+
 // W^(2) gradient from mirror order to the canonical order of the grad view (a gather; a scatter
 // would cost a sector read-fill)
-__global__ void grad_from_mirror_kernel(const int32_t* __restrict__ nonbinary, const float* __restrict__ gm,
-                                        const int32_t* __restrict__ minv, float* __restrict__ grad,
-                                        const LayerMeta* __restrict__ meta) {
+struct MirrorGradArgs {
+    const int32_t* nonbinary;
+    const float* gm;
+    const int32_t* minv;
+    float* grad;
+    const LayerMeta* meta;
+};
+__device__ __forceinline__ void grad_from_mirror_body(const MirrorGradArgs& M, const VGrid vg) {
+    if (*M.nonbinary) return;
+    const int64_t n = M.meta->nnz;
+    for (int64_t k = (int64_t)vg.bx * blockDim.x + threadIdx.x; k < n; k += (int64_t)vg.gx * blockDim.x)
+        M.grad[k] = __ldcg(M.gm + __ldg(M.minv + k));   // L2: gm was written by the previous phase
+}
+__global__ void grad_from_mirror_kernel(MirrorGradArgs M) {
     SMLP_PDL_ENTRY();
-    if (*nonbinary) return;
-    const int64_t n = meta->nnz;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
-        grad[k] = __ldg(gm + __ldg(minv + k));
+    grad_from_mirror_body(M, hw_grid());
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1724,15 +1847,27 @@ __global__ void grad_from_mirror_kernel(const int32_t* __restrict__ nonbinary, c
 // two float4 groups in flight per iteration.  g and v are streamed once (evict_first); w is kept
 // (evict_last): the mirror gather of the same layer reads it right after.
 // G2: the fused path's split last-chunk gradient is in g2 (the update adds g2 + g)
+struct UpdateArgs {
+    float* w;
+    float* v;
+    const float* g;
+    const float* g2;
+    int64_t n;
+    float lr, mu, wd;
+    int64_t decay_end;
+    float gs;
+};
 template <bool G2>
-__global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w, float* __restrict__ v,
-                                                          const float* __restrict__ g, const float* __restrict__ g2,
-                                                          int64_t n, float lr,
-                                                          float mu, float wd, int64_t decay_end, float gs) {
-    SMLP_PDL_ENTRY();
+__device__ __forceinline__ void sgd_update4_body(const UpdateArgs& U, const VGrid vg) {
+    float* __restrict__ w = U.w;
+    float* __restrict__ v = U.v;
+    const float* __restrict__ g = U.g;
+    const float* __restrict__ g2 = U.g2;
+    const int64_t n = U.n, decay_end = U.decay_end;
+    const float lr = U.lr, mu = U.mu, wd = U.wd, gs = U.gs;
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     const int64_t n4 = n >> 2;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)vg.bx * blockDim.x + threadIdx.x, stride = (int64_t)vg.gx * blockDim.x;
     // weight decay on [0, decay_end) (the weight slices), none on the biases after it; decay_end
     // is a multiple of 32, so a float4 group never straddles it
     auto upd = [&](float4 wk, float4 vk, float4 gk, int64_t k4) {
@@ -1783,6 +1918,11 @@ __global__ void __launch_bounds__(256) sgd_update4_kernel(float* __restrict__ w,
         w[t] = wk + vk;
     }
 }
+template <bool G2>
+__global__ void __launch_bounds__(256) sgd_update4_kernel(UpdateArgs U) {
+    SMLP_PDL_ENTRY();
+    sgd_update4_body<G2>(U, hw_grid());
+}
 
 // mirror refresh of several layers in one launch (small models: launch count matters more than
 // overlap); blockIdx.y = layer
@@ -1792,12 +1932,15 @@ struct MirrorSet {
     const LayerMeta* meta[SMLP_MAX_LAYERS];
     float* mval[SMLP_MAX_LAYERS];
 };
+__device__ __forceinline__ void mirror_values_multi_body(const MirrorSet& M, const VGrid vg) {
+    const int l = vg.by;
+    const int64_t n = M.meta[l]->nnz;
+    for (int64_t t = (int64_t)vg.bx * blockDim.x + threadIdx.x; t < n; t += (int64_t)vg.gx * blockDim.x)
+        M.mval[l][t] = __ldcg(M.val[l] + __ldg(M.mperm[l] + t));   // L2: val was just updated (persistent step)
+}
 __global__ void __launch_bounds__(256) mirror_values_multi_kernel(const __grid_constant__ MirrorSet M) {
     SMLP_PDL_ENTRY();
-    const int l = blockIdx.y;
-    const int64_t n = M.meta[l]->nnz;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
-        M.mval[l][t] = __ldg(M.val[l] + __ldg(M.mperm[l] + t));
+    mirror_values_multi_body(M, hw_grid());
 }
 
 // mirror copy mval[t] = val[mperm[t]], 4 consecutive t per thread (4 independent gathers in flight)
@@ -1921,6 +2064,301 @@ __global__ void __launch_bounds__(256, 4) bwd_short_rows_kernel(BwdArgs A) {
     }
 }
 
+// ==========================================================================================
+// Persistent step (small models; DESIGN.md §5 "persistent step").  A model of <= 4M parameters
+// is launch- and latency-bound: its ~17 kernels per step each do a few microseconds of work.  For
+// such a model every API call (forward; backward + Eq. 1 + mirror refresh) is ONE cooperative
+// launch of persist_step_kernel: one resident wave of 256-thread blocks that runs the call's
+// kernels as phases -- the same __device__ bodies the standalone kernels run, with the same
+// virtual grids, so the results are bit-identical -- separated by grid-wide barriers.  The phase
+// list is recorded by the host code that would otherwise launch the kernels (Recorder below) and
+// passed by value as the kernel parameter.
+// ==========================================================================================
+enum PhaseKind : int {
+    PK_STAGE = 0, PK_FWD_ROWS, PK_FWD_FINISH, PK_FWD_NARROW, PK_FWD_NARROW_FIN, PK_SOFTMAX,
+    PK_BWD_ROWS, PK_BWD_FINISH, PK_BWD_NARROW_ROWS, PK_UPDATE, PK_MIRROR, PK_RESET_FLAG, PK_FWD_BITS, PK_BWD_BITS,
+    PK_GRAD_FROM_MIRROR
+};
+constexpr int PMAX = 24;
+union PhaseArgs {
+    StageArgs st;
+    FwdArgs f;
+    NarrowArgs n;
+    SoftmaxArgs s;
+    BwdArgs b;
+    UpdateArgs u;
+    BitsArgs bits;
+    MirrorGradArgs mg;
+    int32_t* flag;
+};
+struct PPhase {
+    int kind;
+    int gx, gy;   // virtual grid (PK_FWD_NARROW_FIN: gx = CTA partials, gy = logit elements)
+    int sub;      // PK_FWD_NARROW*/PK_BWD_NARROW_ROWS: padded n_L; PK_BWD_ROWS: HAS_DPREV 4 | GOLD 2 | DROP 1
+    PhaseArgs a;
+};
+struct PProgram {
+    int n;
+    int nsm;         // SMs of the device (each hosts exactly gridDim.x / nsm blocks of the wave)
+    unsigned* bar;   // grid barrier state [count, generation] (the handle's, zeroed at create)
+    unsigned* smslot;   // [nsm] blocks placed on each SM so far (the handle's; grows by the wave's share per launch)
+    MirrorSet mirror;
+    PPhase ph[PMAX];
+};
+
+template <int CB>
+union PhaseSmem {
+    FwdRowsSmem<CB> fr;
+    BwdRowsSmem<CB> br;
+    StageSmem st;
+    SoftmaxSmem so;
+    FwdNarrowSmem<CB, NARROW_MAX> fn;
+    BwdNarrowRowsSmem<CB, 16> bn;
+    FwdBitsSmem fb;
+    BwdBitsSmem bb;
+};
+// the phase's arguments are copied from the kernel parameter into shared memory at the start of
+// every phase (one coalesced read per block): the bodies read their fields from shared memory
+// instead of through generic pointers into the parameter buffer (an L2 round trip after every
+// barrier's L1 invalidation, several of them dependent per phase)
+template <int CB>
+struct PersistSmem {
+    __align__(16) PhaseArgs args[2];   // double-buffered: phase i + 1's are loaded during phase i's barrier
+    __align__(16) PhaseSmem<CB> u;
+};
+__device__ __forceinline__ void stage_phase_args(PhaseArgs& dst, const PhaseArgs& src, int t0) {
+    const int* s = reinterpret_cast<const int*>(&src);
+    int* d = reinterpret_cast<int*>(&dst);
+    for (int w = (int)threadIdx.x - t0; w < (int)(sizeof(PhaseArgs) / sizeof(int)); w += (int)blockDim.x - t0)
+        if (w >= 0) d[w] = s[w];
+}
+
+// Phase entry points of the persistent kernel: real (non-inlined) calls, so each phase body gets
+// its own register allocation instead of sharing one with every other phase of the switch.  The
+// arguments are read in place from the shared-memory copy the kernel staged (a private copy per
+// thread measured 1.6x slower: the 250-500 B structs spill at 64 registers).
+template <int CB>
+__device__ __noinline__ void pk_stage(int bx, const StageArgs& S, int gx, int gy, PersistSmem<CB>& sm) {
+    for (int v = bx; v < gx * gy; v += gridDim.x) {
+        stage_input_body(S, VGrid{v % gx, v / gx, gx}, sm.u.st);
+        __syncthreads();
+    }
+}
+template <int CB>
+__device__ __noinline__ void pk_fwd_rows(int bx, const FwdArgs& A, PersistSmem<CB>& sm) {
+    fwd_rows_body<CB>(A, VGrid{bx, 0, (int)gridDim.x}, sm.u.fr);
+}
+template <int CB>
+__device__ __noinline__ void pk_fwd_finish(int bx, const FwdArgs& A) {
+    fwd_finish_body<CB>(A, VGrid{bx, 0, (int)gridDim.x});
+}
+template <int CB, int NOUT>
+__device__ __noinline__ void pk_fwd_narrow(int bx, const NarrowArgs& A, int gx, PersistSmem<CB>& sm) {
+    if constexpr (CB * NOUT <= NARROW_MAX_ELEMS) {
+        for (int v = bx; v < gx; v += gridDim.x) {
+            fwd_narrow_body<CB, CB, NOUT>(A, VGrid{v, 0, gx}, *reinterpret_cast<FwdNarrowSmem<CB, NOUT>*>(&sm.u));
+            __syncthreads();
+        }
+    }
+}
+template <int CB, int NOUT>
+__device__ __noinline__ void pk_fwd_narrow_fin(int bx, const NarrowArgs& A, int nparts, int count) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (int)((bx * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int e = gw; e < count; e += nw) fwd_narrow_finish_body<CB, CB, NOUT>(A, nparts, e, lane);
+}
+template <int CB, int NOUT>
+__device__ __noinline__ void pk_bwd_narrow(int bx, const NarrowArgs& A, PersistSmem<CB>& sm) {
+    if constexpr (CB * NOUT <= NARROW_MAX_ELEMS && NOUT <= 16)
+        bwd_narrow_rows_body<CB, CB, NOUT>(A, VGrid{bx, 0, (int)gridDim.x},
+                                           *reinterpret_cast<BwdNarrowRowsSmem<CB, NOUT>*>(&sm.u));
+}
+template <int CB, bool HD, bool GO, bool DR>
+__device__ __noinline__ void pk_bwd_rows(int bx, const BwdArgs& A, PersistSmem<CB>& sm) {
+    bwd_rows_body<CB, CB, HD, GO, DR>(A, VGrid{bx, 0, (int)gridDim.x}, sm.u.br);
+}
+template <int CB>
+__device__ __noinline__ void pk_bwd_finish(int bx, const BwdArgs& A) {
+    bwd_finish_body<CB, CB>(A, VGrid{bx, 0, (int)gridDim.x});
+}
+template <int CB>
+__device__ __noinline__ void pk_softmax(int bx, const SoftmaxArgs& A, PersistSmem<CB>& sm) {
+    if (bx == 0) softmax_ce_body(A, sm.u.so);
+}
+template <int CB, bool DROP>
+__device__ __noinline__ void pk_fwd_bits(int bx, const BitsArgs& A, PersistSmem<CB>& sm) {
+    fwd_bits_body<CB, DROP>(A, VGrid{bx, 0, (int)gridDim.x}, sm.u.fb);
+}
+template <int CB>
+__device__ __noinline__ void pk_bwd_bits(int bx, const BitsArgs& A, PersistSmem<CB>& sm) {
+    bwd_bits_rows_body<CB>(A, VGrid{bx, 0, (int)gridDim.x}, sm.u.bb);
+}
+__device__ __noinline__ void pk_grad_from_mirror(int bx, const MirrorGradArgs& M) {
+    grad_from_mirror_body(M, VGrid{bx, 0, (int)gridDim.x});
+}
+__device__ __noinline__ void pk_update(int bx, const UpdateArgs& U) {
+    sgd_update4_body<false>(U, VGrid{bx, 0, (int)gridDim.x});
+}
+__device__ __noinline__ void pk_mirror(int bx, const MirrorSet& M, int gx, int gy) {
+    for (int v = bx; v < gx * gy; v += gridDim.x) mirror_values_multi_body(M, VGrid{v % gx, v / gx, gx});
+}
+
+// Grid-wide barrier of the persistent kernel (all blocks are co-resident: cooperative launch).
+// One arrival atomic per block; the last arrival resets the count and bumps the generation word,
+// the others poll it with volatile (L2) loads.  cg::this_grid().sync() polls with an L1
+// invalidation per iteration (CCTL.IVALL), which -- with 4 blocks per SM still working on a phase
+// -- wipes their L1 (spilled registers, gathered rows) thousands of times per barrier; measured
+// 2.5x slower steps.  Here the L1 is invalidated once, by the acquire fence after the wait.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, PhaseArgs* next = nullptr, const PhaseArgs* next_src = nullptr) {
+    __syncthreads();
+    // warps 1..7 stage the next phase's arguments while thread 0 waits for the other blocks
+    if (next && threadIdx.x >= 32) stage_phase_args(*next, *next_src, 32);
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen_p = bar + 1;
+        const unsigned gen = *gen_p;
+        __threadfence();                                  // release this block's writes of the phase
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen_p == gen) __nanosleep(20);
+        }
+        __threadfence();                                  // acquire: later loads see every block's writes
+    }
+    __syncthreads();
+}
+
+#ifdef SMLP_PERSIST_TIMING
+__device__ unsigned long long g_phase_ns[PMAX + 1];
+#endif
+template <int CB>
+__global__ void __launch_bounds__(256, 4) persist_step_kernel(const __grid_constant__ PProgram P) {
+#ifdef SMLP_PERSIST_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_phase_ns[PMAX] = t;
+    }
+#endif
+    extern __shared__ __align__(16) unsigned char psm_raw[];
+    PersistSmem<CB>& sm = *reinterpret_cast<PersistSmem<CB>*>(psm_raw);
+    // Spread block index: a cooperative wave places CONSECUTIVE blocks on the same few SMs
+    // (measured: blocks 0-23 of 592 on SMs 142-147, tools/smid_probe.cu), so a phase with few
+    // virtual blocks (staging, the narrow output layer, softmax) would run on 1-6 SMs.  Each
+    // block takes slot k of its SM instead; bx = k * nsm + smid is a permutation of the grid in
+    // which bx = 0 .. nsm-1 sit on distinct SMs.  (Every SM hosts exactly gridDim.x / nsm blocks;
+    // the counters are cleared at the end of the launch.)
+    __shared__ int s_bx;
+    if (threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        const unsigned per_sm = gridDim.x / (unsigned)P.nsm;
+        const unsigned slot = atomicAdd(P.smslot + smid, 1u) % per_sm;
+        s_bx = (int)(slot * (unsigned)P.nsm + smid);
+    }
+    __syncthreads();
+    const int bx = s_bx;
+    if (P.n > 0) stage_phase_args(sm.args[0], P.ph[0].a, 0);
+    __syncthreads();
+    for (int i = 0; i < P.n; ++i) {
+        const PPhase& ph = P.ph[i];
+        const int nout = ph.sub;
+        const PhaseArgs& a = sm.args[i & 1];
+        // a finish phase with no split rows (device counts, the same in every block) is skipped
+        // together with its barrier
+        if ((ph.kind == PK_FWD_FINISH && a.f.meta->n_fmulti == 0) ||
+            (ph.kind == PK_BWD_FINISH && a.b.meta->n_bmulti == 0)) {
+            // (skipped with its barrier; the next phase's arguments go to the other buffer now)
+            if (i + 1 < P.n) stage_phase_args(sm.args[(i + 1) & 1], P.ph[i + 1].a, 0);
+            __syncthreads();
+            continue;
+        }
+        switch (ph.kind) {
+            case PK_STAGE: pk_stage<CB>(bx, a.st, ph.gx, ph.gy, sm); break;
+            case PK_FWD_ROWS: pk_fwd_rows<CB>(bx, a.f, sm); break;
+            case PK_FWD_FINISH: pk_fwd_finish<CB>(bx, a.f); break;
+            case PK_FWD_NARROW:
+                if (nout == 2) pk_fwd_narrow<CB, 2>(bx, a.n, ph.gx, sm);
+                else if (nout == 4) pk_fwd_narrow<CB, 4>(bx, a.n, ph.gx, sm);
+                else if (nout == 8) pk_fwd_narrow<CB, 8>(bx, a.n, ph.gx, sm);
+                else if (nout == 16) pk_fwd_narrow<CB, 16>(bx, a.n, ph.gx, sm);
+                else pk_fwd_narrow<CB, 32>(bx, a.n, ph.gx, sm);
+                break;
+            case PK_FWD_NARROW_FIN:
+                if (nout == 2) pk_fwd_narrow_fin<CB, 2>(bx, a.n, ph.gx, ph.gy);
+                else if (nout == 4) pk_fwd_narrow_fin<CB, 4>(bx, a.n, ph.gx, ph.gy);
+                else if (nout == 8) pk_fwd_narrow_fin<CB, 8>(bx, a.n, ph.gx, ph.gy);
+                else if (nout == 16) pk_fwd_narrow_fin<CB, 16>(bx, a.n, ph.gx, ph.gy);
+                else pk_fwd_narrow_fin<CB, 32>(bx, a.n, ph.gx, ph.gy);
+                break;
+            case PK_SOFTMAX: pk_softmax<CB>(bx, a.s, sm); break;
+            case PK_BWD_ROWS:
+                switch (ph.sub) {
+                    case 4: pk_bwd_rows<CB, true, false, false>(bx, a.b, sm); break;
+                    case 5: pk_bwd_rows<CB, true, false, true>(bx, a.b, sm); break;
+                    case 6: pk_bwd_rows<CB, true, true, false>(bx, a.b, sm); break;
+                    case 7: pk_bwd_rows<CB, true, true, true>(bx, a.b, sm); break;
+                    case 0: pk_bwd_rows<CB, false, false, false>(bx, a.b, sm); break;
+                    case 2: pk_bwd_rows<CB, false, true, false>(bx, a.b, sm); break;
+                    default: break;
+                }
+                break;
+            case PK_BWD_FINISH: pk_bwd_finish<CB>(bx, a.b); break;
+            case PK_BWD_NARROW_ROWS:
+                if (nout == 2) pk_bwd_narrow<CB, 2>(bx, a.n, sm);
+                else if (nout == 4) pk_bwd_narrow<CB, 4>(bx, a.n, sm);
+                else if (nout == 8) pk_bwd_narrow<CB, 8>(bx, a.n, sm);
+                else pk_bwd_narrow<CB, 16>(bx, a.n, sm);
+                break;
+            case PK_UPDATE: pk_update(bx, a.u); break;
+            case PK_MIRROR: pk_mirror(bx, P.mirror, ph.gx, ph.gy); break;
+            case PK_RESET_FLAG:
+                if (bx == 0 && threadIdx.x == 0) *a.flag = 0;
+                break;
+            case PK_FWD_BITS:
+                if (ph.sub) pk_fwd_bits<CB, true>(bx, a.bits, sm);
+                else pk_fwd_bits<CB, false>(bx, a.bits, sm);
+                break;
+            case PK_BWD_BITS: pk_bwd_bits<CB>(bx, a.bits, sm); break;
+            case PK_GRAD_FROM_MIRROR: pk_grad_from_mirror(bx, a.mg); break;
+            default: break;
+        }
+        // every phase's writes are visible to the next (and smem is free again)
+        if (i + 1 < P.n) grid_barrier(P.bar, &sm.args[(i + 1) & 1], &P.ph[i + 1].a);
+        else grid_barrier(P.bar);
+#ifdef SMLP_PERSIST_TIMING    // A/B build only: per-phase end times (ns) after the barrier
+        if (bx == 0 && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            g_phase_ns[i] = t;
+        }
+#endif
+    }
+    // every block took its slot before the first barrier: clear the counters for the next launch
+    if (bx == 0)
+        for (int t = threadIdx.x; t < P.nsm; t += blockDim.x) P.smslot[t] = 0;
+}
+
+// Host side: the launch sites record their phases here while h->rec is set (no launch, no count)
+struct Recorder {
+    PProgram P;
+    bool ok = true;
+    PPhase* add(int kind, int gx, int gy, int sub) {
+        if (P.n >= PMAX) {
+            ok = false;
+            return nullptr;
+        }
+        PPhase* ph = &P.ph[P.n++];
+        ph->kind = kind;
+        ph->gx = gx;
+        ph->gy = gy;
+        ph->sub = sub;
+        return ph;
+    }
+};
+inline Recorder* recorder(smlp_handle* h) { return static_cast<Recorder*>(h->rec); }
+
 // grid of the finish kernels: their row count lives in device memory (graph-stable), so the grid
 // is sized for the capacity but capped at 2 blocks per SM (grid-stride loops): split rows are rare
 // (C5: ~0.03% of the rows), and a wider grid of mostly idle blocks costs a few microseconds per launch
@@ -1953,6 +2391,17 @@ static int64_t short_min_rows(const smlp_handle* h) {
 template <int CB>
 int launch_fwd(smlp_handle* h, const FwdArgs& A, const Layer& L) {
     constexpr int P = 32 / (CB / 4);
+    if (Recorder* R = recorder(h)) {
+        const bool short_rows = CB == 128 && L.nnz < (int64_t)h->short_max_fwd * L.n_out && L.n_out >= short_min_rows(h);
+        if (CB != h->CB || short_rows) {
+            R->ok = false;
+            return SMLP_OK;
+        }
+        if (PPhase* ph = R->add(PK_FWD_ROWS, 0, 0, 0)) ph->a.f = A;
+        if (L.fslot_cap > 0)
+            if (PPhase* ph = R->add(PK_FWD_FINISH, 0, 0, 0)) ph->a.f = A;
+        return SMLP_OK;
+    }
     if constexpr (CB == 128) {
         // layers of short rows (< 16 entries per mirror row on average): stream whole rows
         // (and enough 32-row units to give every resident warp one: a narrow layer keeps the row kernel)
@@ -1978,6 +2427,19 @@ template <int CB, int CBF>
 int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev) {
     constexpr int P = 32 / (CB / 4);
     const bool gold = !A.first && !A.no_gold, drop = A.dropout_prev != 0;
+    if (Recorder* R = recorder(h)) {
+        const bool short_rows = CB == 128 && CBF == 128 && L.nnz < (int64_t)h->short_max_bwd * L.n_in &&
+                                L.n_in >= short_min_rows(h);
+        if (CB != CBF || CB != h->CB || short_rows) {
+            R->ok = false;
+            return SMLP_OK;
+        }
+        const int mode = (has_dprev ? 4 : 0) | (gold ? 2 : 0) | (drop ? 1 : 0);
+        if (PPhase* ph = R->add(PK_BWD_ROWS, 0, 0, mode)) ph->a.b = A;
+        if (has_dprev && L.bslot_cap > 0)
+            if (PPhase* ph = R->add(PK_BWD_FINISH, 0, 0, 0)) ph->a.b = A;
+        return SMLP_OK;
+    }
     if constexpr (CB == 128 && CBF == 128) {
         // layers of short canonical rows (< 8 entries on average): stream whole rows
         if (L.nnz < (int64_t)h->short_max_bwd * L.n_in &&
@@ -2059,6 +2521,19 @@ int launch_narrow_n(smlp_handle* h, const NarrowArgs& A, const Layer& L, bool fw
     if constexpr (NOUT * CB > NARROW_MAX_ELEMS) {
         return set_err(h, SMLP_E_ARG, "narrow output layer too wide for chunk_batch");
     } else {
+        if (Recorder* R = recorder(h)) {
+            if (CB != CBF || CB != h->CB || (!fwd && !(NOUT <= 16 && L.dense))) {
+                R->ok = false;
+                return SMLP_OK;
+            }
+            if (fwd) {
+                if (PPhase* ph = R->add(PK_FWD_NARROW, L.ngrid, 1, NOUT)) ph->a.n = A;
+                if (PPhase* ph = R->add(PK_FWD_NARROW_FIN, L.ngrid, A.n_out * CB, NOUT)) ph->a.n = A;
+            } else {
+                if (PPhase* ph = R->add(PK_BWD_NARROW_ROWS, 0, 0, NOUT)) ph->a.n = A;
+            }
+            return SMLP_OK;
+        }
         if (fwd) {
             launch_pdl(h->pdl, fwd_narrow_kernel<CB, CBF, NOUT>, L.ngrid, NARROW_WARPS * 32, h->stream, A);
             SMLP_CK_LAUNCH(h, "fwd_narrow_kernel");
@@ -2130,6 +2605,10 @@ int refresh_mirror_values(smlp_handle* h, Layer& Ly) {
 }
 
 int run_probs(smlp_handle* h, int B, float* probs) {
+    if (Recorder* R = recorder(h)) {
+        R->ok = false;
+        return SMLP_OK;
+    }
     launch_pdl(h->pdl, softmax_probs_kernel, (B + 127) / 128, 128, h->stream, h->act[h->L], probs, h->sizes[h->L - 1], B, h->CBf);
     SMLP_CK_LAUNCH(h, "softmax_probs_kernel");
     return SMLP_OK;
@@ -2185,6 +2664,11 @@ int launch_bits(smlp_handle* h, const BitsArgs& A, const Layer& L2, bool fwd) {
 }
 
 int dispatch_bits(smlp_handle* h, const BitsArgs& A, const Layer& L2, bool fwd) {
+    if (Recorder* R = recorder(h)) {
+        if ((fwd ? h->CBf : h->CB) != h->CB) R->ok = false;
+        else if (PPhase* ph = R->add(fwd ? PK_FWD_BITS : PK_BWD_BITS, 0, 0, A.dropout_on ? 1 : 0)) ph->a.bits = A;
+        return SMLP_OK;
+    }
     SMLP_DISPATCH_CB(h, fwd ? h->CBf : h->CB, launch_bits, h, A, L2, fwd);
 }
 
@@ -2211,17 +2695,24 @@ NarrowArgs narrow_args(smlp_handle* h, Layer& Ly, int c, bool fwd) {
     return A;
 }
 
-int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, bool train, uint64_t step,
-                float* probs) {
+static int run_forward_phases(smlp_handle* h, const float* x, const int32_t* x_idx, int B, bool train, uint64_t step,
+                              float* probs) {
     const int CB = h->CBf;    // the forward tensors' chunk width
     const int nchunks = (B + CB - 1) / CB;
     {
         dim3 grid((unsigned)((h->sizes[0] + 127) / 128), (unsigned)((nchunks * CB + 31) / 32));
         const int vec = (h->sizes[0] % 4 == 0) && ((uintptr_t)x % 16 == 0);
         prof_start(h, K_STAGE, 1, 8.0 * (double)B * (double)h->sizes[0], 0.0);
-        if (h->xbits) SMLP_CK(h, cudaMemsetAsync(h->d_nonbinary, 0, sizeof(int32_t), h->stream));
-        launch_pdl(h->pdl, stage_input_kernel, grid, dim3(32, 32), h->stream, x, x_idx, B, nchunks, CB, h->sizes[0], h->act[1], h->xbits, h->d_nonbinary, vec);
-        SMLP_CK_LAUNCH(h, "stage_input_kernel");
+        const StageArgs S{x, x_idx, B, nchunks, CB, h->sizes[0], h->act[1], h->xbits, h->d_nonbinary, vec};
+        if (Recorder* R = recorder(h)) {
+            if (h->xbits)                    // the non-binary flag is cleared one phase before staging sets it
+                if (PPhase* ph = R->add(PK_RESET_FLAG, 1, 1, 0)) ph->a.flag = h->d_nonbinary;
+            if (PPhase* ph = R->add(PK_STAGE, (int)grid.x, (int)grid.y, 0)) ph->a.st = S;
+        } else {
+            if (h->xbits) SMLP_CK(h, cudaMemsetAsync(h->d_nonbinary, 0, sizeof(int32_t), h->stream));
+            launch_pdl(h->pdl, stage_input_kernel, grid, 256, h->stream, S);
+            SMLP_CK_LAUNCH(h, "stage_input_kernel");
+        }
         prof_stop(h);
     }
     const bool drop = train && h->dropout > 0.f;
@@ -2320,12 +2811,16 @@ static int launch_update(smlp_handle* h, cudaStream_t stream, int64_t lo, int64_
     float* v = h->mom + lo;
     const float* g = h->grad + lo;
     const float* gb = g2 ? h->grad2 + lo : nullptr;
-    const float lr = sgd->lr, mu = sgd->momentum, wd = sgd->weight_decay, gs = sgd->grad_scale;
-    const int64_t n = hi - lo;
+    const UpdateArgs U{w, v, g, gb, hi - lo, sgd->lr, sgd->momentum, sgd->weight_decay, decay_end, sgd->grad_scale};
+    if (Recorder* R = recorder(h)) {
+        if (g2 || stream != h->stream) R->ok = false;
+        else if (PPhase* ph = R->add(PK_UPDATE, 0, 0, 0)) ph->a.u = U;
+        return SMLP_OK;
+    }
     if (g2)
-        launch_pdl(h->pdl, sgd_update4_kernel<true>, grid, threads, stream, w, v, g, gb, n, lr, mu, wd, decay_end, gs);
+        launch_pdl(h->pdl, sgd_update4_kernel<true>, grid, threads, stream, U);
     else
-        launch_pdl(h->pdl, sgd_update4_kernel<false>, grid, threads, stream, w, v, g, gb, n, lr, mu, wd, decay_end, gs);
+        launch_pdl(h->pdl, sgd_update4_kernel<false>, grid, threads, stream, U);
     SMLP_CK_LAUNCH(h, "sgd_update4_kernel");
     return SMLP_OK;
 }
@@ -2340,12 +2835,14 @@ static int ensure_aux(smlp_handle* h) {
 // W^(l)'s gradient (and b_{l-1}'s) is final: record the layer event (sparse_mlp_wait_layer lets a
 // communication stream start that layer's allreduce while the backward continues)
 static int layer_done(smlp_handle* h, int l) {
+    if (h->rec) return SMLP_OK;   // persistent step: recorded after its launch (every layer at once)
     if (!h->layer_ev[l]) SMLP_CK(h, cudaEventCreateWithFlags(&h->layer_ev[l], cudaEventDisableTiming));
     SMLP_CK(h, cudaEventRecord(h->layer_ev[l], h->stream));
     return SMLP_OK;
 }
 
-int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, bool split_last) {
+static int run_backward_phases(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss,
+                               bool split_last) {
     const int CB = h->CB;
     const int B = h->trace_B;
     const int nchunks = (B + CB - 1) / CB;
@@ -2368,8 +2865,12 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
         S.CB = CB;
         S.CBf = h->CBf;
         prof_start(h, K_SOFTMAX, L, 8.0 * (double)B * (double)S.nL, 0.0);
-        launch_pdl(h->pdl, softmax_ce_kernel, 1, 512, h->stream, S);
-        SMLP_CK_LAUNCH(h, "softmax_ce_kernel");
+        if (Recorder* R = recorder(h)) {
+            if (PPhase* ph = R->add(PK_SOFTMAX, 1, 1, 0)) ph->a.s = S;
+        } else {
+            launch_pdl(h->pdl, softmax_ce_kernel, 1, 256, h->stream, S);
+            SMLP_CK_LAUNCH(h, "softmax_ce_kernel");
+        }
         prof_stop(h);
     }
     // chunk-major, chunks in reverse: the forward ended on the last chunk, and layer l of chunk c
@@ -2461,8 +2962,13 @@ int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, fl
         SMLP_TRY(dispatch_bits(h, A, L2, false));
         prof_stop(h);
         prof_start(h, K_LAYER_UPDATE, 2, 12.0 * nnz, 0.0);
-        launch_pdl(h->pdl, grad_from_mirror_kernel, launch_grid(h, L2.cap, 256), 256, h->stream, h->d_nonbinary, h->gmirror2, L2.minv, L2.grad, L2.meta);
-        SMLP_CK_LAUNCH(h, "grad_from_mirror_kernel");
+        const MirrorGradArgs MG{h->d_nonbinary, h->gmirror2, L2.minv, L2.grad, L2.meta};
+        if (Recorder* R = recorder(h)) {
+            if (PPhase* ph = R->add(PK_GRAD_FROM_MIRROR, 0, 0, 0)) ph->a.mg = MG;
+        } else {
+            launch_pdl(h->pdl, grad_from_mirror_kernel, launch_grid(h, L2.cap, 256), 256, h->stream, MG);
+            SMLP_CK_LAUNCH(h, "grad_from_mirror_kernel");
+        }
         prof_stop(h);
         SMLP_TRY(layer_done(h, 2));
     }
@@ -2494,10 +3000,19 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
         if (nl > 0) {
             const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((cmax + 255) / 256, h->num_sms * 4)),
                             (unsigned)nl);
-            launch_pdl(h->pdl, mirror_values_multi_kernel, grid, 256, h->stream, M);
-            SMLP_CK_LAUNCH(h, "mirror_values_multi_kernel");
+            if (Recorder* R = recorder(h)) {
+                R->P.mirror = M;
+                R->add(PK_MIRROR, (int)grid.x, (int)grid.y, 0);
+            } else {
+                launch_pdl(h->pdl, mirror_values_multi_kernel, grid, 256, h->stream, M);
+                SMLP_CK_LAUNCH(h, "mirror_values_multi_kernel");
+            }
         }
         prof_stop(h);
+        return SMLP_OK;
+    }
+    if (Recorder* R = recorder(h)) {   // large models: per-layer slices + side-stream refreshes
+        R->ok = false;
         return SMLP_OK;
     }
     SMLP_TRY(ensure_aux(h));
@@ -2523,6 +3038,118 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
     }
     prof_stop(h);
     return SMLP_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// persistent step: launch of a recorded program (one cooperative wave), and the API-level entry
+// points that record when the handle takes the persistent path (h->persist) and fall back to
+// the per-kernel launches when a call needs a phase the persistent kernel does not carry
+// ------------------------------------------------------------------------------------------
+static_assert(sizeof(PProgram) <= 32000, "the phase list is passed as one kernel parameter");
+
+template <int CB>
+static int launch_persist_cb(smlp_handle* h, const PProgram& P) {
+    static int per_sm = 0;
+    const size_t smem = sizeof(PersistSmem<CB>);
+    if (per_sm == 0) {
+        SMLP_CK(h, cudaFuncSetAttribute(persist_step_kernel<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SMLP_CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persist_step_kernel<CB>, 256, smem));
+        if (per_sm < 1) return set_err(h, SMLP_E_CUDA, "persistent step kernel does not fit an SM");
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(per_sm * h->num_sms));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SMLP_CK(h, cudaLaunchKernelEx(&cfg, persist_step_kernel<CB>, P));
+    SMLP_CK_LAUNCH(h, "persist_step_kernel");
+#ifdef SMLP_PERSIST_TIMING
+    {
+        unsigned long long t[PMAX + 1];
+        cudaStreamSynchronize(h->stream);
+        cudaMemcpyFromSymbol(t, g_phase_ns, sizeof(t));
+        unsigned long long prev = t[PMAX];
+        fprintf(stderr, "persist phases:");
+        for (int i = 0; i < P.n; ++i) {
+            fprintf(stderr, " %d:%.1f", P.ph[i].kind, (double)(t[i] - prev) / 1e3);
+            prev = t[i];
+        }
+        fprintf(stderr, " us\n");
+    }
+#endif
+    return SMLP_OK;
+}
+
+static int launch_persist(smlp_handle* h, PProgram& P, int prof_kind, double bytes, double flops) {
+    P.bar = h->gbar;
+    P.smslot = h->gbar + 2;
+    P.nsm = h->num_sms;
+    prof_start(h, prof_kind, 0, bytes, flops);
+    int rc;
+    switch (h->CB) {
+        case 8: rc = launch_persist_cb<8>(h, P); break;
+        case 16: rc = launch_persist_cb<16>(h, P); break;
+        case 32: rc = launch_persist_cb<32>(h, P); break;
+        case 64: rc = launch_persist_cb<64>(h, P); break;
+        case 128: rc = launch_persist_cb<128>(h, P); break;
+        default: rc = set_err(h, SMLP_E_ARG, "persistent step: unsupported chunk_batch");
+    }
+    prof_stop(h);
+    return rc;
+}
+
+// Records the phases `body` would launch; returns 1 (and leaves nothing enqueued) when the call
+// must take the per-kernel path instead.
+template <typename F>
+static int record_program(smlp_handle* h, Recorder& R, F&& body, int* rc) {
+    R.P.n = 0;
+    R.ok = true;
+    h->rec = &R;
+    h->rec_bytes = h->rec_flops = 0.0;
+    *rc = body();
+    h->rec = nullptr;
+    return (*rc == SMLP_OK && R.ok && R.P.n > 0) ? 0 : 1;
+}
+
+int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, bool train, uint64_t step,
+                float* probs) {
+    if (h->persist) {
+        Recorder R;
+        int rc;
+        if (record_program(h, R, [&] { return run_forward_phases(h, x, x_idx, B, train, step, probs); }, &rc) == 0)
+            return launch_persist(h, R.P, K_PERSIST_FWD, h->rec_bytes, h->rec_flops);
+        if (rc != SMLP_OK) return rc;
+    }
+    return run_forward_phases(h, x, x_idx, B, train, step, probs);
+}
+
+// backward (a4-a5) and, when fused, the Eq. 1 pass + mirror refresh (a6) of the same call
+int run_backward_step(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, const smlp_sgd* fused) {
+    auto body = [&]() -> int {
+        SMLP_TRY(run_backward_phases(h, labels, y_idx, loss, fused != nullptr));
+        if (fused) SMLP_TRY(run_step(h, fused));
+        return SMLP_OK;
+    };
+    if (h->persist) {
+        Recorder R;
+        int rc;
+        if (record_program(h, R, body, &rc) == 0) {
+            SMLP_TRY(launch_persist(h, R.P, K_PERSIST_BWD, h->rec_bytes, h->rec_flops));
+            for (int l = h->L; l >= 2; --l) SMLP_TRY(layer_done(h, l));   // every layer final at once
+            return SMLP_OK;
+        }
+        if (rc != SMLP_OK) return rc;
+    }
+    return body();
+}
+
+int run_backward(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, bool split_last) {
+    return run_backward_phases(h, labels, y_idx, loss, split_last);
 }
 
 }  // namespace smlp

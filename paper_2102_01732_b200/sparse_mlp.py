@@ -40,7 +40,8 @@ EXPORTED = [
     "sparse_mlp_params_updated", "sparse_mlp_plan_chunks", "sparse_mlp_join", "sparse_mlp_params_averaged",
 ]
 KERNEL_KINDS = {0: "stage_input", 1: "fwd", 2: "fwd_finish", 3: "softmax_ce", 4: "bwd", 5: "bwd_finish",
-                6: "sgd_update", 7: "fwd_bits", 8: "bwd_bits", 9: "layer_update", 10: "mirror_values"}
+                6: "sgd_update", 7: "fwd_bits", 8: "bwd_bits", 9: "layer_update", 10: "mirror_values",
+                11: "persist_fwd", 12: "persist_bwd"}
 
 
 class SparseMLPError(RuntimeError):
