@@ -385,6 +385,32 @@ __device__ __forceinline__ float4 group_allreduce(float4 v) {
     return v;
 }
 
+// Sum of a float4 over the P groups of a warp, scattered: lane (g, q) ends with the components
+// c = r P + g (r < NR) it finishes in the epilogue -- 3 shuffles for P = 4 instead of 8 for an
+// all-reduce.  Fixed pairing, so the result is deterministic.
+template <int CB>
+__device__ __forceinline__ void group_reduce_scatter(float4 v, int g, float (&out)[RowCfg<CB>::NR]) {
+    using C = RowCfg<CB>;
+    constexpr int G = C::G, P = C::P;
+    if constexpr (P == 1) {
+        out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+    } else if constexpr (P == 2) {          // g = 0 keeps (x, z), g = 1 keeps (y, w)
+        const bool hi = g & 1;
+        const float k0 = hi ? v.y : v.x, k1 = hi ? v.w : v.z, s0 = hi ? v.x : v.y, s1 = hi ? v.z : v.w;
+        out[0] = k0 + __shfl_xor_sync(FULL, s0, G);
+        out[1] = k1 + __shfl_xor_sync(FULL, s1, G);
+    } else {
+#pragma unroll
+        for (int m = 4 * G; m < 32; m <<= 1) v = f4add(v, shfl_xor4(v, m));   // groups beyond 4
+        const bool b1 = (g & 2) != 0, b0 = (g & 1) != 0;
+        const float ka = b1 ? v.z : v.x, kb = b1 ? v.w : v.y, sa = b1 ? v.x : v.z, sb = b1 ? v.y : v.w;
+        const float pa = ka + __shfl_xor_sync(FULL, sa, 2 * G);   // component (g & 2) + 0
+        const float pb = kb + __shfl_xor_sync(FULL, sb, 2 * G);   // component (g & 2) + 1
+        const float keep = b0 ? pb : pa, send = b0 ? pa : pb;
+        out[0] = keep + __shfl_xor_sync(FULL, send, G);           // component g & 3
+    }
+}
+
 // cp.async (LDGSTS): global -> shared without a register destination, zero-filled when !valid
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, bool valid, uint64_t pol) {
@@ -425,8 +451,8 @@ __device__ __forceinline__ void window_pad(int2* win, int n, int lane, int zero_
 // (g, q) finishes components c = r P + g of its float4 (columns 4q + c), so all 32 lanes share
 // the bias / All-ReLU / dropout / mask work and the store is one coalesced row.
 template <int CB>
-__device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, const float4& acc, float bj, int lane,
-                                                  uint32_t step_lo) {
+__device__ __forceinline__ void fwd_rows_epilogue_c(const FwdArgs& A, int64_t j, const float (&zr)[RowCfg<CB, true>::NR],
+                                                    float bj, int lane, uint32_t step_lo) {
     using C = RowCfg<CB, true>;
     constexpr int G = C::G, P = C::P, NR = C::NR;
     const int g = lane / G, q = lane % G;
@@ -441,7 +467,7 @@ __device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, c
     for (int r = 0; r < NR; ++r) {
         const int c = r * P + g;
         const bool valid = c < 4;
-        const float z = comp(acc, c & 3) + bj;
+        const float z = zr[r] + bj;
         if (!A.hidden) {
             out[r] = z;
             continue;
@@ -476,6 +502,17 @@ __device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, c
         A.zmask[j] = make_uint4(zb[0], zb[1], zb[2], zb[3]);
         if (A.dropout_on) A.kmask[j] = make_uint4(kb[0], kb[1], kb[2], kb[3]);
     }
+}
+
+// the same with the row's complete float4 in every lane
+template <int CB>
+__device__ __forceinline__ void fwd_rows_epilogue(const FwdArgs& A, int64_t j, const float4& acc, float bj, int lane,
+                                                  uint32_t step_lo) {
+    using C = RowCfg<CB, true>;
+    float zr[C::NR];
+#pragma unroll
+    for (int r = 0; r < C::NR; ++r) zr[r] = comp(acc, (r * C::P + lane / C::G) & 3);
+    fwd_rows_epilogue_c<CB>(A, j, zr, bj, lane, step_lo);
 }
 
 // NS gather slots of a batch, all issued before the first FMA (entry u P + g of the window in slot u)
@@ -532,7 +569,7 @@ __device__ __forceinline__ void stage_window(int2* win, const int (&ix)[NW], con
 
 template <int CB>
 struct FwdRowsSmem {
-    int2 win_all[WARPS_PER_BLOCK][RowCfg<CB, true>::WIN];
+    __align__(16) int2 win_all[WARPS_PER_BLOCK][RowCfg<CB, true>::WIN];
 };
 template <int CB>
 __device__ __forceinline__ void fwd_rows_body(const FwdArgs& A, const VGrid vg, FwdRowsSmem<CB>& sm) {
@@ -574,11 +611,13 @@ __device__ __forceinline__ void fwd_rows_body(const FwdArgs& A, const VGrid vg, 
 #pragma unroll
         for (int b = 0; b < NB; ++b)
             if (b * EB < n) fwd_batch<CB>(A.a_prev, win + b * EB, n - b * EB, g, q, acc, pg);
-        acc = group_allreduce<G>(acc);
         if (cur.w < 0) {
-            fwd_rows_epilogue<CB>(A, cur.x, acc, bj, lane, step_lo);
-        } else if (g == 0) {
-            st4(A.ws + (int64_t)cur.w * CB + q * 4, acc);
+            float zr[C::NR];
+            group_reduce_scatter<CB>(acc, g, zr);
+            fwd_rows_epilogue_c<CB>(A, cur.x, zr, bj, lane, step_lo);
+        } else {
+            acc = group_allreduce<G>(acc);
+            if (g == 0) st4(A.ws + (int64_t)cur.w * CB + q * 4, acc);
         }
         cur = nxt;
         nxt = nn;
@@ -908,32 +947,6 @@ __device__ __forceinline__ BwdSide bwd_side(const BwdArgs& A, int64_t i, int64_t
     return t;
 }
 
-// Sum of a float4 over the P groups of a warp, scattered: lane (g, q) ends with the components
-// c = r P + g (r < NR) it finishes in the epilogue -- 3 shuffles for P = 4 instead of 8 for an
-// all-reduce.  Fixed pairing, so the result is deterministic.
-template <int CB>
-__device__ __forceinline__ void group_reduce_scatter(float4 v, int g, float (&out)[RowCfg<CB>::NR]) {
-    using C = RowCfg<CB>;
-    constexpr int G = C::G, P = C::P;
-    if constexpr (P == 1) {
-        out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
-    } else if constexpr (P == 2) {          // g = 0 keeps (x, z), g = 1 keeps (y, w)
-        const bool hi = g & 1;
-        const float k0 = hi ? v.y : v.x, k1 = hi ? v.w : v.z, s0 = hi ? v.x : v.y, s1 = hi ? v.z : v.w;
-        out[0] = k0 + __shfl_xor_sync(FULL, s0, G);
-        out[1] = k1 + __shfl_xor_sync(FULL, s1, G);
-    } else {
-#pragma unroll
-        for (int m = 4 * G; m < 32; m <<= 1) v = f4add(v, shfl_xor4(v, m));   // groups beyond 4
-        const bool b1 = (g & 2) != 0, b0 = (g & 1) != 0;
-        const float ka = b1 ? v.z : v.x, kb = b1 ? v.w : v.y, sa = b1 ? v.x : v.z, sb = b1 ? v.y : v.w;
-        const float pa = ka + __shfl_xor_sync(FULL, sa, 2 * G);   // component (g & 2) + 0
-        const float pb = kb + __shfl_xor_sync(FULL, sb, 2 * G);   // component (g & 2) + 1
-        const float keep = b0 ? pb : pa, send = b0 ? pa : pb;
-        out[0] = keep + __shfl_xor_sync(FULL, send, G);           // component g & 3
-    }
-}
-
 // backward epilogue of one complete input row i: f'_{l-1} from the sign bits, dropout keep bits,
 // store of delta_{l-1}[i], and the bias gradient of layer l-1 (a fixed 32-lane butterfly, then
 // accumulated over chunks in order).  d[r] = component r P + g of the row's sum.
@@ -1016,7 +1029,7 @@ __device__ __forceinline__ void bwd_batch(const float* __restrict__ d_out, const
 template <int CB>
 struct BwdRowsSmem {
     static constexpr int RB = RowCfg<CB>::NB < 2 ? RowCfg<CB>::NB : 2;   // batches per reduction round
-    int2 win_all[WARPS_PER_BLOCK][2][SEG_NNZ];
+    __align__(16) int2 win_all[WARPS_PER_BLOCK][2][SEG_NNZ];
     __align__(16) float4 ai_all[WARPS_PER_BLOCK][2][RowCfg<CB>::G];
     __align__(16) float red_all[WARPS_PER_BLOCK][RB * RowCfg<CB>::EB * RowCfg<CB>::S];
 };
@@ -1699,10 +1712,10 @@ __device__ __forceinline__ void fwd_bits_body(const BitsArgs& A, const VGrid vg,
             float w_nn;
             ld_entry(blk + 64 + lane, src_nn, w_nn);
             const uint4 xb_n = blk + 32 + lane < E1 ? __ldg(xb4 + src_n) : make_uint4(0, 0, 0, 0);
-            rec[wib][lane][0] = make_float2(w, __uint_as_float(xb.x));
-            rec[wib][lane][1] = make_float2(w, __uint_as_float(xb.y));
-            rec[wib][lane][2] = make_float2(w, __uint_as_float(xb.z));
-            rec[wib][lane][3] = make_float2(w, __uint_as_float(xb.w));
+            rec[wib][lane][0] = make_float2(w, __uint_as_float(__funnelshift_l(xb.x, xb.x, 1)));
+            rec[wib][lane][1] = make_float2(w, __uint_as_float(__funnelshift_l(xb.y, xb.y, 1)));
+            rec[wib][lane][2] = make_float2(w, __uint_as_float(__funnelshift_l(xb.z, xb.z, 1)));
+            rec[wib][lane][3] = make_float2(w, __uint_as_float(__funnelshift_l(xb.w, xb.w, 1)));
             __syncwarp();
             const int n = min(32, E1 - blk);
             // the block's entries row by row: a tight loop up to the next row end, then the row's
@@ -1712,21 +1725,22 @@ __device__ __forceinline__ void fwd_bits_body(const BitsArgs& A, const VGrid vg,
                 while (blk + u == row_end && row < nrows) finish_row();
                 if (u >= n) break;
                 const int stop = min(n, row_end - blk);
-                float2 alo = make_float2(acc.x, acc.y), ahi = make_float2(acc.z, acc.w);
                 const char* rp = reinterpret_cast<const char*>(myrec);
 #pragma unroll 4
                 for (; u < stop; ++u) {
                     const float2 r = *reinterpret_cast<const float2*>(rp + u * (XBITS_WORDS * 8));
-                    // x in {0, 1}: fmaf(w, x, acc) is acc + w for x = 1 and acc for x = 0, bit for bit;
-                    // the 4 x's come from the nibble by ALU selects (a shared-memory table read per
-                    // entry kept the L1 / shared pipe at 94%)
-                    const uint32_t nib = __float_as_uint(r.y) >> sh;
-                    const float4 m = make_float4((nib & 1u) ? 1.f : 0.f, (nib & 2u) ? 1.f : 0.f,
-                                                 (nib & 4u) ? 1.f : 0.f, (nib & 8u) ? 1.f : 0.f);
-                    alo = ffma2(make_float2(r.x, r.x), make_float2(m.x, m.y), alo);
-                    ahi = ffma2(make_float2(r.x, r.x), make_float2(m.z, m.w), ahi);
+                    // x in {0, 1}: acc + w x is acc + w for x = 1 and acc for x = 0, bit for bit, so
+                    // each column is one predicated add.  The published word is rotated left by
+                    // one: the lane's nibble lands on bits 1..4 and all four predicates come from
+                    // one register-to-predicate move (R2P): 7 instructions per entry (LDS, SHF,
+                    // R2P, 4 FADD) instead of ~18 with selects + FFMA2 (294 -> 216 us at C5)
+                    const uint32_t rw = __float_as_uint(r.y);
+                    const uint32_t nib = __funnelshift_r(rw, rw, sh);
+                    if (nib & 2u) acc.x += r.x;
+                    if (nib & 4u) acc.y += r.x;
+                    if (nib & 8u) acc.z += r.x;
+                    if (nib & 16u) acc.w += r.x;
                 }
-                acc = make_float4(alo.x, alo.y, ahi.x, ahi.y);
             }
             __syncwarp();
             w = w_n;
