@@ -161,12 +161,13 @@ def cpu_baseline_job(cfg_name: str, batch: int, steps: int, evolve: bool = False
             "evolve_s": None if t_ev is None else round(t_ev, 2), "step_s": round(dt / steps, 2)}
 
 
-def gathered_bytes(rec, sizes, nnz, cb, cbf, bits_layer2=False):
+def gathered_bytes(rec, sizes, nnz, cb, cbf, bits_layer2=False, implicit_delta=False):
     """L2->SM gather bytes of one launch of a row kernel (SURVEY.md §8(d) second ceiling): one
     chunk-wide fp32 row per connection -- the forward gathers a_{l-1} rows (CBf columns), the
     backward delta_l rows (CB columns).  Narrow output layers stream instead (0).  With the
     binary-input path, W^(2)'s fp32 row kernels return at once (0) and the bit kernels gather one
-    16-B bit row (128 batch columns) per connection."""
+    16-B bit row (128 batch columns) per connection.  With the implicit delta_{L-1}
+    the backward of W^(L-1) gathers one 16-B record per connection instead of a delta row."""
     l, k = rec["layer"], rec["kernel"]
     if k in ("fwd_bits", "bwd_bits"):
         return float(nnz[l - 1]) * 16.0
@@ -176,6 +177,8 @@ def gathered_bytes(rec, sizes, nnz, cb, cbf, bits_layer2=False):
         return 0.0
     if l == len(sizes) and sizes[-1] <= 32:
         return 0.0
+    if implicit_delta and k == "bwd" and l == len(sizes) - 1:
+        return float(nnz[l - 1]) * 16.0
     w = cbf if k == "fwd" else cb
     return float(nnz[l - 1]) * w * 4.0
 
@@ -403,7 +406,8 @@ def main():
             step_gb = 0.0
             bits2 = any(r["kernel"] == "fwd_bits" for r in prof)
             for r in prof:
-                gb = gathered_bytes(r, cfg.sizes, nnz, info0["chunk_batch"], info0["fwd_chunk_batch"], bits2)
+                gb = gathered_bytes(r, cfg.sizes, nnz, info0["chunk_batch"], info0["fwd_chunk_batch"], bits2,
+                                    bool(info0.get("implicit_delta")))
                 if gb <= 0:
                     continue
                 avg = r["total_ms"] / r["launches"]

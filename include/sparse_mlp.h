@@ -133,6 +133,10 @@ typedef struct {
     int64_t  param_count;                    /* floats in the param / grad views          */
     int64_t  launches;                       /* kernels launched by this handle so far    */
     int32_t  fwd_chunk_batch;                /* CBf: chunk width of a_l and the masks     */
+    int32_t  implicit_delta;                 /* 1: the backward of W^(L-1) recomputes delta_{L-1}
+                                                from per-neuron records (dense-capped 2-output
+                                                W^(L), chunk_batch <= 64, no dropout) instead of
+                                                gathering it; results are bit-identical           */
 } smlp_info;
 
 /* sparse_mlp_create — PAPER.md:51-52 ("Initially each W^(l) is a Erdos-Renyi random graph"),

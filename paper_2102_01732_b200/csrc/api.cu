@@ -255,6 +255,12 @@ int build_handle(smlp_handle* h, const smlp_config* cfg) {
         if (!h->xbits) return set_err(h, SMLP_E_ARG, "SMLP_INPUT_BINARY needs max_batch <= 128");
         h->input_binary = true;
     }
+    {   // implicit delta_{L-1}: a dense-capped 2-output layer on top of a row-kernel hidden layer
+        const Layer& Lo = h->layers[L - 2];
+        if (h->implicit_delta && L >= 4 && Lo.narrow_bwd && Lo.dense && Lo.nout_pad == 2 && CB <= 64 &&
+            !(cfg->dropout > 0.f))
+            h->drec = zalloc<uint4>(h, (size_t)h->sizes[L - 2] + 1, &rc);
+    }
     h->d_loss = zalloc<float>(h, 1, &rc);
     if (rc) return rc;
     // --- Erdos-Renyi initialisation (R1, R2)
@@ -374,6 +380,7 @@ int sparse_mlp_create(const smlp_config* cfg, smlp_handle** out) {
         h->has_allocator = true;
     }
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+    if (const char* e = std::getenv("SMLP_IMPLICIT_DELTA")) h->implicit_delta = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_NARROW_SPARSE_BWD")) h->narrow_sparse_bwd = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMLP_SHORT_MAX_FWD")) h->short_max_fwd = std::atoi(e);
     if (const char* e = std::getenv("SMLP_SHORT_MAX_BWD")) h->short_max_bwd = std::atoi(e);
@@ -664,6 +671,7 @@ int sparse_mlp_info(smlp_handle* h, smlp_info* info) {
     }
     info->param_count = h->param_count;
     info->launches = h->launches;
+    info->implicit_delta = h->drec ? 1 : 0;
     return SMLP_OK;
 }
 

@@ -146,6 +146,12 @@ struct smlp_handle {
     uint32_t* xbits = nullptr;      // [n_1][XBITS_WORDS] bit-packed input (binary-input path) or null
     int32_t* d_nonbinary = nullptr; // set by stage_input when an input value is not 0 or 1
     float* gmirror2 = nullptr;      // [cap of W^(2)] gradient in mirror order (binary-input path)
+    // implicit delta_{L-1}: per neuron j of layer L-1 and backward chunk, the sign bits of
+    // z_{L-1}[j] over the chunk's columns and the two weights of row j of a dense-capped 2-output
+    // W^(L) -- written by the output layer's backward, gathered (16 B instead of a 4 CB-byte
+    // delta row) by the backward of W^(L-1), which recomputes delta_{L-1}[j] from it and delta_L
+    uint4* drec = nullptr;          // [n_{L-1} + 1], the last record all zero (padding slots)
+    bool implicit_delta = true;
     float* d_loss = nullptr;        // scratch loss for train_step_host
     float* x_stage[2] = {nullptr, nullptr};   // [max_batch x n_1] x2 for train_step_host (double-buffered)
     int32_t* y_stage[2] = {nullptr, nullptr};

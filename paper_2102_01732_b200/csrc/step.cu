@@ -844,6 +844,12 @@ struct BwdArgs {
     int l2hint;                      // L2 policies: gathers evict_last, streamed operands evict_first
     const int32_t* row_ptr;          // canonical row pointers (short-row streaming kernel)
     const int32_t* rowid;            // canonical row of each entry (short-row streaming kernel)
+    // implicit delta_l (l = L-1 under a dense-capped 2-output layer, RECOMP kernels): per-neuron records
+    // (sign bits of the chunk's columns, w_j0, w_j1), delta_L of the chunk [2][CB], and the negative
+    // slope of layer l's activation; zero_row then indexes the all-zero record
+    const uint4* drec;
+    const float* dL;
+    float rc_slope;
 };
 
 // Forward-layout position of a backward chunk's local column lc (CB = R CBF, R in {1, 2, 4}; the
@@ -991,9 +997,35 @@ __device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, c
     }
 }
 
-template <int CB, int NS, bool HAS_DPREV>
+// operands of the implicit delta_l (RECOMP): delta_L of the lane's 4 columns, the slope, and where
+// the lane's sign bits sit in a record
+struct Recomp {
+    float4 d0, d1;
+    float slope;
+    int sh;          // bit position of the lane's first column in its sign word
+    bool hi;         // the lane's columns are 32..63 (second sign word)
+};
+// delta_l[j] of the lane's 4 columns from neuron j's record: f'(z) (w_j0 delta_L[0] + w_j1 delta_L[1]),
+// the expression (and rounding) of bwd_narrow_rows_body; x 1 is skipped (exact)
+__device__ __forceinline__ float4 recomp_delta(const uint4& rc, const Recomp& R) {
+    const float w0 = __uint_as_float(rc.z), w1 = __uint_as_float(rc.w);
+    const uint32_t nib = ((R.hi ? rc.y : rc.x) >> R.sh) << 1;   // bits 1..4: one register-to-predicate move
+    float4 d;
+    d.x = fmaf(w1, R.d1.x, fmaf(w0, R.d0.x, 0.f));
+    d.y = fmaf(w1, R.d1.y, fmaf(w0, R.d0.y, 0.f));
+    d.z = fmaf(w1, R.d1.z, fmaf(w0, R.d0.z, 0.f));
+    d.w = fmaf(w1, R.d1.w, fmaf(w0, R.d0.w, 0.f));
+    if (!(nib & 2u)) d.x *= R.slope;
+    if (!(nib & 4u)) d.y *= R.slope;
+    if (!(nib & 8u)) d.z *= R.slope;
+    if (!(nib & 16u)) d.w *= R.slope;
+    return d;
+}
+
+template <int CB, int NS, bool HAS_DPREV, bool RECOMP>
 __device__ __forceinline__ void bwd_slots(const float* __restrict__ d_out, const int2* win, float* red,
-                                          const float4& ai, int g, int q, float4& dacc, uint64_t pg) {
+                                          const float4& ai, int g, int q, float4& dacc, uint64_t pg,
+                                          const uint4* rec, const Recomp& R) {
     using C = RowCfg<CB>;
     constexpr int P = C::P, S = C::S;
     float4 dx[NS];
@@ -1002,7 +1034,8 @@ __device__ __forceinline__ void bwd_slots(const float* __restrict__ d_out, const
     for (int u = 0; u < NS; ++u) {
         const int2 e = win[u * P + g];
         wv[u] = __int_as_float(e.y);
-        dx[u] = ldg4_hint(d_out + (int64_t)e.x * CB + q * 4, pg);
+        if constexpr (RECOMP) dx[u] = recomp_delta(rec[u * P + g], R);   // the entry's record, staged by the row loop
+        else dx[u] = ldg4_hint(d_out + (int64_t)e.x * CB + q * 4, pg);
     }
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
@@ -1013,15 +1046,23 @@ __device__ __forceinline__ void bwd_slots(const float* __restrict__ d_out, const
     }
 }
 
-template <int CB, bool HAS_DPREV>
+template <int CB, bool HAS_DPREV, bool RECOMP>
 __device__ __forceinline__ void bwd_batch(const float* __restrict__ d_out, const int2* win, float* red, int nb,
-                                          const float4& ai, int g, int q, float4& dacc, uint64_t pg) {
+                                          const float4& ai, int g, int q, float4& dacc, uint64_t pg,
+                                          const uint4* rec, const Recomp& R) {
     using C = RowCfg<CB>;
-    if constexpr (C::NQ == 1) {
-        bwd_slots<CB, C::QS, HAS_DPREV>(d_out, win, red, ai, g, q, dacc, pg);
+    if constexpr (RECOMP && C::NQ == 2) {
+        // records come from shared memory: nothing in flight to keep, so a quad at a time (half the
+        // registers of a full batch; same entries, same order)
+        bwd_slots<CB, C::QS, HAS_DPREV, RECOMP>(d_out, win, red, ai, g, q, dacc, pg, rec, R);
+        if (nb > C::QS * C::P)
+            bwd_slots<CB, C::QS, HAS_DPREV, RECOMP>(d_out, win + C::QS * C::P, red + C::QS * C::P * C::S, ai, g, q, dacc,
+                                                    pg, rec + C::QS * C::P, R);
+    } else if constexpr (C::NQ == 1) {
+        bwd_slots<CB, C::QS, HAS_DPREV, RECOMP>(d_out, win, red, ai, g, q, dacc, pg, rec, R);
     } else {
-        if (nb > C::QS * C::P) bwd_slots<CB, C::U, HAS_DPREV>(d_out, win, red, ai, g, q, dacc, pg);
-        else bwd_slots<CB, C::QS, HAS_DPREV>(d_out, win, red, ai, g, q, dacc, pg);
+        if (nb > C::QS * C::P) bwd_slots<CB, C::U, HAS_DPREV, RECOMP>(d_out, win, red, ai, g, q, dacc, pg, rec, R);
+        else bwd_slots<CB, C::QS, HAS_DPREV, RECOMP>(d_out, win, red, ai, g, q, dacc, pg, rec, R);
     }
 }
 
@@ -1033,8 +1074,13 @@ struct BwdRowsSmem {
     __align__(16) float4 ai_all[WARPS_PER_BLOCK][2][RowCfg<CB>::G];
     __align__(16) float red_all[WARPS_PER_BLOCK][RB * RowCfg<CB>::EB * RowCfg<CB>::S];
 };
-template <int CB, int CBF, bool HAS_DPREV, bool GOLD, bool DROP>
-__device__ __forceinline__ void bwd_rows_body(const BwdArgs& A, const VGrid vg, BwdRowsSmem<CB>& sm) {
+// per-warp staging of a segment's records (RECOMP kernels only)
+struct BwdRecSmem {
+    __align__(16) uint4 rec_all[WARPS_PER_BLOCK][SEG_NNZ];
+};
+template <int CB, int CBF, bool HAS_DPREV, bool GOLD, bool DROP, bool RECOMP = false>
+__device__ __forceinline__ void bwd_rows_body(const BwdArgs& A, const VGrid vg, BwdRowsSmem<CB>& sm,
+                                              BwdRecSmem* rsm = nullptr) {
     using C = RowCfg<CB>;
     constexpr int G = C::G, EB = C::EB, NW = C::NW, NB = C::NB, S = C::S, NR = C::NR;
     constexpr int RB = BwdRowsSmem<CB>::RB;
@@ -1055,6 +1101,16 @@ __device__ __forceinline__ void bwd_rows_body(const BwdArgs& A, const VGrid vg, 
     const int4 none = make_int4(0, 0, 0, -2);
     const uint64_t pg = gather_policy(A.l2hint), ps = stream_policy(A.l2hint);
     const FwdPos<CB, CBF> fp(4 * q, A.n_prev);   // the lane's 4 columns in the forward layout
+    Recomp R{};
+    uint4* rec = nullptr;
+    if constexpr (RECOMP) {
+        R.d0 = ldg4(A.dL + q * 4);
+        R.d1 = ldg4(A.dL + CB + q * 4);
+        R.slope = A.rc_slope;
+        R.sh = (4 * q) & 31;
+        R.hi = 4 * q >= 32;
+        rec = rsm->rec_all[wib];
+    }
     // window + a_{l-1}[i] of a segment into buffer b (cp.async, one segment ahead: no registers held)
     auto prefetch = [&](const int4& sg, int b) {
         window_async(win[b], A.col, A.val, sg.y, sg.z, lane, ps);
@@ -1089,6 +1145,16 @@ __device__ __forceinline__ void bwd_rows_body(const BwdArgs& A, const VGrid vg, 
         for (int r = 0; r < SEG_NNZ / 32; ++r)
             SMLP_BOUND((unsigned)win[buf][lane + 32 * r].x <= (unsigned)A.zero_row, "bwd gathered row");
         __syncwarp();
+        if constexpr (RECOMP) {
+            // the segment's records in one round trip: lane t fetches those of window entries t, t + 32
+            // (padding entries: the all-zero record) and stages them for the batches below
+            uint4 rc[NW];
+#pragma unroll
+            for (int r = 0; r < NW; ++r) rc[r] = __ldg(A.drec + win[buf][lane + 32 * r].x);
+#pragma unroll
+            for (int r = 0; r < NW; ++r) rec[lane + 32 * r] = rc[r];
+            __syncwarp();
+        }
         const float4 ai = ais[buf][q];
         float4 dacc = f4zero();
         float gsum[NW];
@@ -1100,8 +1166,8 @@ __device__ __forceinline__ void bwd_rows_body(const BwdArgs& A, const VGrid vg, 
 #pragma unroll
                 for (int b = b0; b < b0 + RB; ++b)
                     if (b * EB < n)
-                        bwd_batch<CB, HAS_DPREV>(A.d_out, win[buf] + b * EB, red + (b - b0) * EB * S, n - b * EB, ai, g, q,
-                                                 dacc, pg);
+                        bwd_batch<CB, HAS_DPREV, RECOMP>(A.d_out, win[buf] + b * EB, red + (b - b0) * EB * S, n - b * EB,
+                                                         ai, g, q, dacc, pg, rec + b * EB, R);
                 __syncwarp();
                 // window entry e = lane + 32 r of this round: fixed-order sum of its G lane partials
 #if !SMLP_EXP_NO_SDDMM
@@ -1164,6 +1230,17 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     __shared__ BwdRowsSmem<CB> sm;
     bwd_rows_body<CB, CBF, HAS_DPREV, GOLD, DROP>(A, hw_grid(), sm);
 }
+// the same with the implicit delta_l (layer L-1 under a dense-capped 2-output layer, no dropout)
+#ifndef SMLP_RECOMP_MINB
+#define SMLP_RECOMP_MINB 4
+#endif
+template <int CB, int CBF, bool GOLD>
+__global__ void __launch_bounds__(256, SMLP_RECOMP_MINB) bwd_rows_recomp_kernel(BwdArgs A) {
+    SMLP_PDL_ENTRY();
+    __shared__ BwdRowsSmem<CB> sm;
+    __shared__ BwdRecSmem rsm;
+    bwd_rows_body<CB, CBF, true, GOLD, false, true>(A, hw_grid(), sm, &rsm);
+}
 
 // ------------------------------------------------------------------------------------------
 // narrow output layer (l = L, n_L <= NARROW_MAX): both passes walk the canonical CSR rows i of
@@ -1199,6 +1276,7 @@ struct NarrowArgs {
     int n_out;
     int ncols;                // fwd: columns present in this launch (<= its width)
     const LayerMeta* meta;    // device nnz: complete layer (nnz = n_in n_out) -> row i = [i n_out, (i+1) n_out)
+    uint4* drec;              // bwd, 2-output dense-capped layer: per-row record for the implicit delta_{L-1} (or null)
     float neg_slope_prev;
     float keep_scale_prev;
     int dropout_prev;
@@ -1509,6 +1587,7 @@ __device__ __forceinline__ void bwd_narrow_rows_body(const NarrowArgs& A, const 
         }
         uint4 zb = make_uint4(0, 0, 0, 0), kb = make_uint4(FULL, FULL, FULL, FULL);
         float bsum = 0.f;
+        uint32_t pw0 = 0u, pw1 = 0u;              // sign bits of the chunk's columns 0..31 / 32..63 (implicit delta record)
         for (int sl = 0; sl < NS; ++sl) {
             // a slice lies inside one forward chunk (CBF >= min(CB, 32) = CS): its rows and masks
             const FwdPos<CB, CBF> fp(sl * CS, A.n_in);
@@ -1546,6 +1625,11 @@ __device__ __forceinline__ void bwd_narrow_rows_body(const NarrowArgs& A, const 
                     const float o = A.dropout_prev ? (keep ? x * A.keep_scale_prev : 0.f) : x;
                     bsum += o;
                     tl[lane * TS + c] = o;
+                    if constexpr (NOUT == 2 && CB <= 64) {
+                        const uint32_t bit = (pos ? 1u : 0u) << (b & 31);
+                        if (b & 32) pw1 |= bit;
+                        else pw0 |= bit;
+                    }
                 }
             }
             __syncwarp();
@@ -1561,6 +1645,11 @@ __device__ __forceinline__ void bwd_narrow_rows_body(const NarrowArgs& A, const 
             }
         }
         if (!valid) continue;
+        if constexpr (NOUT == 2 && CB <= 64) {
+            // implicit delta_{L-1}: the backward of W^(L-1) recomputes delta_{L-1}[i] of this chunk from
+            // (sign bits, w_i0, w_i1) and delta_L with the very expression above
+            if (A.drec) A.drec[i] = make_uint4(pw0, pw1, __float_as_uint(w[0]), __float_as_uint(w[1]));
+        }
 #pragma unroll
         for (int jj = 0; jj < NOUT; ++jj) {       // Eq. 1 / gradient accumulation of the row's entries
             if (jj < len) {
@@ -2474,6 +2563,21 @@ int launch_bwd(smlp_handle* h, const BwdArgs& A, const Layer& L, bool has_dprev)
 #undef SMLP_BWD_SHORT
         }
     }
+    if constexpr (CB <= 64) {
+        if (A.drec) {   // implicit delta_l: records instead of delta rows (has_dprev, no dropout: api.cu)
+            if (gold)
+                launch_pdl(h->pdl, bwd_rows_recomp_kernel<CB, CBF, true>, rows_grid(h, bwd_rows_recomp_kernel<CB, CBF, true>, L.bseg_cap), WARPS_PER_BLOCK * 32, h->stream, A);
+            else
+                launch_pdl(h->pdl, bwd_rows_recomp_kernel<CB, CBF, false>, rows_grid(h, bwd_rows_recomp_kernel<CB, CBF, false>, L.bseg_cap), WARPS_PER_BLOCK * 32, h->stream, A);
+            SMLP_CK_LAUNCH(h, "bwd_rows_recomp_kernel");
+            if (L.bslot_cap > 0) {
+                const int g2 = persistent_grid(h, std::max<int64_t>(1, L.bslot_cap / 2), P);
+                launch_pdl(h->pdl, bwd_finish_kernel<CB, CBF>, g2, WARPS_PER_BLOCK * 32, h->stream, A);
+                SMLP_CK_LAUNCH(h, "bwd_finish_kernel");
+            }
+            return SMLP_OK;
+        }
+    }
     const int mode = (has_dprev ? 4 : 0) | (gold ? 2 : 0) | (drop ? 1 : 0);
 #define SMLP_BWD_ROWS(HD, GO, DR)                                                                             \
 case (HD ? 4 : 0) | (GO ? 2 : 0) | (DR ? 1 : 0):                                                            \
@@ -2918,6 +3022,7 @@ static int run_backward_phases(smlp_handle* h, const int32_t* labels, const int3
                 A.dropout_prev = dropout_prev;
                 A.first = first;
                 A.last = last;
+                A.drec = (l == L && has_dprev) ? h->drec : nullptr;
                 prof_start(h, K_BWD, l, 12.0 * nnz / nchunks + act_bytes, (has_dprev ? 4.0 : 2.0) * nnz * Bc);
                 SMLP_TRY(dispatch_narrow(h, A, Ly, false, CB));
                 prof_stop(h);
@@ -2962,7 +3067,16 @@ static int run_backward_phases(smlp_handle* h, const int32_t* labels, const int3
             }
             A.zero_row = (int)((int64_t)(h->max_chunks - c) * nout);
             A.l2hint = 1;
-            prof_start(h, K_BWD, l, 12.0 * nnz / nchunks + act_bytes, (has_dprev ? 4.0 : 2.0) * nnz * Bc);
+            if (l == L - 1 && h->drec && has_dprev && !dropout_prev && !recorder(h)) {
+                // implicit delta_{L-1}: gather the records the output layer's backward just wrote
+                A.drec = h->drec;
+                A.dL = h->delta[L] + (int64_t)c * h->sizes[L - 1] * CB;
+                A.rc_slope = neg_slope_of(h, l);
+                A.zero_row = (int)nout;
+            }
+            // (implicit delta_l: 16-B records instead of the delta_l rows)
+            const double dl_bytes = A.drec ? 4.0 * Bc * (double)nout - 16.0 * (double)nout : 0.0;
+            prof_start(h, K_BWD, l, 12.0 * nnz / nchunks + act_bytes - dl_bytes, (has_dprev ? 4.0 : 2.0) * nnz * Bc);
             SMLP_TRY(dispatch_bwd(h, A, Ly, has_dprev));
             prof_stop(h);
             if (last) SMLP_TRY(layer_done(h, l));

@@ -82,7 +82,7 @@ class smlp_info(C.Structure):
                 ("nnz", C.c_int64 * SMLP_MAX_LAYERS), ("cap", C.c_int64 * SMLP_MAX_LAYERS),
                 ("dense_capped", C.c_int32 * SMLP_MAX_LAYERS), ("val_offset", C.c_int64 * SMLP_MAX_LAYERS),
                 ("bias_offset", C.c_int64 * SMLP_MAX_LAYERS), ("param_count", C.c_int64),
-                ("launches", C.c_int64), ("fwd_chunk_batch", C.c_int32)]
+                ("launches", C.c_int64), ("fwd_chunk_batch", C.c_int32), ("implicit_delta", C.c_int32)]
 
 
 _lib = None
@@ -384,7 +384,7 @@ class SparseMLP:
                 "cap": list(inf.cap[:L]), "dense_capped": list(inf.dense_capped[:L]),
                 "val_offset": list(inf.val_offset[:L]), "bias_offset": list(inf.bias_offset[:L]),
                 "param_count": inf.param_count, "launches": inf.launches,
-                "fwd_chunk_batch": inf.fwd_chunk_batch}
+                "fwd_chunk_batch": inf.fwd_chunk_batch, "implicit_delta": inf.implicit_delta}
 
     def sparse_mlp_export_layer(self, l: int) -> dict:
         nnz = self.sparse_mlp_info()["nnz"][l - 1]

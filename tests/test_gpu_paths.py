@@ -15,7 +15,8 @@ import pytest
 from oracle import model as M
 from oracle.compare import rel_err
 from synth import get_config, make_dataset
-from tests.gpu_helpers import TOL, assert_topology_equal, assert_values_close, check_and_resync, pair, to_dev
+from tests.gpu_helpers import (TOL, assert_topology_equal, assert_values_close, check_and_resync,
+                               load_oracle_state_into_gpu, pair, to_dev)
 
 pytestmark = pytest.mark.gpu
 
@@ -653,3 +654,58 @@ def test_c5_full_size_evolve_and_prune_bitexact():
     torch.cuda.synchronize()
     assert list(pruned_g) == list(pruned_o) and list(removed_g) == list(removed_o)
     assert_topology_equal(g, st, "C5 prune")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,chunk,fchunk", [(128, 64, 32), (100, 64, None), (33, 32, None), (128, 32, None), (7, 16, None)])
+def test_implicit_delta_matches_gathered_and_oracle(B, chunk, fchunk, monkeypatch):
+    """Layer L-1 under a dense-capped 2-output layer (C1, like C4 / C5 / T1-T5): the backward of
+    W^(L-1) recomputes delta_{L-1}[j] from 16-B per-neuron records (sign bits, w_j0, w_j1) and
+    delta_L instead of gathering its rows.  Bit-identical to the gathering kernels
+    (SMLP_IMPLICIT_DELTA=0) over several fused steps and a prune + evolve, and within 1e-4 of the
+    oracle (P:596-599 for the step; Eq. 3's derivative P:106-112 is what the records carry)."""
+    torch = _torch()
+    from paper_2102_01732_b200 import SGD
+    from tests.test_gpu_parity import _batch     # a kink-free seeded batch (R32)
+    cfg = get_config("C1", batch=B)
+    if fchunk:
+        monkeypatch.setenv("SMLP_FWD_CB", str(fchunk))
+    g1, st = pair(cfg, max_batch=128, chunk_batch=chunk)
+    monkeypatch.setenv("SMLP_IMPLICIT_DELTA", "0")
+    g0, _ = pair(cfg, max_batch=128, chunk_batch=chunk)
+    assert g1.info()["implicit_delta"] == 1 and g0.info()["implicit_delta"] == 0
+    assert g1.info()["dense_capped"][-1] == 1
+    sgd = SGD(cfg.lr, cfg.momentum, cfg.weight_decay)
+    L = cfg.n_layers
+    for step in range(3):
+        x, y, tr = _batch(cfg, st, B=B, step=step)
+        for g in (g0, g1):
+            g.forward(to_dev(x), train=True, step=step)
+            g.backward(to_dev(y))
+        torch.cuda.synchronize()
+        for l in range(2, L + 1):
+            for kind in (2, 3):       # weight and bias gradients: the same bits
+                a, b = g0.sparse_mlp_export_trace(kind, l), g1.sparse_mlp_export_trace(kind, l)
+                assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (step, kind, l)
+        gr = M.backward(st, tr, y)
+        for Ly in st.layers:
+            assert rel_err(g1.sparse_mlp_export_trace(2, Ly.l), gr.g[Ly.l - 2], gr.gmag[Ly.l - 2]) <= TOL, ("g", Ly.l)
+            assert rel_err(g1.sparse_mlp_export_trace(3, Ly.l), gr.gb[Ly.l - 2], gr.gbmag[Ly.l - 2]) <= TOL, ("gb", Ly.l)
+        for g in (g0, g1):
+            g.step(sgd)
+        M.step(st, gr, cfg.lr, cfg.momentum, cfg.weight_decay)
+        torch.cuda.synchronize()
+        for l in range(2, L + 1):     # the updated weights and momenta: the same bits
+            a, b = g0.export_layer(l), g1.export_layer(l)
+            assert np.array_equal(a["w"].view(np.uint32), b["w"].view(np.uint32)), (step, "w", l)
+            assert np.array_equal(a["v"].view(np.uint32), b["v"].view(np.uint32)), (step, "v", l)
+        check_and_resync(g1, st)      # within 1e-4 of the oracle, then both restart from its state
+        load_oracle_state_into_gpu(g0, st)
+        if step == 0:     # pruned hidden neurons leave EMPTY rows in the dense-capped output layer
+            import oracle.topology as T
+            for g in (g0, g1):
+                g.prune_neurons(0.3)
+                g.evolve_topology(cfg.zeta, 0)
+            T.prune(st, 0.3)
+            T.evolve(st, cfg.zeta, 0)
+            assert_topology_equal(g1, st, "after prune + evolve")
