@@ -12,6 +12,9 @@ lines = [l for l in open(sys.argv[1]) if l.startswith('"')]
 rows = [r for r in csv.DictReader(lines) if r["Metric Name"] == "gpu__time_duration.sum"]
 starts = [i for i, r in enumerate(rows) if "stage_input_kernel" in r["Kernel Name"]]
 step = rows[starts[-1]:]
+if len(starts) >= 2 and len(step) < starts[-1] - starts[-2]:
+    # the capture's launch limit cut the last step short: take the last complete one
+    step = rows[starts[-2]:starts[-1]]
 agg = collections.OrderedDict()
 for r in step:
     name = re.sub(r"smlp::<unnamed>::|\(.*$", "", r["Kernel Name"].replace("(anonymous namespace)::", ""))
