@@ -997,9 +997,6 @@ __device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, c
     }
 }
 
-#ifndef SMLP_RECOMP_FFMA2
-#define SMLP_RECOMP_FFMA2 0
-#endif
 // operands of the implicit delta_l (RECOMP): delta_L of the lane's 4 columns, the slope, and where
 // the lane's sign bits sit in a record
 struct Recomp {
@@ -1013,19 +1010,11 @@ struct Recomp {
 __device__ __forceinline__ float4 recomp_delta(const uint4& rc, const Recomp& R) {
     const float w0 = __uint_as_float(rc.z), w1 = __uint_as_float(rc.w);
     const uint32_t nib = ((R.hi ? rc.y : rc.x) >> R.sh) << 1;   // bits 1..4: one register-to-predicate move
-#if SMLP_RECOMP_FFMA2
     // fmaf(w1, d1, fmaf(w0, d0, 0)) per column, two columns per FFMA2 (bit for bit two fmaf)
     const float2 z2 = make_float2(0.f, 0.f), w00 = make_float2(w0, w0), w11 = make_float2(w1, w1);
     const float2 lo = ffma2(w11, make_float2(R.d1.x, R.d1.y), ffma2(w00, make_float2(R.d0.x, R.d0.y), z2));
     const float2 hh = ffma2(w11, make_float2(R.d1.z, R.d1.w), ffma2(w00, make_float2(R.d0.z, R.d0.w), z2));
     float4 d = make_float4(lo.x, lo.y, hh.x, hh.y);
-#else
-    float4 d;
-    d.x = fmaf(w1, R.d1.x, fmaf(w0, R.d0.x, 0.f));
-    d.y = fmaf(w1, R.d1.y, fmaf(w0, R.d0.y, 0.f));
-    d.z = fmaf(w1, R.d1.z, fmaf(w0, R.d0.z, 0.f));
-    d.w = fmaf(w1, R.d1.w, fmaf(w0, R.d0.w, 0.f));
-#endif
     if (!(nib & 2u)) d.x *= R.slope;
     if (!(nib & 4u)) d.y *= R.slope;
     if (!(nib & 8u)) d.z *= R.slope;
@@ -1242,11 +1231,8 @@ __global__ void __launch_bounds__(256, 4) bwd_rows_kernel(BwdArgs A) {
     bwd_rows_body<CB, CBF, HAS_DPREV, GOLD, DROP>(A, hw_grid(), sm);
 }
 // the same with the implicit delta_l (layer L-1 under a dense-capped 2-output layer, no dropout)
-#ifndef SMLP_RECOMP_MINB
-#define SMLP_RECOMP_MINB 4
-#endif
 template <int CB, int CBF, bool GOLD>
-__global__ void __launch_bounds__(256, SMLP_RECOMP_MINB) bwd_rows_recomp_kernel(BwdArgs A) {
+__global__ void __launch_bounds__(256, 4) bwd_rows_recomp_kernel(BwdArgs A) {
     SMLP_PDL_ENTRY();
     __shared__ BwdRowsSmem<CB> sm;
     __shared__ BwdRecSmem rsm;
