@@ -981,22 +981,10 @@ __device__ __forceinline__ void bwd_rows_epilogue(const BwdArgs& A, int64_t i, c
     if constexpr (P == 1) {   // the lane holds its 4 columns: one 16-B store
         st4(A.d_prev + i * CB + q * 4, make_float4(out[0], out[1], out[2], out[3]));
     } else {
-#if SMLP_EXP_DPREV_LAST
-        if (A.drec) {   // the recompute kernel leaves the L2 to delta_{l-1}: keep it for the next layer's gathers
-            const uint64_t pl = policy_evict_last();
 #pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                const int c = r * P + g;
-                if (c < 4) st_hint(A.d_prev + i * CB + q * 4 + c, out[r], pl);
-            }
-        } else
-#endif
-        {
-#pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                const int c = r * P + g;
-                if (c < 4) A.d_prev[i * CB + q * 4 + c] = out[r];
-            }
+        for (int r = 0; r < NR; ++r) {
+            const int c = r * P + g;
+            if (c < 4) A.d_prev[i * CB + q * 4 + c] = out[r];
         }
     }
 #pragma unroll
@@ -1021,12 +1009,9 @@ struct Recomp {
 // the expression (and rounding) of bwd_narrow_rows_body; x 1 is skipped (exact)
 __device__ __forceinline__ float4 recomp_delta(const uint4& rc, const Recomp& R) {
     const float w0 = __uint_as_float(rc.z), w1 = __uint_as_float(rc.w);
-#if SMLP_EXP_ROT
+    // the lane's 4 sign bits rotated onto bits 1..4: one register-to-predicate move sets all four
     const uint32_t sw = R.hi ? rc.y : rc.x;
-    const uint32_t nib = __funnelshift_r(sw, sw, (R.sh + 31) & 31);   // rotate: the lane's bits on 1..4
-#else
-    const uint32_t nib = ((R.hi ? rc.y : rc.x) >> R.sh) << 1;   // bits 1..4: one register-to-predicate move
-#endif
+    const uint32_t nib = __funnelshift_r(sw, sw, (R.sh + 31) & 31);
     // fmaf(w1, d1, fmaf(w0, d0, 0)) per column, two columns per FFMA2 (bit for bit two fmaf)
     const float2 z2 = make_float2(0.f, 0.f), w00 = make_float2(w0, w0), w11 = make_float2(w1, w1);
     const float2 lo = ffma2(w11, make_float2(R.d1.x, R.d1.y), ffma2(w00, make_float2(R.d0.x, R.d0.y), z2));
