@@ -83,6 +83,7 @@ struct Layer {
     int ngrid = 0;          // CTAs of the narrow forward
     float* nws = nullptr;   // [ngrid][nout_pad][CB] CTA partial logits
     bool split = false;     // the last backward chunk's gradient is in grad2 (the Eq. 1 pass adds it)
+    bool updated_early = false;  // Eq. 1 + mirror refresh already issued on the side stream by this backward (run_step skips it)
     bool narrow_bwd = false; // the backward of a narrow layer streams its rows too (dense-capped only by default)
     // biases of neuron layer l live in param/mom/grad at bias_off
     float* bias = nullptr;

@@ -2959,11 +2959,12 @@ static int layer_done(smlp_handle* h, int l) {
 }
 
 static int run_backward_phases(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss,
-                               bool split_last) {
+                               bool split_last, const smlp_sgd* early = nullptr) {
     const int CB = h->CB;
     const int B = h->trace_B;
     const int nchunks = (B + CB - 1) / CB;
     const int L = h->L;
+    for (auto& Ly : h->layers) Ly.updated_early = false;
     {
         Layer& Lo = h->layers[L - 2];
         SoftmaxArgs S{};
@@ -3081,6 +3082,28 @@ static int run_backward_phases(smlp_handle* h, const int32_t* labels, const int3
             if (last) SMLP_TRY(layer_done(h, l));
         }
     }
+#if SMLP_EXP_EARLY_UPDATE
+    if (early && h->xbits && !recorder(h) && h->param_count > SMALL_MODEL_PARAMS) {
+        // fused step of a large model with the bit path: the gradients of W^(3..L) are final, and what
+        // is left of the backward (the set-bit walk of W^(2), bound by latency and instruction issue)
+        // leaves the memory system idle -- so Eq. 1 and the mirror refresh of those layers (streaming
+        // and gather passes) run on the side stream under it; run_step joins them
+        SMLP_TRY(ensure_aux(h));
+        SMLP_CK(h, cudaEventRecord(h->aux_ev[0], h->stream));
+        SMLP_CK(h, cudaStreamWaitEvent(h->aux_stream, h->aux_ev[0], 0));
+        for (auto& Ly : h->layers) {
+            if (Ly.l < 3) continue;
+            const bool g2 = Ly.split;
+            Ly.split = false;
+            SMLP_TRY(launch_update(h, h->aux_stream, Ly.val_off, Ly.val_off + Ly.cap, true, early, g2));
+            Ly.updated_early = true;
+            if (Ly.narrow) continue;
+            mirror_values_kernel<<<launch_grid(h, (Ly.cap + 3) / 4, 256), 256, 0, h->aux_stream>>>(Ly.val, Ly.mperm, Ly.meta,
+                                                                                         Ly.mval);
+            SMLP_CK_LAUNCH(h, "mirror_values_kernel");
+        }
+    }
+#endif
     if (h->xbits) {   // binary-input layer 2 (returns at once if not binary)
         Layer& L2 = h->layers[0];
         BitsArgs A = bits_args(h, L2, nchunks);
@@ -3147,6 +3170,11 @@ int run_step(smlp_handle* h, const smlp_sgd* sgd) {
     prof_start(h, K_SGD, 0, 20.0 * (double)n, 0.0);
     bool side = false;
     for (auto& Ly : h->layers) {
+        if (Ly.updated_early) {   // issued on the side stream by the backward (under the bit kernels)
+            Ly.updated_early = false;
+            side = true;
+            continue;
+        }
         const bool g2 = Ly.split;
         Ly.split = false;
         SMLP_TRY(launch_update(h, h->stream, Ly.val_off, Ly.val_off + Ly.cap, true, sgd, g2));
@@ -3258,7 +3286,7 @@ int run_forward(smlp_handle* h, const float* x, const int32_t* x_idx, int B, boo
 // backward (a4-a5) and, when fused, the Eq. 1 pass + mirror refresh (a6) of the same call
 int run_backward_step(smlp_handle* h, const int32_t* labels, const int32_t* y_idx, float* loss, const smlp_sgd* fused) {
     auto body = [&]() -> int {
-        SMLP_TRY(run_backward_phases(h, labels, y_idx, loss, fused != nullptr));
+        SMLP_TRY(run_backward_phases(h, labels, y_idx, loss, fused != nullptr, fused));
         if (fused) SMLP_TRY(run_step(h, fused));
         return SMLP_OK;
     };
