@@ -3082,7 +3082,6 @@ static int run_backward_phases(smlp_handle* h, const int32_t* labels, const int3
             if (last) SMLP_TRY(layer_done(h, l));
         }
     }
-#if SMLP_EXP_EARLY_UPDATE
     if (early && h->xbits && !recorder(h) && h->param_count > SMALL_MODEL_PARAMS) {
         // fused step of a large model with the bit path: the gradients of W^(3..L) are final, and what
         // is left of the backward (the set-bit walk of W^(2), bound by latency and instruction issue)
@@ -3103,7 +3102,6 @@ static int run_backward_phases(smlp_handle* h, const int32_t* labels, const int3
             SMLP_CK_LAUNCH(h, "mirror_values_kernel");
         }
     }
-#endif
     if (h->xbits) {   // binary-input layer 2 (returns at once if not binary)
         Layer& L2 = h->layers[0];
         BitsArgs A = bits_args(h, L2, nchunks);
